@@ -1,0 +1,198 @@
+/*
+ * vlut.h -- C ABI of libvlut.so: the B200 (sm_100a) Vec-LUT ternary mpGeMM.
+ *
+ * Method: Vec-LUT, arXiv 2512.06443.  "P:n" cites /root/reference/PAPER.md
+ * line n (LaTeX source), "S:n" SPEC.md line n.  The notation follows the
+ * paper's Table 2: W x A = O, W in {-1,0,1}^{M x K} (ternary
+ * weights), A in int8^{K x N} (activations, token axis N contiguous,
+ * P:430-434), O in R^{M x N} (output, token axis contiguous).  g in {4,5} is
+ * the weight group size; a group of g trits is one base-3 byte index
+ * into a 3^g-row table of the group's signed
+ * activation sums (Eq. 1).
+ *
+ * Conventions for every entry point:
+ *   - Plain C types only.  "dev" pointers are CUDA device pointers, "host"
+ *     pointers are ordinary host memory.  `stream` is a cudaStream_t passed
+ *     as void* (0 = legacy default stream).
+ *   - The caller owns every buffer.  The library never allocates or frees
+ *     device memory; it keeps no global mutable state except a thread-local
+ *     error string and a per-device property/attribute cache.
+ *   - Arguments are validated on the host before anything is launched.  On
+ *     failure nothing is launched, a status != VLUT_OK is returned and
+ *     vlut_last_error() describes it.  Nothing aborts or throws across the ABI.
+ *   - Work is enqueued on `stream` and is asynchronous: a device fault
+ *     surfaces at the caller's next synchronisation, not as a return value.
+ *   - Results are deterministic and bit-identical for every launch plan
+ *     (integer accumulation is exact and associative; fp32 epilogue op order
+ *     is fixed).
+ *   - Thread-safe and reentrant for distinct output buffers.
+ */
+#ifndef VLUT_H_
+#define VLUT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  VLUT_OK = 0,
+  VLUT_ERR_INVALID_ARGUMENT = 1, /* null pointer, negative size, bad g     */
+  VLUT_ERR_INVALID_TRIT = 2,     /* a weight outside {-1,0,1}      */
+  VLUT_ERR_SHAPE = 3,            /* g does not divide K, M/K/N mismatch with the descriptor, size overflow */
+  VLUT_ERR_BUFFER_TOO_SMALL = 4, /* payload buffer smaller than vlut_packed_bytes() */
+  VLUT_ERR_MISALIGNED = 5,       /* a device pointer not aligned as documented */
+  VLUT_ERR_CORRUPT_DESCRIPTOR = 6, /* bad magic/version/fields in vlut_packed_weights */
+  VLUT_ERR_CUDA = 7,             /* a CUDA runtime call or launch failed   */
+  VLUT_ERR_UNSUPPORTED = 8       /* a plan the device cannot run (e.g. cluster size) */
+} vlut_status;
+
+#define VLUT_MAGIC 0x31544C56u /* "VLT1" little-endian */
+#define VLUT_VERSION 1u
+#define VLUT_KG_TILE 16 /* groups per packed K-tile (one 16-byte index vector per row) */
+#define VLUT_M_TILE 32  /* row padding granularity of the packed payload */
+
+/*
+ * Packed ternary weights (a1; P:284 offline stage, P:436-441 tile-contiguous
+ * layout).  A POD value the caller keeps next to the payload buffer.
+ *
+ * Payload layout (device, `payload_bytes` bytes, 16-byte aligned):
+ *   byte payload[kt][m][j]   kt in [0, kg_tiles), m in [0, m_pad), j in [0,16)
+ *   = index of group (kt*16 + j) of weight row m, where group k of row m
+ *     covers features k*g .. k*g+g-1 (reading c4) and
+ *     index = sum_{r<g} (W[m][k*g+r] + 1) * 3^r  (Alg. 1 GetSign, P:382;
+ *     least-significant trit first, reading c1).
+ *   Rows m >= M and groups k >= K/g hold the all-zero index (3^g-1)/2
+ *   (40 for g=4, 121 for g=5) and contribute exactly 0.
+ * The K-tile index is outermost, matching the K->M loop order of Alg. 1
+ * (P:441); within a tile the 16 index bytes of one row are contiguous so one
+ * 16-byte load fetches a row's indices for 16 groups, and a CTA's rows of one
+ * K-tile form one contiguous, coalesced block.
+ */
+typedef struct {
+  uint32_t magic;          /* VLUT_MAGIC                                  */
+  uint32_t version;        /* VLUT_VERSION                                */
+  int32_t M, K, g;         /* logical shape; g in {4,5}                   */
+  int32_t m_pad;           /* M rounded up to VLUT_M_TILE                 */
+  int32_t kg_tiles;        /* ceil((K/g) / VLUT_KG_TILE)                  */
+  int32_t m_tile, kg_tile; /* VLUT_M_TILE, VLUT_KG_TILE                   */
+  int32_t reserved;
+  int64_t payload_bytes;   /* kg_tiles * m_pad * 16                        */
+  const void* payload;     /* device pointer (caller-owned)               */
+} vlut_packed_weights;
+
+/*
+ * Launch plan of the fused mpGeMM kernel (K1).  m_cta = 32*warps output rows
+ * per CTA, n_cta = 64 tokens per CTA, `splits` CTAs of one thread-block
+ * cluster share an (M-block, N-tile) and split its K range; their int32
+ * partials are reduced through distributed shared memory (a5).
+ */
+typedef struct {
+  int32_t warps;        /* 8, 12 or 16                                      */
+  int32_t splits;       /* 1, 2 or 4 (cluster size along K)                  */
+  int32_t m_cta;        /* 32 * warps                                       */
+  int32_t n_cta;        /* 64                                               */
+  int32_t grid_ctas;    /* total CTAs launched                              */
+  int32_t smem_bytes;   /* dynamic shared memory per CTA                    */
+} vlut_launch_plan;
+
+/* Payload bytes for an M x K ternary matrix packed with group size g
+ * (kg_tiles * m_pad * 16).  Returns 0 if the arguments are invalid (M<=0,
+ * K<=0, g not in {4,5}, g does not divide K) or the size overflows. */
+size_t vlut_packed_bytes(int M, int K, int g);
+
+/*
+ * Pack ternary weights (a1, offline).
+ *   w_trits_host : host, int8 [M][K] row-major, values in {-1,0,1}.
+ *   payload_dev  : device, >= vlut_packed_bytes(M,K,g) bytes, 16-B aligned.
+ *   desc_out     : host, filled on success (payload = payload_dev).
+ * Validates every trit (VLUT_ERR_INVALID_TRIT, nothing written), packs on the
+ * host and copies to the device with cudaMemcpyAsync on `stream`, then
+ * synchronises `stream` (the host staging buffer is freed before return).
+ */
+vlut_status vlut_pack_weights(const int8_t* w_trits_host, int M, int K, int g,
+                              void* payload_dev, size_t payload_bytes,
+                              vlut_packed_weights* desc_out, void* stream);
+
+/*
+ * Same packing, done on the device from device-resident trits (for large
+ * weights; one launch, asynchronous).  Invalid trits are not detected here
+ * beyond being mapped into range; use vlut_pack_weights for validation.
+ *   w_trits_dev : device int8 [M][K].   Other arguments as above.
+ */
+vlut_status vlut_pack_weights_device(const int8_t* w_trits_dev, int M, int K, int g,
+                                     void* payload_dev, size_t payload_bytes,
+                                     vlut_packed_weights* desc_out, void* stream);
+
+/* Inverse of the packing, on the host (tests, checkpoint export):
+ * payload_host (kg_tiles*m_pad*16 bytes, as described by desc) -> int8 trits
+ * [M][K].  Returns VLUT_ERR_INVALID_TRIT on a byte >= 3^g (corrupt payload,
+ * S:164).  Padding bytes are not inspected. */
+vlut_status vlut_unpack_weights_host(const vlut_packed_weights* desc,
+                                     const uint8_t* payload_host, int8_t* w_trits_host);
+
+/* The heuristic launch plan for (M, K, N, g) on the current device. */
+vlut_status vlut_plan(int M, int K, int N, int g, vlut_launch_plan* plan);
+
+/*
+ * Vec-LUT mpGeMM with fp32 dequant epilogue (a2-a6):
+ *   out[m][n] = fl( (float)acc[m][n] * fl(a_scale[n] * w_scale) )
+ *   acc[m][n] = sum_k W[m][k] * A[k][n]   (exact int32; Alg. 1 + Eq. 2,
+ *              P:326-351; tables per Eq. 1, topological order
+ *              P:503-513; INT16->INT32 hierarchical accumulation P:483-491)
+ *   W       : packed weights (desc->M == M, desc->K == K).
+ *   A       : device int8 [K][N], token axis contiguous; any
+ *             int8 value including -128.
+ *   a_scale : device fp32 [N], per-token activation scale.
+ *   w_scale : per-tensor weight scale (reading c7).
+ *   out     : device fp32 [M][N], token axis contiguous.
+ * M == 0 or N == 0 is a no-op returning VLUT_OK.  A, out need 4-byte
+ * alignment; 16-byte alignment and N % 16 == 0 take the vectorised path.
+ */
+vlut_status vlut_mpgemm(const vlut_packed_weights* W, const int8_t* A,
+                        const float* a_scale, float w_scale, float* out,
+                        int M, int K, int N, void* stream);
+
+/* As vlut_mpgemm with an explicit plan (NULL = heuristic).  Any valid plan
+ * gives bit-identical results. */
+vlut_status vlut_mpgemm_ex(const vlut_packed_weights* W, const int8_t* A,
+                           const float* a_scale, float w_scale, float* out,
+                           int M, int K, int N, const vlut_launch_plan* plan,
+                           void* stream);
+
+/* Raw int32 accumulators, no scales (bit-exact test hook):
+ *   acc_out : device int32 [M][N].  Other arguments as vlut_mpgemm_ex. */
+vlut_status vlut_mpgemm_acc(const vlut_packed_weights* W, const int8_t* A,
+                            int32_t* acc_out, int M, int K, int N,
+                            const vlut_launch_plan* plan, void* stream);
+
+/*
+ * Per-token absmax int8 quantizer (a7; w1.6A8 named at P:102; formula
+ * S:339-347, reading c8), IEEE single precision throughout:
+ *   x'[k][n] = x[k][n] * (y ? y[k][n] : 1)      (fp32 multiply, config 5's
+ *                                                gate (.) up glue, c14)
+ *   amax_n = max_k |x'[k][n]|, s_n = amax_n / 127 (1 if amax_n == 0)
+ *   q[k][n] = clamp(roundf(x'[k][n] / s_n), -127, 127)
+ *   x, y : device fp32 [K][N] (y may be NULL);  q : device int8 [K][N];
+ *   scale : device fp32 [N].
+ * Non-finite inputs are not detected (the caller's responsibility).
+ */
+vlut_status vlut_quantize(const float* x, const float* y, int K, int N,
+                          int8_t* q, float* scale, void* stream);
+
+/* Number of kernel launches one vlut_mpgemm/vlut_mpgemm_acc call enqueues
+ * (1: the whole path, split-K reduction included, is one cluster launch). */
+int vlut_launches_per_mpgemm(void);
+
+/* Message for the last failing call on this thread ("" if none). */
+const char* vlut_last_error(void);
+
+/* Library version string. */
+const char* vlut_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VLUT_H_ */

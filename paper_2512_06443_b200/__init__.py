@@ -1,1 +1,287 @@
-"""placeholder"""
+"""paper_2512_06443_b200 -- B200-native Vec-LUT ternary mpGeMM (arXiv 2512.06443).
+
+Thin Python binding over the C ABI of ``libvlut.so`` (``include/vlut.h``):
+argument marshalling only.  Every step of the hot path (table build, lookup,
+accumulation, split-K reduction, dequant, quantization, packing on device)
+runs in the CUDA kernels of ``csrc/``; PyTorch is used only for device memory,
+streams and ``torch.distributed``.  There is no CPU fallback: if the library
+is missing or no CUDA device is present, calls raise.
+
+The binding keeps the C names: ``packed_bytes``, ``pack_weights``,
+``pack_weights_device``, ``mpgemm``, ``mpgemm_ex``, ``mpgemm_acc``,
+``quantize``, ``plan``, ``last_error``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+__all__ = [
+    "VlutError", "PackedWeights", "LaunchPlan", "lib", "lib_path", "packed_bytes",
+    "pack_weights", "pack_weights_device", "unpack_weights_host", "plan", "mpgemm",
+    "mpgemm_ex", "mpgemm_acc", "quantize", "last_error", "EXPORTS",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libvlut.so")
+
+STATUS = {
+    0: "VLUT_OK", 1: "VLUT_ERR_INVALID_ARGUMENT", 2: "VLUT_ERR_INVALID_TRIT",
+    3: "VLUT_ERR_SHAPE", 4: "VLUT_ERR_BUFFER_TOO_SMALL", 5: "VLUT_ERR_MISALIGNED",
+    6: "VLUT_ERR_CORRUPT_DESCRIPTOR", 7: "VLUT_ERR_CUDA", 8: "VLUT_ERR_UNSUPPORTED",
+}
+VLUT_MAGIC = 0x31544C56
+VLUT_VERSION = 1
+
+
+class VlutError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class _Desc(ctypes.Structure):
+    _fields_ = [
+        ("magic", ctypes.c_uint32), ("version", ctypes.c_uint32),
+        ("M", ctypes.c_int32), ("K", ctypes.c_int32), ("g", ctypes.c_int32),
+        ("m_pad", ctypes.c_int32), ("kg_tiles", ctypes.c_int32),
+        ("m_tile", ctypes.c_int32), ("kg_tile", ctypes.c_int32),
+        ("reserved", ctypes.c_int32), ("payload_bytes", ctypes.c_int64),
+        ("payload", ctypes.c_void_p),
+    ]
+
+
+class _Plan(ctypes.Structure):
+    _fields_ = [("warps", ctypes.c_int32), ("splits", ctypes.c_int32),
+                ("m_cta", ctypes.c_int32), ("n_cta", ctypes.c_int32),
+                ("grid_ctas", ctypes.c_int32), ("smem_bytes", ctypes.c_int32)]
+
+
+# Every symbol include/vlut.h declares (tests check the .so exports them all).
+EXPORTS = {
+    "vlut_packed_bytes": ([ctypes.c_int, ctypes.c_int, ctypes.c_int], ctypes.c_size_t),
+    "vlut_pack_weights": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                           ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(_Desc),
+                           ctypes.c_void_p], ctypes.c_int),
+    "vlut_pack_weights_device": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                  ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(_Desc),
+                                  ctypes.c_void_p], ctypes.c_int),
+    "vlut_unpack_weights_host": ([ctypes.POINTER(_Desc), ctypes.c_void_p, ctypes.c_void_p],
+                                 ctypes.c_int),
+    "vlut_plan": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                   ctypes.POINTER(_Plan)], ctypes.c_int),
+    "vlut_mpgemm": ([ctypes.POINTER(_Desc), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_float,
+                     ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                     ctypes.c_void_p], ctypes.c_int),
+    "vlut_mpgemm_ex": ([ctypes.POINTER(_Desc), ctypes.c_void_p, ctypes.c_void_p,
+                        ctypes.c_float, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                        ctypes.c_int, ctypes.POINTER(_Plan), ctypes.c_void_p], ctypes.c_int),
+    "vlut_mpgemm_acc": ([ctypes.POINTER(_Desc), ctypes.c_void_p, ctypes.c_void_p,
+                         ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_Plan),
+                         ctypes.c_void_p], ctypes.c_int),
+    "vlut_quantize": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "vlut_launches_per_mpgemm": ([], ctypes.c_int),
+    "vlut_last_error": ([], ctypes.c_char_p),
+    "vlut_version": ([], ctypes.c_char_p),
+}
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libvlut.so (built in-tree by ``__graft_entry__.build()``).  Raises
+    if it is missing -- there is deliberately no fallback."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(lib_path):
+            raise RuntimeError(f"{lib_path} is missing: run `python -c 'import __graft_entry__ "
+                               f"as g; g.build()'` (there is no CPU fallback)")
+        L = ctypes.CDLL(lib_path)
+        for name, (args, res) in EXPORTS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    return lib().vlut_last_error().decode()
+
+
+def _check(st: int) -> None:
+    if st != 0:
+        raise VlutError(st, last_error())
+
+
+def _stream_ptr(stream) -> ctypes.c_void_p:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dev_ptr(t) -> ctypes.c_void_p:
+    if t is None:
+        return ctypes.c_void_p(0)
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+@dataclass
+class LaunchPlan:
+    warps: int
+    splits: int
+    m_cta: int = 0
+    n_cta: int = 64
+    grid_ctas: int = 0
+    smem_bytes: int = 0
+
+    def _c(self) -> _Plan:
+        return _Plan(self.warps, self.splits, self.m_cta, self.n_cta, self.grid_ctas,
+                     self.smem_bytes)
+
+
+class PackedWeights:
+    """Device payload tensor + the C descriptor (a1)."""
+
+    def __init__(self, payload, desc: _Desc):
+        self.payload = payload  # keeps the device memory alive
+        self.desc = desc
+
+    @property
+    def M(self):
+        return self.desc.M
+
+    @property
+    def K(self):
+        return self.desc.K
+
+    @property
+    def g(self):
+        return self.desc.g
+
+    @property
+    def nbytes(self):
+        return int(self.desc.payload_bytes)
+
+
+def packed_bytes(M: int, K: int, g: int) -> int:
+    return int(lib().vlut_packed_bytes(M, K, g))
+
+
+def pack_weights(w_trits: np.ndarray, g: int, device=None, stream=None) -> PackedWeights:
+    """Host trits int8 [M][K] -> device packed weights (validated on host)."""
+    import torch
+    w = np.ascontiguousarray(w_trits, dtype=np.int8)
+    M, K = w.shape
+    nb = packed_bytes(M, K, g)
+    if nb == 0:
+        raise VlutError(3, f"cannot pack M={M} K={K} g={g}")
+    payload = torch.empty(nb, dtype=torch.uint8, device=device or "cuda")
+    d = _Desc()
+    with torch.cuda.device(payload.device):
+        _check(lib().vlut_pack_weights(ctypes.c_void_p(w.ctypes.data), M, K, g,
+                                       _dev_ptr(payload), nb, ctypes.byref(d),
+                                       _stream_ptr(stream)))
+    return PackedWeights(payload, d)
+
+
+def pack_weights_device(w_trits, g: int, stream=None) -> PackedWeights:
+    """Device trits (torch int8 CUDA [M][K]) -> packed weights, on the GPU."""
+    import torch
+    M, K = w_trits.shape
+    nb = packed_bytes(M, K, g)
+    if nb == 0:
+        raise VlutError(3, f"cannot pack M={M} K={K} g={g}")
+    payload = torch.empty(nb, dtype=torch.uint8, device=w_trits.device)
+    d = _Desc()
+    with torch.cuda.device(payload.device):
+        _check(lib().vlut_pack_weights_device(_dev_ptr(w_trits), M, K, g, _dev_ptr(payload), nb,
+                                              ctypes.byref(d), _stream_ptr(stream)))
+    return PackedWeights(payload, d)
+
+
+def unpack_weights_host(pw: PackedWeights) -> np.ndarray:
+    host = pw.payload.cpu().numpy()
+    out = np.zeros((pw.M, pw.K), dtype=np.int8)
+    _check(lib().vlut_unpack_weights_host(ctypes.byref(pw.desc),
+                                          ctypes.c_void_p(host.ctypes.data),
+                                          ctypes.c_void_p(out.ctypes.data)))
+    return out
+
+
+def plan(M: int, K: int, N: int, g: int) -> LaunchPlan:
+    p = _Plan()
+    _check(lib().vlut_plan(M, K, N, g, ctypes.byref(p)))
+    return LaunchPlan(p.warps, p.splits, p.m_cta, p.n_cta, p.grid_ctas, p.smem_bytes)
+
+
+def _plan_ptr(p: Optional[LaunchPlan]):
+    if p is None:
+        return None, ctypes.POINTER(_Plan)()
+    c = p._c()
+    return c, ctypes.byref(c)
+
+
+def mpgemm_ex(W: PackedWeights, A, a_scale, w_scale: float, out=None,
+              plan: Optional[LaunchPlan] = None, stream=None):
+    """fp32 out[M][N] = dequant(W x A) (a2-a6).  A: torch int8 CUDA [K][N]."""
+    import torch
+    K, N = A.shape
+    M = W.M
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    keep, pp = _plan_ptr(plan)
+    _check(lib().vlut_mpgemm_ex(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(a_scale),
+                                float(w_scale), _dev_ptr(out), M, K, N, pp,
+                                _stream_ptr(stream)))
+    return out
+
+
+def mpgemm(W: PackedWeights, A, a_scale, w_scale: float, out=None, stream=None):
+    """The north-star entry point vlut_mpgemm(W_packed, A_int8, a_scale,
+    w_scale, out, M, K, N, stream)."""
+    import torch
+    K, N = A.shape
+    M = W.M
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    _check(lib().vlut_mpgemm(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(a_scale),
+                             float(w_scale), _dev_ptr(out), M, K, N, _stream_ptr(stream)))
+    return out
+
+
+def mpgemm_acc(W: PackedWeights, A, out=None, plan: Optional[LaunchPlan] = None, stream=None):
+    """Raw int32 accumulators [M][N] (bit-exact test hook)."""
+    import torch
+    K, N = A.shape
+    M = W.M
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.int32, device=A.device)
+    keep, pp = _plan_ptr(plan)
+    _check(lib().vlut_mpgemm_acc(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(out), M, K, N,
+                                 pp, _stream_ptr(stream)))
+    return out
+
+
+def quantize(x, y=None, q=None, scale=None, stream=None):
+    """Per-token absmax int8 quantizer of fp32 [K][N] (x * y if y given)."""
+    import torch
+    K, N = x.shape
+    if q is None:
+        q = torch.empty((K, N), dtype=torch.int8, device=x.device)
+    if scale is None:
+        scale = torch.empty((N,), dtype=torch.float32, device=x.device)
+    _check(lib().vlut_quantize(_dev_ptr(x), _dev_ptr(y), K, N, _dev_ptr(q), _dev_ptr(scale),
+                               _stream_ptr(stream)))
+    return q, scale

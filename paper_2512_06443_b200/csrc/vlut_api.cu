@@ -1,0 +1,418 @@
+// vlut_api.cu -- host side of libvlut.so: argument validation, the weight
+// packer (a1), the launch planner and the launches.  See include/vlut.h for
+// the contract of every entry point.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/vlut.h"
+#include "vlut_aux_kernels.cuh"
+#include "vlut_kernel.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+vlut_status fail(vlut_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+vlut_status ok() {
+  g_err.clear();
+  return VLUT_OK;
+}
+
+#define VLUT_CUDA_TRY(expr)                                                              \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(VLUT_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(e_));        \
+  } while (0)
+
+struct DeviceInfo {
+  bool init = false;
+  int sms = 0;
+  int smem_optin = 0;
+  int cc_major = 0, cc_minor = 0;
+};
+
+std::mutex g_mu;
+DeviceInfo g_dev[64];
+
+vlut_status device_info(DeviceInfo* out) {
+  int dev = 0;
+  VLUT_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(VLUT_ERR_CUDA, "device ordinal %d out of range", dev);
+  std::lock_guard<std::mutex> lk(g_mu);
+  DeviceInfo& d = g_dev[dev];
+  if (!d.init) {
+    VLUT_CUDA_TRY(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
+    VLUT_CUDA_TRY(
+        cudaDeviceGetAttribute(&d.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    VLUT_CUDA_TRY(cudaDeviceGetAttribute(&d.cc_major, cudaDevAttrComputeCapabilityMajor, dev));
+    VLUT_CUDA_TRY(cudaDeviceGetAttribute(&d.cc_minor, cudaDevAttrComputeCapabilityMinor, dev));
+    d.init = true;
+  }
+  *out = d;
+  return VLUT_OK;
+}
+
+inline bool valid_g(int g) { return g == 4 || g == 5; }
+
+inline int pow3i(int g) { return g == 4 ? 81 : 243; }
+
+bool layout_of(int M, int K, int g, int* m_pad, int* kg_tiles, size_t* bytes) {
+  if (M <= 0 || K <= 0 || !valid_g(g) || K % g) return false;
+  const long long mp = ((long long)M + VLUT_M_TILE - 1) / VLUT_M_TILE * VLUT_M_TILE;
+  const long long kgt = ((long long)(K / g) + VLUT_KG_TILE - 1) / VLUT_KG_TILE;
+  const long long b = kgt * mp * 16;
+  if (mp > (1LL << 30) || kgt > (1LL << 30) || b <= 0) return false;
+  *m_pad = (int)mp;
+  *kg_tiles = (int)kgt;
+  *bytes = (size_t)b;
+  return true;
+}
+
+vlut_status check_desc(const vlut_packed_weights* W, int M, int K) {
+  if (!W) return fail(VLUT_ERR_INVALID_ARGUMENT, "W descriptor is NULL");
+  if (W->magic != VLUT_MAGIC || W->version != VLUT_VERSION)
+    return fail(VLUT_ERR_CORRUPT_DESCRIPTOR, "bad descriptor magic/version");
+  int mp = 0, kgt = 0;
+  size_t bytes = 0;
+  if (!layout_of(W->M, W->K, W->g, &mp, &kgt, &bytes) || W->m_pad != mp ||
+      W->kg_tiles != kgt || W->payload_bytes != (int64_t)bytes || W->m_tile != VLUT_M_TILE ||
+      W->kg_tile != VLUT_KG_TILE || !W->payload)
+    return fail(VLUT_ERR_CORRUPT_DESCRIPTOR, "descriptor fields inconsistent");
+  if (((uintptr_t)W->payload) & 15) return fail(VLUT_ERR_MISALIGNED, "payload not 16-B aligned");
+  if (W->M != M || W->K != K)
+    return fail(VLUT_ERR_SHAPE, "shape (M=%d,K=%d) does not match descriptor (M=%d,K=%d)", M,
+                K, W->M, W->K);
+  return VLUT_OK;
+}
+
+// ------------------------------------------------------------ planner
+int smem_bytes_for(int g, int warps) {
+  if (g == 4) {
+    if (warps == 8) return vlut::Layout<4, 8>::SMEM;
+    if (warps == 12) return vlut::Layout<4, 12>::SMEM;
+    return vlut::Layout<4, 16>::SMEM;
+  }
+  if (warps == 8) return vlut::Layout<5, 8>::SMEM;
+  if (warps == 12) return vlut::Layout<5, 12>::SMEM;
+  return vlut::Layout<5, 16>::SMEM;
+}
+
+// Cost model (shared-memory cycles per CTA):
+//   lookups   m_cta * 64 tokens * 2 B per group  /128 B/clk
+//   build     3^g * 128 B per group               /128 B/clk
+//   reduce    (S-1)/S * m_cta * 256 B over DSMEM   / ~20 B/clk
+// total = waves * per-CTA, waves = ceil(CTAs / slots), slots = SMs (cluster
+// sizes <= 2) or 132 (cluster 4, which strands SMs on some GPCs).
+void plan_for(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
+  const int KG = K / g;
+  const int kgt = (KG + VLUT_KG_TILE - 1) / VLUT_KG_TILE;
+  const int NT = (N + vlut::kNcta - 1) / vlut::kNcta;
+  const int rows = pow3i(g);
+  double best_cost = 1e300;
+  const int warps_opts[3] = {16, 12, 8};
+  const int split_opts[3] = {1, 2, 4};
+  for (int wi = 0; wi < 3; ++wi) {
+    const int warps = warps_opts[wi];
+    const int mcta = 32 * warps;
+    const long long MT = (M + mcta - 1) / mcta;
+    for (int si = 0; si < 3; ++si) {
+      const int S = split_opts[si];
+      if (S > kgt) continue;
+      const long long ctas = MT * NT * S;
+      if (ctas > 65535LL * 65535LL) continue;
+      const int slots = (S <= 2) ? (sms / S) * S : (sms * 132 / 148 / S) * S;
+      if (slots <= 0) continue;
+      const long long waves = (ctas + slots - 1) / slots;
+      const double tiles = (double)((kgt + S - 1) / S);
+      const double per_group = (double)mcta * 128.0 / 128.0 + rows;  // SMEM cycles
+      double per_cta = tiles * VLUT_KG_TILE * per_group;
+      per_cta += 2000.0;  // prologue / epilogue
+      if (S > 1) per_cta += (double)(S - 1) / S * mcta * 256.0 / 20.0;
+      const double cost = waves * per_cta;
+      if (cost < best_cost * 0.999) {
+        best_cost = cost;
+        best->warps = warps;
+        best->splits = S;
+        best->m_cta = mcta;
+        best->n_cta = vlut::kNcta;
+        best->grid_ctas = (int)ctas;
+        best->smem_bytes = smem_bytes_for(g, warps);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ launches
+template <int G, int WARPS, bool ACC>
+vlut_status launch_k1(const vlut::Params& p, int S, int NT, int MT, cudaStream_t st) {
+  using L = vlut::Layout<G, WARPS>;
+  auto kern = vlut::vlut_mpgemm_kernel<G, WARPS, ACC>;
+  static std::once_flag flags[64];
+  int dev = 0;
+  VLUT_CUDA_TRY(cudaGetDevice(&dev));
+  cudaError_t attr_err = cudaSuccess;
+  std::call_once(flags[dev & 63], [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+  });
+  VLUT_CUDA_TRY(attr_err);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)S, (unsigned)NT, (unsigned)MT);
+  cfg.blockDim = dim3(L::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = L::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  VLUT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
+  return VLUT_OK;
+}
+
+template <bool ACC>
+vlut_status dispatch(int g, int warps, const vlut::Params& p, int S, int NT, int MT,
+                     cudaStream_t st) {
+  if (g == 4) {
+    if (warps == 8) return launch_k1<4, 8, ACC>(p, S, NT, MT, st);
+    if (warps == 12) return launch_k1<4, 12, ACC>(p, S, NT, MT, st);
+    if (warps == 16) return launch_k1<4, 16, ACC>(p, S, NT, MT, st);
+  } else {
+    if (warps == 8) return launch_k1<5, 8, ACC>(p, S, NT, MT, st);
+    if (warps == 12) return launch_k1<5, 12, ACC>(p, S, NT, MT, st);
+    if (warps == 16) return launch_k1<5, 16, ACC>(p, S, NT, MT, st);
+  }
+  return fail(VLUT_ERR_UNSUPPORTED, "no kernel variant for g=%d warps=%d", g, warps);
+}
+
+vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,
+                       float w_scale, void* out, int M, int K, int N,
+                       const vlut_launch_plan* plan_in, void* stream, bool acc_only) {
+  if (M < 0 || K <= 0 || N < 0) return fail(VLUT_ERR_INVALID_ARGUMENT, "bad sizes M=%d K=%d N=%d", M, K, N);
+  if (M == 0 || N == 0) return ok();
+  vlut_status st = check_desc(W, M, K);
+  if (st != VLUT_OK) return st;
+  if (!A || !out || (!acc_only && !a_scale))
+    return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL device pointer");
+  if (((uintptr_t)out) & 3) return fail(VLUT_ERR_MISALIGNED, "out not 4-B aligned");
+  if (!acc_only && (((uintptr_t)a_scale) & 3))
+    return fail(VLUT_ERR_MISALIGNED, "a_scale not 4-B aligned");
+  if ((long long)N > (1LL << 30)) return fail(VLUT_ERR_SHAPE, "N too large");
+  DeviceInfo d;
+  st = device_info(&d);
+  if (st != VLUT_OK) return st;
+  vlut_launch_plan plan = {};
+  if (plan_in) {
+    plan = *plan_in;
+    if (!(plan.warps == 8 || plan.warps == 12 || plan.warps == 16) ||
+        !(plan.splits == 1 || plan.splits == 2 || plan.splits == 4))
+      return fail(VLUT_ERR_INVALID_ARGUMENT, "invalid plan warps=%d splits=%d", plan.warps,
+                  plan.splits);
+  } else {
+    plan_for(M, K, N, W->g, d.sms, &plan);
+  }
+  if (plan.splits > W->kg_tiles) plan.splits = 1;
+  const int smem = smem_bytes_for(W->g, plan.warps);
+  if (smem > d.smem_optin)
+    return fail(VLUT_ERR_UNSUPPORTED, "needs %d B shared memory, device allows %d", smem,
+                d.smem_optin);
+  vlut::Params p;
+  p.payload = static_cast<const uint8_t*>(W->payload);
+  p.A = A;
+  p.a_scale = a_scale;
+  p.w_scale = w_scale;
+  p.out = static_cast<float*>(out);
+  p.M = M;
+  p.K = K;
+  p.N = N;
+  p.m_pad = W->m_pad;
+  p.kg_tiles = W->kg_tiles;
+  p.splits = plan.splits;
+  const uintptr_t ap = (uintptr_t)A;
+  p.a_vec = (N % 16 == 0 && (ap & 15) == 0) ? 16 : ((N % 4 == 0 && (ap & 3) == 0) ? 4 : 1);
+  p.out_vec4 = (N % 4 == 0 && (((uintptr_t)out) & 15) == 0) ? 1 : 0;
+  const int mcta = 32 * plan.warps;
+  const long long NT = (N + vlut::kNcta - 1) / vlut::kNcta;
+  const long long MT = (M + mcta - 1) / mcta;
+  if (NT > 65535 || MT > 65535) return fail(VLUT_ERR_SHAPE, "grid too large");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  st = acc_only ? dispatch<true>(W->g, plan.warps, p, plan.splits, (int)NT, (int)MT, s)
+                : dispatch<false>(W->g, plan.warps, p, plan.splits, (int)NT, (int)MT, s);
+  if (st != VLUT_OK) return st;
+  return ok();
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+extern "C" {
+
+const char* vlut_last_error(void) { return g_err.c_str(); }
+
+const char* vlut_version(void) { return "vlut-b200 0.1 (sm_100a)"; }
+
+int vlut_launches_per_mpgemm(void) { return 1; }
+
+size_t vlut_packed_bytes(int M, int K, int g) {
+  int mp = 0, kgt = 0;
+  size_t b = 0;
+  if (!layout_of(M, K, g, &mp, &kgt, &b)) return 0;
+  return b;
+}
+
+static vlut_status fill_desc(int M, int K, int g, void* payload_dev, size_t payload_bytes,
+                             vlut_packed_weights* desc_out, int* m_pad, int* kgt) {
+  if (!desc_out || !payload_dev) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!valid_g(g)) return fail(VLUT_ERR_INVALID_ARGUMENT, "g must be 4 or 5 (got %d)", g);
+  if (M <= 0 || K <= 0) return fail(VLUT_ERR_INVALID_ARGUMENT, "M, K must be > 0");
+  if (K % g) return fail(VLUT_ERR_SHAPE, "g=%d does not divide K=%d", g, K);
+  size_t need = 0;
+  if (!layout_of(M, K, g, m_pad, kgt, &need)) return fail(VLUT_ERR_SHAPE, "size overflow");
+  if (payload_bytes < need)
+    return fail(VLUT_ERR_BUFFER_TOO_SMALL, "payload needs %zu bytes, got %zu", need,
+                payload_bytes);
+  if (((uintptr_t)payload_dev) & 15) return fail(VLUT_ERR_MISALIGNED, "payload not 16-B aligned");
+  memset(desc_out, 0, sizeof(*desc_out));
+  desc_out->magic = VLUT_MAGIC;
+  desc_out->version = VLUT_VERSION;
+  desc_out->M = M;
+  desc_out->K = K;
+  desc_out->g = g;
+  desc_out->m_pad = *m_pad;
+  desc_out->kg_tiles = *kgt;
+  desc_out->m_tile = VLUT_M_TILE;
+  desc_out->kg_tile = VLUT_KG_TILE;
+  desc_out->payload_bytes = (int64_t)need;
+  desc_out->payload = payload_dev;
+  return VLUT_OK;
+}
+
+vlut_status vlut_pack_weights(const int8_t* w, int M, int K, int g, void* payload_dev,
+                              size_t payload_bytes, vlut_packed_weights* desc_out,
+                              void* stream) {
+  if (!w) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL weights");
+  vlut_packed_weights d;
+  int mp = 0, kgt = 0;
+  vlut_status st = fill_desc(M, K, g, payload_dev, payload_bytes, &d, &mp, &kgt);
+  if (st != VLUT_OK) return st;
+  const int KG = K / g;
+  const uint8_t zero = (uint8_t)((pow3i(g) - 1) / 2);
+  std::vector<uint8_t> host((size_t)d.payload_bytes, zero);
+  for (int m = 0; m < M; ++m) {
+    const int8_t* row = w + (size_t)m * K;
+    for (int k = 0; k < KG; ++k) {
+      int idx = 0, p3 = 1;
+      for (int r = 0; r < g; ++r) {
+        const int t = row[k * g + r];
+        if (t < -1 || t > 1)
+          return fail(VLUT_ERR_INVALID_TRIT, "invalid trit %d at (%d,%d)", t, m, k * g + r);
+        idx += (t + 1) * p3;
+        p3 *= 3;
+      }
+      host[((size_t)(k / VLUT_KG_TILE) * mp + m) * 16 + (k % VLUT_KG_TILE)] = (uint8_t)idx;
+    }
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  VLUT_CUDA_TRY(cudaMemcpyAsync(payload_dev, host.data(), host.size(), cudaMemcpyHostToDevice, s));
+  VLUT_CUDA_TRY(cudaStreamSynchronize(s));
+  *desc_out = d;
+  return ok();
+}
+
+vlut_status vlut_pack_weights_device(const int8_t* w_dev, int M, int K, int g,
+                                     void* payload_dev, size_t payload_bytes,
+                                     vlut_packed_weights* desc_out, void* stream) {
+  if (!w_dev) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL weights");
+  vlut_packed_weights d;
+  int mp = 0, kgt = 0;
+  vlut_status st = fill_desc(M, K, g, payload_dev, payload_bytes, &d, &mp, &kgt);
+  if (st != VLUT_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long long total = d.payload_bytes;
+  const int threads = 256;
+  long long blocks = (total + threads - 1) / threads;
+  if (blocks > 148LL * 64) blocks = 148LL * 64;
+  vlut::vlut_pack_kernel<<<(unsigned)blocks, threads, 0, s>>>(
+      w_dev, M, K, g, mp, kgt, static_cast<uint8_t*>(payload_dev));
+  VLUT_CUDA_TRY(cudaGetLastError());
+  *desc_out = d;
+  return ok();
+}
+
+vlut_status vlut_unpack_weights_host(const vlut_packed_weights* desc, const uint8_t* payload,
+                                     int8_t* w) {
+  if (!desc || !payload || !w) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL argument");
+  int mp = 0, kgt = 0;
+  size_t bytes = 0;
+  if (desc->magic != VLUT_MAGIC || !layout_of(desc->M, desc->K, desc->g, &mp, &kgt, &bytes) ||
+      desc->m_pad != mp || desc->kg_tiles != kgt)
+    return fail(VLUT_ERR_CORRUPT_DESCRIPTOR, "bad descriptor");
+  const int g = desc->g, K = desc->K, KG = K / g, R = pow3i(g);
+  for (int m = 0; m < desc->M; ++m)
+    for (int k = 0; k < KG; ++k) {
+      int idx = payload[((size_t)(k / VLUT_KG_TILE) * mp + m) * 16 + (k % VLUT_KG_TILE)];
+      if (idx >= R) return fail(VLUT_ERR_INVALID_TRIT, "corrupt payload byte %d at (%d,%d)", idx, m, k);
+      for (int r = 0; r < g; ++r) {
+        w[(size_t)m * K + k * g + r] = (int8_t)(idx % 3 - 1);
+        idx /= 3;
+      }
+    }
+  return ok();
+}
+
+vlut_status vlut_plan(int M, int K, int N, int g, vlut_launch_plan* plan) {
+  if (!plan) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL plan");
+  if (M <= 0 || K <= 0 || N <= 0 || !valid_g(g)) return fail(VLUT_ERR_INVALID_ARGUMENT, "bad sizes");
+  if (K % g) return fail(VLUT_ERR_SHAPE, "g=%d does not divide K=%d", g, K);
+  DeviceInfo d;
+  vlut_status st = device_info(&d);
+  if (st != VLUT_OK) return st;
+  memset(plan, 0, sizeof(*plan));
+  plan_for(M, K, N, g, d.sms, plan);
+  return ok();
+}
+
+vlut_status vlut_mpgemm(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,
+                        float w_scale, float* out, int M, int K, int N, void* stream) {
+  return run_mpgemm(W, A, a_scale, w_scale, out, M, K, N, nullptr, stream, false);
+}
+
+vlut_status vlut_mpgemm_ex(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,
+                           float w_scale, float* out, int M, int K, int N,
+                           const vlut_launch_plan* plan, void* stream) {
+  return run_mpgemm(W, A, a_scale, w_scale, out, M, K, N, plan, stream, false);
+}
+
+vlut_status vlut_mpgemm_acc(const vlut_packed_weights* W, const int8_t* A, int32_t* acc_out,
+                            int M, int K, int N, const vlut_launch_plan* plan, void* stream) {
+  return run_mpgemm(W, A, nullptr, 0.f, acc_out, M, K, N, plan, stream, true);
+}
+
+vlut_status vlut_quantize(const float* x, const float* y, int K, int N, int8_t* q, float* scale,
+                          void* stream) {
+  if (K < 0 || N < 0) return fail(VLUT_ERR_INVALID_ARGUMENT, "bad sizes");
+  if (K == 0 || N == 0) return ok();
+  if (!x || !q || !scale) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const unsigned blocks = (unsigned)((N + 31) / 32);
+  vlut::vlut_quantize_kernel<<<blocks, vlut::kQuantWarps * 32, 0, s>>>(x, y, K, N, q, scale);
+  VLUT_CUDA_TRY(cudaGetLastError());
+  return ok();
+}
+
+}  // extern "C"

@@ -1,0 +1,188 @@
+"""C-ABI library tests that need no GPU: the .so loads, exports every symbol
+include/vlut.h declares, validates arguments before touching CUDA, and its
+host-side layout logic (packed bytes, unpacking) matches the documented
+layout.  Also a host-side check that the kernel's shared-memory access
+patterns are bank-conflict free (the design claim of DESIGN.md §K1)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2512_06443_b200 as v
+from paper_2512_06443_b200 import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "vlut.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(vlut_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol():
+    L = v.lib()
+    declared = header_functions()
+    assert len(declared) >= 10
+    for name in declared:
+        assert hasattr(L, name), name
+        assert name in v.EXPORTS, name
+    assert v.lib().vlut_launches_per_mpgemm() == 1
+    assert b"sm_100a" in v.lib().vlut_version()
+
+
+def test_packed_bytes():
+    assert v.packed_bytes(256, 512, 4) == 8 * 256 * 16          # 128 groups = 8 K-tiles
+    assert v.packed_bytes(6912, 2560, 4) == 40 * 6912 * 16
+    assert v.packed_bytes(3072, 23040, 5) == 288 * 3072 * 16
+    assert v.packed_bytes(33, 20, 4) == 1 * 64 * 16             # M padded to 32, KG padded to 16
+    for bad in [(0, 8, 4), (8, 0, 4), (8, 9, 4), (8, 8, 3), (8, 10, 6), (-1, 8, 4)]:
+        assert v.packed_bytes(*bad) == 0
+
+
+def layout_payload(W, g):
+    """Build a payload by the layout documented in include/vlut.h, from the
+    oracle's logical packing (test-side; independent of the library)."""
+    M, K = W.shape
+    idx = oracle.pack_matrix(W, g)
+    KG = K // g
+    m_pad = -(-M // 32) * 32
+    kgt = -(-KG // 16)
+    pay = np.full((kgt, m_pad, 16), oracle.zero_index(g), np.uint8)
+    for k in range(KG):
+        pay[k // 16, :M, k % 16] = idx[:, k]
+    return pay.reshape(-1), m_pad, kgt
+
+
+def make_desc(M, K, g, m_pad, kgt, ptr):
+    d = v._Desc()
+    d.magic, d.version = v.VLUT_MAGIC, v.VLUT_VERSION
+    d.M, d.K, d.g, d.m_pad, d.kg_tiles, d.m_tile, d.kg_tile = M, K, g, m_pad, kgt, 32, 16
+    d.payload_bytes = kgt * m_pad * 16
+    d.payload = ptr
+    return d
+
+
+@pytest.mark.parametrize("M,K,g", [(1, 4, 4), (45, 200, 4), (70, 85, 5), (32, 320, 5)])
+def test_unpack_host_matches_documented_layout(M, K, g):
+    W = synth.ternary_weights(M, K, seed=M * K)
+    pay, m_pad, kgt = layout_payload(W, g)
+    d = make_desc(M, K, g, m_pad, kgt, 0x1000)
+    out = np.zeros((M, K), np.int8)
+    st = v.lib().vlut_unpack_weights_host(ctypes.byref(d), ctypes.c_void_p(pay.ctypes.data),
+                                          ctypes.c_void_p(out.ctypes.data))
+    assert st == 0 and np.array_equal(out, W)
+    pay2 = pay.copy()
+    pay2[3] = 3 ** g  # corrupt byte
+    if M * (K // g) > 3 or True:
+        st = v.lib().vlut_unpack_weights_host(ctypes.byref(d), ctypes.c_void_p(pay2.ctypes.data),
+                                              ctypes.c_void_p(out.ctypes.data))
+        # byte 3 of tile 0 row 0 is group 3 of row 0 if K/g > 3, else padding
+        assert st == (2 if K // g > 3 else 0)
+
+
+def test_pack_validation_without_gpu():
+    L = v.lib()
+    d = v._Desc()
+    fake = ctypes.c_void_p(0x10000)
+    W = np.zeros((4, 8), np.int8)
+    W[1, 3] = 2
+    wp = ctypes.c_void_p(W.ctypes.data)
+    assert L.vlut_pack_weights(wp, 4, 8, 4, fake, 4096, ctypes.byref(d), None) == 2   # INVALID_TRIT
+    assert "invalid trit" in v.last_error()
+    assert L.vlut_pack_weights(wp, 4, 9, 4, fake, 4096, ctypes.byref(d), None) == 3   # SHAPE
+    assert L.vlut_pack_weights(wp, 4, 8, 3, fake, 4096, ctypes.byref(d), None) == 1   # bad g
+    assert L.vlut_pack_weights(wp, 4, 8, 4, fake, 16, ctypes.byref(d), None) == 4     # too small
+    assert L.vlut_pack_weights(wp, 4, 8, 4, ctypes.c_void_p(0x10001), 4096,
+                               ctypes.byref(d), None) == 5                          # misaligned
+    assert L.vlut_pack_weights(None, 4, 8, 4, fake, 4096, ctypes.byref(d), None) == 1
+
+
+def test_mpgemm_validation_without_gpu():
+    L = v.lib()
+    d = make_desc(64, 128, 4, 64, 2, 0x10000)
+    p = ctypes.c_void_p(0x20000)
+    # N == 0 / M == 0: no-op
+    assert L.vlut_mpgemm(ctypes.byref(d), p, p, 0.02, p, 64, 128, 0, None) == 0
+    assert L.vlut_mpgemm(None, p, p, 0.02, p, 0, 128, 5, None) == 0
+    bad = make_desc(64, 128, 4, 64, 2, 0x10000)
+    bad.magic = 0
+    assert L.vlut_mpgemm(ctypes.byref(bad), p, p, 0.02, p, 64, 128, 8, None) == 6
+    bad = make_desc(64, 128, 4, 64, 3, 0x10000)  # wrong kg_tiles
+    assert L.vlut_mpgemm(ctypes.byref(bad), p, p, 0.02, p, 64, 128, 8, None) == 6
+    assert L.vlut_mpgemm(ctypes.byref(d), p, p, 0.02, p, 64, 132, 8, None) == 3       # K mismatch
+    assert L.vlut_mpgemm(ctypes.byref(d), None, p, 0.02, p, 64, 128, 8, None) == 1
+    assert L.vlut_mpgemm(ctypes.byref(d), p, p, 0.02, ctypes.c_void_p(0x20002), 64, 128, 8,
+                         None) == 5
+    assert L.vlut_mpgemm(None, p, p, 0.02, p, 64, 128, 8, None) == 1
+
+
+def test_fails_loudly_without_cuda_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    L = v.lib()
+    d = make_desc(64, 128, 4, 64, 2, 0x10000)
+    p = ctypes.c_void_p(0x20000)
+    st = L.vlut_mpgemm(ctypes.byref(d), p, p, 0.02, p, 64, 128, 8, None)
+    assert st == 7 and v.last_error()  # VLUT_ERR_CUDA, no silent fallback
+    with pytest.raises(v.VlutError):
+        v.plan(64, 128, 8, 4)
+
+
+# ------------------------------------------------------------------ bank-conflict model
+def wavefronts_128(addrs):
+    """Shared-memory wavefronts of one warp-wide 16-byte access: served as 4
+    phases of 8 lanes; within a phase, each 16-byte chunk position (bank
+    group = (addr // 16) % 8) holding distinct chunks costs one extra pass."""
+    total = 0
+    for ph in range(4):
+        groups = {}
+        for a in addrs[8 * ph: 8 * ph + 8]:
+            groups.setdefault((a // 16) % 8, set()).add(a // 16)
+        total += max(len(s) for s in groups.values())
+    return total
+
+
+def test_lookup_rotation_is_conflict_free():
+    rng = synth.rng(1)
+    row_bytes = 128
+    for _ in range(200):
+        idx = rng.integers(0, 81, size=32)  # data-dependent rows per lane
+        for s in range(8):
+            addrs = [int(idx[l]) * row_bytes + ((l + s) & 7) * 16 for l in range(32)]
+            assert wavefronts_128(addrs) == 4
+    # without rotation the same access conflicts
+    idx = np.arange(32) % 81
+    addrs = [int(idx[l]) * row_bytes + 0 for l in range(32)]
+    assert wavefronts_128(addrs) > 4
+
+
+def test_reduction_tile_swizzle_is_conflict_free():
+    for warp in range(16):
+        for s in range(8):
+            for h in range(2):
+                addrs = []
+                for lane in range(32):
+                    r = warp * 32 + lane
+                    c = (lane + s) & 7
+                    u = (2 * c + h) ^ ((r >> 2) & 1)
+                    addrs.append(r * 256 + u * 16)
+                assert wavefronts_128(addrs) == 4
+    # row-contiguous reads of the epilogue: lanes 0-15 row x, 16-31 row x+1
+    for x in range(0, 64, 2):
+        addrs = []
+        for lane in range(32):
+            r = x + lane // 16
+            u = lane % 16
+            addrs.append(r * 256 + (u ^ ((r >> 2) & 1)) * 16)
+        assert wavefronts_128(addrs) == 4

@@ -1,0 +1,225 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (north star): int32 accumulators bit-exact; fp32 outputs within 1e-6
+relative error of the fp64 definition (and, by fixed op order, bit-identical
+to the oracle's fp32 dequant); quantizer codes and scales bit-exact.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2512_06443_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+REL_TOL = 1e-6  # north star: <= 1e-6 relative error on fp32 outputs
+
+
+@pytest.fixture(scope="module")
+def v():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2512_06443_b200 as vl
+    return vl
+
+
+def dev():
+    return torch.device("cuda:0")
+
+
+def to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev())
+
+
+def check_fp32(got, acc_ref, a_scale, w_scale):
+    ref = oracle.dequant_f64(acc_ref, a_scale, w_scale)
+    g = got.astype(np.float64)
+    nz = ref != 0
+    assert np.all(g[~nz] == 0)
+    rel = np.abs(g[nz] - ref[nz]) / np.abs(ref[nz])
+    assert rel.size == 0 or rel.max() <= REL_TOL, rel.max()
+    ref32 = oracle.dequant_f32(acc_ref, a_scale, w_scale)
+    assert np.array_equal(got.view(np.int32), ref32.view(np.int32))
+
+
+ALL_PLANS = [(w, s) for w in (8, 12, 16) for s in (1, 2, 4)]
+
+
+# ------------------------------------------------------------------ quantizer
+@pytest.mark.parametrize("K,N", [(1, 1), (5, 3), (512, 8), (2560, 257), (6912, 64)])
+def test_quantize_bit_exact(v, K, N):
+    x = synth.activations_f32(K, N, seed=K + N)
+    if N > 2:
+        x[:, 1] = 0.0          # zero column -> scale 1
+        x[:, 2] *= 1e-30       # tiny values
+    q, s = v.quantize(to_dev(x))
+    qr, sr = oracle.quantize(x)
+    assert np.array_equal(s.cpu().numpy().view(np.int32), sr.view(np.int32))
+    assert np.array_equal(q.cpu().numpy(), qr)
+
+
+def test_quantize_mul_bit_exact(v):
+    K, N = 700, 96
+    a = synth.activations_f32(K, N, seed=1)
+    b = synth.activations_f32(K, N, seed=2)
+    q, s = v.quantize(to_dev(a), to_dev(b))
+    qr, sr = oracle.quantize((a * b).astype(np.float32))
+    assert np.array_equal(s.cpu().numpy(), sr) and np.array_equal(q.cpu().numpy(), qr)
+
+
+# ------------------------------------------------------------------ packer
+@pytest.mark.parametrize("M,K,g", [(1, 4, 4), (33, 200, 4), (100, 85, 5), (384, 2560, 4)])
+def test_pack_roundtrip_and_device_packer(v, M, K, g):
+    W = synth.ternary_weights(M, K, seed=M + K)
+    pw = v.pack_weights(W, g, device=dev())
+    assert np.array_equal(v.unpack_weights_host(pw), W)
+    pd = v.pack_weights_device(to_dev(W), g)
+    torch.cuda.synchronize()
+    assert torch.equal(pw.payload, pd.payload)
+
+
+def test_pack_rejects_invalid_trit(v):
+    W = np.zeros((4, 8), np.int8)
+    W[2, 5] = -2
+    with pytest.raises(v.VlutError) as e:
+        v.pack_weights(W, 4, device=dev())
+    assert e.value.name == "VLUT_ERR_INVALID_TRIT"
+
+
+# ------------------------------------------------------------------ mpGeMM, exact int32
+SHAPES = [
+    # (M, K, N, g) -- tails in every dimension, several tiles
+    (1, 4, 1, 4), (7, 20, 3, 4), (32, 64, 64, 4), (33, 68, 65, 4), (100, 512, 8, 4),
+    (256, 512, 8, 4), (385, 1024, 130, 4), (520, 1280, 63, 4), (1000, 260, 256, 4),
+    (5, 5, 1, 5), (70, 85, 17, 5), (129, 640, 64, 5), (400, 1280, 100, 5), (777, 2560, 200, 5),
+]
+
+
+@pytest.mark.parametrize("M,K,N,g", SHAPES)
+def test_mpgemm_acc_bit_exact_default_plan(v, M, K, N, g):
+    W = synth.ternary_weights(M, K, seed=3 * M + K)
+    A = synth.int8_activations(K, N, seed=N + 17)  # full int8 range incl. -128
+    pw = v.pack_weights(W, g, device=dev())
+    acc = v.mpgemm_acc(pw, to_dev(A))
+    torch.cuda.synchronize()
+    assert np.array_equal(acc.cpu().numpy(), oracle.gemm_i32(W, A))
+
+
+@pytest.mark.parametrize("g", [4, 5])
+@pytest.mark.parametrize("warps,splits", ALL_PLANS)
+def test_mpgemm_acc_every_plan(v, g, warps, splits):
+    M, K, N = 700, 64 * g * 5 + 4 * g, 150  # 5.25 K-tiles: ragged split ranges
+    W = synth.ternary_weights(M, K, seed=11)
+    A = synth.int8_activations(K, N, seed=12)
+    pw = v.pack_weights(W, g, device=dev())
+    acc = v.mpgemm_acc(pw, to_dev(A), plan=v.LaunchPlan(warps, splits))
+    torch.cuda.synchronize()
+    assert np.array_equal(acc.cpu().numpy(), oracle.gemm_i32(W, A))
+
+
+@pytest.mark.parametrize("g", [4, 5])
+def test_mpgemm_adversarial_extremes(v, g):
+    # |acc| up to 128 * K: all +1 weights against all -128 / +127 activations,
+    # a long K (many SWAR flushes), every field at its bias bound
+    M, K, N = 64, 23040 if g == 4 else 23040, 64
+    W = np.ones((M, K), np.int8)
+    W[1::2] = -1
+    W[2::4] = 0
+    A = np.full((K, N), -128, np.int8)
+    A[:, 1::2] = 127
+    pw = v.pack_weights(W, g, device=dev())
+    acc = v.mpgemm_acc(pw, to_dev(A)).cpu().numpy()
+    ref = oracle.gemm_i32(W, A)
+    assert np.array_equal(acc, ref)
+    assert ref.min() == -128 * K or ref.max() == 128 * K
+
+
+def test_mpgemm_zero_and_negation(v):
+    M, K, N = 300, 1024, 128
+    A = synth.int8_activations(K, N, seed=5)
+    Ad = to_dev(A)
+    pz = v.pack_weights(np.zeros((M, K), np.int8), 4, device=dev())
+    assert not v.mpgemm_acc(pz, Ad).any().item()
+    W = synth.ternary_weights(M, K, seed=6)
+    a = v.mpgemm_acc(v.pack_weights(W, 4, device=dev()), Ad)
+    b = v.mpgemm_acc(v.pack_weights(-W, 4, device=dev()), Ad)
+    assert torch.equal(a, -b)
+
+
+# ------------------------------------------------------------------ fp32 epilogue
+@pytest.mark.parametrize("M,K,N,g", [(256, 512, 8, 4), (385, 1024, 130, 4), (200, 1280, 96, 5)])
+def test_mpgemm_fp32_matches_oracle(v, M, K, N, g):
+    W = synth.ternary_weights(M, K, seed=M)
+    x = synth.activations_f32(K, N, seed=N)
+    q, s = oracle.quantize(x)
+    pw = v.pack_weights(W, g, device=dev())
+    out = v.mpgemm(pw, to_dev(q), to_dev(s), synth.W_SCALE)
+    torch.cuda.synchronize()
+    check_fp32(out.cpu().numpy(), oracle.gemm_i32(W, q), s, synth.W_SCALE)
+
+
+def test_unaligned_N_paths(v):
+    # N % 16 != 0 (4-byte staging) and N odd (byte staging, scalar stores)
+    for N in (4, 12, 9, 1):
+        M, K = 96, 256
+        W = synth.ternary_weights(M, K, seed=N)
+        A = synth.int8_activations(K, N, seed=N + 1)
+        s = synth.token_scales(N, seed=N + 2)
+        pw = v.pack_weights(W, 4, device=dev())
+        out = v.mpgemm(pw, to_dev(A), to_dev(s), 0.5)
+        acc = v.mpgemm_acc(pw, to_dev(A))
+        torch.cuda.synchronize()
+        ref = oracle.gemm_i32(W, A)
+        assert np.array_equal(acc.cpu().numpy(), ref)
+        check_fp32(out.cpu().numpy(), ref, s, 0.5)
+
+
+def test_determinism_across_plans(v):
+    M, K, N = 1536, 2560, 256
+    W = synth.ternary_weights(M, K, seed=2, p_zero=0.4)
+    A = synth.int8_activations(K, N, seed=3)
+    s = synth.token_scales(N, seed=4)
+    pw = v.pack_weights(W, 4, device=dev())
+    Ad, sd = to_dev(A), to_dev(s)
+    outs = [v.mpgemm_ex(pw, Ad, sd, 0.02, plan=v.LaunchPlan(w, sp)) for w, sp in ALL_PLANS]
+    outs.append(v.mpgemm(pw, Ad, sd, 0.02))
+    for o in outs[1:]:
+        assert torch.equal(o.view(torch.int32), outs[0].view(torch.int32))
+
+
+# ------------------------------------------------------------------ full BASELINE sizes, sampled
+def sampled_rows_check(v, M, K, N, g, seed, p_zero=None, rows=48):
+    W = synth.ternary_weights(M, K, seed=seed, p_zero=p_zero)
+    x = synth.activations_f32(K, N, seed=seed + 1)
+    xd = to_dev(x)
+    q, s = v.quantize(xd)            # GPU quantizer, as bench.py runs it
+    pw = v.pack_weights_device(to_dev(W), g)
+    out = v.mpgemm(pw, q, s, synth.W_SCALE)
+    torch.cuda.synchronize()
+    qr, sr = oracle.quantize(x)
+    assert np.array_equal(q.cpu().numpy(), qr) and np.array_equal(s.cpu().numpy(), sr)
+    r = synth.rng(seed + 2)
+    pick = np.unique(np.concatenate([[0, M - 1], r.integers(0, M, size=rows)]))
+    acc_ref = oracle.gemm_i32(W[pick], qr)
+    check_fp32(out.cpu().numpy()[pick], acc_ref, sr, synth.W_SCALE)
+
+
+def test_config2_full_size_sampled(v):
+    c = synth.CONFIGS[2]
+    lin = c.linears[0]
+    sampled_rows_check(v, lin.M, lin.K, 256, 4, seed=2000, p_zero=0.4)
+
+
+@pytest.mark.parametrize("N,g", [(256, 4), (1024, 5), (4096, 4), (1, 4), (16, 5)])
+def test_config4_full_size_sampled(v, N, g):
+    sampled_rows_check(v, 3072, 23040, N, g, seed=4000 + N, rows=12 if N >= 1024 else 32)
+
+
+@pytest.mark.parametrize("j", range(5))
+def test_config3_linears_sampled(v, j):
+    lin = synth.CONFIGS[3].linears[j]
+    sampled_rows_check(v, lin.M, lin.K, 1024, 4, seed=3000 + j, rows=8)
