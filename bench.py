@@ -1,0 +1,470 @@
+#!/usr/bin/env python
+"""bench.py -- Vec-LUT ternary mpGeMM on B200: the driver's benchmark contract.
+
+Workload (N=1 GPU): BASELINE.json configs[1], the BitNet-2B-shaped FFN-up
+ternary linear, M=6912, K=2560, N=256 tokens, g=4, weights iid with
+P(-1)=P(+1)=0.3, P(0)=0.4, per-tensor scale 0.02, activations N(0,1) fp32.
+One step = one pass of the hot path over one batch: per-token int8 quantize
+(a7, K3 kernel) -> fused Vec-LUT mpGeMM with fp32 dequant (a2-a6, K1 kernel)
+[-> NCCL all-gather of row shards (a8) when --gpus > 1].  Weights are packed
+once, offline (a1), before timing.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Prints ONE JSON line on rank 0.  Timing: CUDA events on the launching stream
+around each step's kernels; the L2 is flushed (256 MiB memset) between steps
+outside those windows; the sum of per-step durations is the timed total, max
+over ranks.  See DESIGN.md §Measurement.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2512_06443_b200 import synth  # noqa: E402
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+SM_COUNT = 148
+SMEM_BYTES_PER_CLK_SM = 128  # 32 banks x 4 B
+SM_MAX_MHZ_FALLBACK = 1965.0
+HBM_FALLBACK_GBS = 6650.0    # B200_PROFILING.md fallback
+
+
+def load_peaks():
+    try:
+        with open(MEASURED_PEAKS) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": HBM_FALLBACK_GBS, "sm_max_mhz": SM_MAX_MHZ_FALLBACK}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks (NVML)
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, torch_dev):
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self.ok = False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            # match the torch device to an NVML handle by UUID (the PCI-bus-id
+            # lookup segfaults in this pynvml build)
+            want = str(getattr(torch.cuda.get_device_properties(torch_dev), "uuid", "")).lower()
+            self.h = None
+            for i in range(pynvml.nvmlDeviceGetCount()):
+                h = pynvml.nvmlDeviceGetHandleByIndex(i)
+                u = pynvml.nvmlDeviceGetUUID(h)
+                u = (u.decode() if isinstance(u, bytes) else str(u)).lower()
+                if want and want in u:
+                    self.h = h
+                    break
+            if self.h is None:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(torch_dev.index or 0)
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # keep benchmarking; report the absence
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except Exception:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.reasons |= int(r)
+            except Exception:
+                pass
+            time.sleep(0.0005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "")}
+        rs = [name for bit, name in self.REASONS.items() if self.reasons & bit and bit != 0x1]
+        return {"sm_mhz": float(statistics.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": float(self.max_mhz), "reasons": rs, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ helpers
+def workload(args):
+    cfg = synth.CONFIGS[2]
+    lin = cfg.linears[0]
+    return dict(cfg=cfg, M=lin.M, K=lin.K, N=cfg.N[0], g=cfg.g[0], p_zero=cfg.p_zero,
+                w_seed=synth.weight_seed(cfg, 0, 0), x_seed=synth.act_seed(cfg, cfg.N[0]))
+
+
+def algorithmic(M, K, N, g):
+    lookups = M * (K // g) * N
+    return dict(lookups=lookups, smem_bytes=2 * lookups,
+                hbm_bytes=M * K // g + K * N + 4 * N + 4 * M * N, dense_ops=2 * M * K * N)
+
+
+# ------------------------------------------------------------------ CPU oracle leg
+def oracle_pipeline_rows(W, x, m0, m1, w_scale):
+    """The oracle's step on rows [m0, m1): quantize (all tokens) -> int32 dot
+    products -> fp32 dequant.  Test infrastructure, timed as the baseline."""
+    import oracle
+    q, s = oracle.quantize(x)
+    acc = np.zeros((W.shape[0], x.shape[1]), np.int32)
+    oracle.gemm_i32_rows(W, q, m0, m1, acc)
+    return oracle.dequant_f32(acc[m0:m1], s, w_scale)
+
+
+def cpu_baseline(W, x, N, budget_s=12.0, min_rows=32):
+    import oracle
+    oracle.build()
+    M = W.shape[0]
+    t0 = time.perf_counter()
+    oracle_pipeline_rows(W, x, 0, min_rows, synth.W_SCALE)
+    t_probe = time.perf_counter() - t0
+    per_row = t_probe / min_rows
+    rows = int(min(M, max(min_rows, budget_s / max(per_row, 1e-9))))
+    t0 = time.perf_counter()
+    done = 0
+    reps = 0
+    while True:
+        oracle_pipeline_rows(W, x, 0, rows, synth.W_SCALE)
+        done += rows
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or reps >= 50:
+            break
+    tok_s = N * (done / M) / el
+    return {"value": tok_s, "unit": "tokens/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"oracle quantize+int32 dot products+fp32 dequant on rows [0,{rows}) of "
+                      f"the {M}-row workload, {reps} pass(es), {el:.1f} s; tokens/s scaled by "
+                      f"rows/M", "seconds": el}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    wl = workload(args)
+    M, K, N, g = wl["M"], wl["K"], wl["N"], wl["g"]
+    W = synth.ternary_weights(M, K, wl["w_seed"], wl["p_zero"])
+    x = synth.activations_f32(K, N, wl["x_seed"])
+    import oracle
+    oracle.build()
+    # size each step so the whole run stays within ~2 minutes
+    t0 = time.perf_counter()
+    oracle_pipeline_rows(W, x, 0, 32, synth.W_SCALE)
+    per_row = (time.perf_counter() - t0) / 32
+    total_steps = args.steps + args.warmup
+    step_budget = min(2.0, 100.0 / max(total_steps, 1))
+    rows = int(min(M, max(8, step_budget / max(per_row, 1e-9))))
+    for _ in range(args.warmup):
+        oracle_pipeline_rows(W, x, 0, rows, synth.W_SCALE)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle_pipeline_rows(W, x, 0, rows, synth.W_SCALE)
+    el = time.perf_counter() - t0
+    sec_per_full_step = el / args.steps * (M / rows)
+    val = N / sec_per_full_step
+    line = {
+        "impl": "reference", "metric": "ternary Vec-LUT mpGeMM tokens/s (configs[1])",
+        "value": val, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sec_per_full_step * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "int32", "data": "synthetic",
+        "config": {"workload": "configs[1]: BitNet-2B FFN-up ternary linear", "M": M, "K": K,
+                   "N": N, "g": g},
+        "cpu_baseline": {"value": val, "unit": "tokens/s", "kind": "oracle",
+                         "cores": oracle.num_threads(),
+                         "sample": f"each step: oracle quantize + int32 dot products + fp32 "
+                                   f"dequant on rows [0,{rows}) of {M}; scaled by rows/M"},
+        "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="vlut", choices=["vlut", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the config 3/4 sweep")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="short run for ncu: no clock warm-up loop, no cpu/sweep/e2e legs")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    if args.profile:
+        args.no_cpu = args.no_sweep = args.no_e2e = True
+
+    import torch
+    import torch.distributed as dist
+    import paper_2512_06443_b200 as v
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream()
+
+    peaks, peaks_src = load_peaks()
+    wl = workload(args)
+    M, K, N, g = wl["M"], wl["K"], wl["N"], wl["g"]
+    alg = algorithmic(M, K, N, g)
+
+    # ---- offline: weights (row shard of this rank) packed on device (a1)
+    W = synth.ternary_weights(M, K, wl["w_seed"], wl["p_zero"])
+    assert M % world == 0
+    Ms = M // world
+    W_r = W[rank * Ms:(rank + 1) * Ms]
+    pw = v.pack_weights_device(torch.from_numpy(np.ascontiguousarray(W_r)).to(dev), g)
+    x_host = synth.activations_f32(K, N, wl["x_seed"])
+    x = torch.from_numpy(x_host).to(dev)
+    q = torch.empty((K, N), dtype=torch.int8, device=dev)
+    s = torch.empty((N,), dtype=torch.float32, device=dev)
+    out_r = torch.empty((Ms, N), dtype=torch.float32, device=dev)
+    out_full = torch.empty((M, N), dtype=torch.float32, device=dev) if world > 1 else out_r
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    plan = v.plan(Ms, K, N, g)
+
+    def step():
+        v.quantize(x, q=q, scale=s, stream=stream)
+        v.mpgemm(pw, q, s, synth.W_SCALE, out=out_r, stream=stream)
+        if world > 1:
+            dist.all_gather_into_tensor(out_full, out_r)
+
+    # ---- warm-up: W steps, plus >= 0.3 s of work so clocks leave idle
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    while not args.profile and time.perf_counter() - t0 < 0.3:
+        for _ in range(20):
+            step()
+        torch.cuda.synchronize()
+
+    # ---- timed region: exactly K steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush, outside the step's event window
+            e = evs[i]
+            e[0].record(stream)
+            v.quantize(x, q=q, scale=s, stream=stream)
+            e[1].record(stream)
+            v.mpgemm(pw, q, s, synth.W_SCALE, out=out_r, stream=stream)
+            e[2].record(stream)
+            if world > 1:
+                dist.all_gather_into_tensor(out_full, out_r)
+            e[3].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [e[0].elapsed_time(e[3]) for e in evs]
+    k1_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    k3_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms, float(np.mean(k1_ms))], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, k1_mean = float(t[0]), float(t[1])
+    else:
+        k1_mean = float(np.mean(k1_ms))
+    ms_per_step = total_ms / args.steps
+    value = N * args.steps / (total_ms * 1e-3)  # whole-job tokens/s (all M rows)
+
+    # ---- e2e through the public API from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        x_pin = torch.from_numpy(x_host).pin_memory()
+        o_pin = torch.empty((M, N), dtype=torch.float32).pin_memory()
+        e2e_steps = max(5, min(args.steps, 50))
+        for _ in range(3):
+            x.copy_(x_pin, non_blocking=True)
+            step()
+            o_pin.copy_(out_full, non_blocking=True)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(e2e_steps):
+            x.copy_(x_pin, non_blocking=True)
+            step()
+            o_pin.copy_(out_full, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = a.elapsed_time(b)
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t[0])
+        e2e = {"value": N * e2e_steps / (e2e_ms * 1e-3), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(x.numel() * 4),
+               "d2h_bytes_per_step": int(o_pin.numel() * 4), "steps": e2e_steps,
+               "ms_per_step": e2e_ms / e2e_steps}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel (K1)
+    a_shard = algorithmic(Ms, K, N, g)
+    sm_max = float(peaks.get("sm_max_mhz", SM_MAX_MHZ_FALLBACK))
+    smem_peak_gbs = SM_COUNT * SMEM_BYTES_PER_CLK_SM * sm_max * 1e6 / 1e9
+    achieved = a_shard["smem_bytes"] / (k1_mean * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "k1_dram_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {
+        "bound": "smem", "achieved": achieved, "peak": smem_peak_gbs, "unit": "GB/s",
+        "frac": achieved / smem_peak_gbs, "traffic": traffic,
+        "kernel": "vlut_mpgemm_kernel (K1)",
+        "algorithmic_bytes_per_launch": a_shard["smem_bytes"],
+        "per_unit": "2 B of shared-memory table read per int16 lookup-add; lookups = M*(K/g)*N",
+        "peak_source": f"derived: {SM_COUNT} SMs x {SMEM_BYTES_PER_CLK_SM} B/clk x "
+                       f"{sm_max:.0f} MHz (sm_max_mhz, {peaks_src})",
+        "k1_ms_mean": k1_mean, "k3_quantize_ms_mean": float(np.mean(k3_ms)),
+        "hbm_achieved_gbs": a_shard["hbm_bytes"] / (k1_mean * 1e-3) / 1e9,
+        "hbm_peak_gbs": float(peaks.get("hbm_gbs", HBM_FALLBACK_GBS)),
+        "lookups_per_s": a_shard["lookups"] / (k1_mean * 1e-3),
+    }
+
+    line = {
+        "metric": "ternary Vec-LUT mpGeMM tokens/s (configs[1])",
+        "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int16",
+        "dtype_detail": "int8 activations x ternary (base-3 packed) weights; int16 LUT "
+                        "lookup-adds, int32 accumulation, fp32 dequant",
+        "data": "synthetic",
+        "config": {"workload": "configs[1]: BitNet-2B FFN-up ternary linear", "M": M, "K": K,
+                   "N": N, "g": g, "weights": "iid ternary P(0)=0.4 P(+-1)=0.3, seeded",
+                   "activations": "N(0,1) fp32, per-token int8 absmax quantized on GPU",
+                   "step": "quantize (K3) + fused Vec-LUT mpGeMM + fp32 dequant (K1)"
+                           + (" + NCCL all-gather of row shards" if world > 1 else ""),
+                   "parallelism": f"row-shard M over {world} GPU(s)" if world > 1 else "single GPU",
+                   "plan": plan.__dict__,
+                   "l2": "flushed between steps (256 MiB memset outside each step's event window)"},
+        "gops": alg["dense_ops"] * args.steps / (total_ms * 1e-3) / 1e9,
+        "gpu_launches": args.steps * 2,
+        "roofline": roofline,
+        "e2e": e2e,
+    }
+    clocks = clk.summary()
+    line["clocks"] = clocks
+
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(W, x_host, N)
+
+    if world == 1 and not args.no_sweep:
+        line["sweep"] = sweep(v, dev, stream, flush)
+
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def sweep(v, dev, stream, flush, reps=10):
+    """Configs 3 and 4 (BASELINE.json configs[2], configs[3]): K1 alone on
+    resident int8 inputs, L2 flushed between launches; N = 256..4096."""
+    import torch
+    R_LU = SM_COUNT * 64 * SM_MAX_MHZ_FALLBACK * 1e6
+    res = []
+
+    def timeit(pw, A, sc, out):
+        for _ in range(2):
+            v.mpgemm(pw, A, sc, synth.W_SCALE, out=out, stream=stream)
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            v.mpgemm(pw, A, sc, synth.W_SCALE, out=out, stream=stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) * 1e-3)
+        return float(np.median(ts))
+
+    c4 = synth.CONFIGS[4]
+    lin = c4.linears[0]
+    W4 = torch.from_numpy(synth.ternary_weights(lin.M, lin.K, synth.weight_seed(c4, 0, 0))).to(dev)
+    for g in (4, 5):
+        pw = v.pack_weights_device(W4, g)
+        for N in c4.N:
+            x = torch.from_numpy(synth.activations_f32(lin.K, N, synth.act_seed(c4, N))).to(dev)
+            A, sc = v.quantize(x)
+            out = torch.empty((lin.M, N), dtype=torch.float32, device=dev)
+            t = timeit(pw, A, sc, out)
+            lk = lin.M * (lin.K // g) * N
+            res.append({"config": 4, "M": lin.M, "K": lin.K, "N": N, "g": g, "us": t * 1e6,
+                        "tokens_s": N / t, "gops": 2 * lin.M * lin.K * N / t / 1e9,
+                        "frac_smem_roofline": lk / R_LU / t})
+        del pw
+    c3 = synth.CONFIGS[3]
+    tot = 0.0
+    for j, lin in enumerate(c3.linears):
+        Wd = torch.from_numpy(synth.ternary_weights(lin.M, lin.K, synth.weight_seed(c3, 0, j))).to(dev)
+        pw = v.pack_weights_device(Wd, 4)
+        x = torch.from_numpy(synth.activations_f32(lin.K, 1024, synth.act_seed(c3, 1024, j))).to(dev)
+        A, sc = v.quantize(x)
+        out = torch.empty((lin.M, 1024), dtype=torch.float32, device=dev)
+        t = timeit(pw, A, sc, out)
+        tot += t
+        lk = lin.M * (lin.K // 4) * 1024
+        res.append({"config": 3, "linear": lin.name, "M": lin.M, "K": lin.K, "N": 1024, "g": 4,
+                    "us": t * 1e6, "frac_smem_roofline": lk / R_LU / t})
+    res.append({"config": 3, "linear": "all 5 in sequence", "N": 1024, "us": tot * 1e6,
+                "tokens_s": 1024 / tot})
+    return res
+
+
+if __name__ == "__main__":
+    sys.exit(main())
