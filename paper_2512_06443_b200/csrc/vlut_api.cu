@@ -409,9 +409,32 @@ vlut_status vlut_quantize(const float* x, const float* y, int K, int N, int8_t* 
   if (K == 0 || N == 0) return ok();
   if (!x || !q || !scale) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const unsigned blocks = (unsigned)((N + 31) / 32);
-  vlut::vlut_quantize_kernel<<<blocks, vlut::kQuantWarps * 32, 0, s>>>(x, y, K, N, q, scale);
-  VLUT_CUDA_TRY(cudaGetLastError());
+  // cluster size along K: enough CTAs that every row fits the register cache
+  // when possible (<= 8, portable), and >= ~2 waves of CTAs over the GPU.
+  const long long tok_blocks = (N + vlut::kQTok - 1) / vlut::kQTok;
+  int CL = 1;
+  while (CL < 8 && ((long long)K > (long long)CL * 64 * vlut::kQCache || tok_blocks * CL < 296))
+    CL *= 2;
+  if (CL > K) CL = 1;
+  if (tok_blocks > 65535) return fail(VLUT_ERR_SHAPE, "N too large");
+  const bool aligned = (N % 4 == 0) && ((((uintptr_t)x) | ((uintptr_t)(y ? y : x))) & 15) == 0 &&
+                       (((uintptr_t)q) & 3) == 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)CL, (unsigned)tok_blocks, 1);
+  cfg.blockDim = dim3(vlut::kQThreads, 1, 1);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (aligned)
+    VLUT_CUDA_TRY(cudaLaunchKernelEx(&cfg, vlut::vlut_quantize_kernel<true>, x, y, K, N, q, scale));
+  else
+    VLUT_CUDA_TRY(cudaLaunchKernelEx(&cfg, vlut::vlut_quantize_kernel<false>, x, y, K, N, q, scale));
   return ok();
 }
 

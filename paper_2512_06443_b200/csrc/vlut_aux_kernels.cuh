@@ -1,65 +1,140 @@
 // vlut_aux_kernels.cuh -- K3 per-token quantizer and the device-side packer.
 #pragma once
 #include <cstdint>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 namespace vlut {
 
 // ---------------------------------------------------------------- K3 quantize (a7)
-// One CTA owns 32 tokens (one warp-width of contiguous fp32 columns) and all K
-// rows: pass 1 computes the per-token absmax (each warp strides over rows,
-// 128-byte coalesced row segments, 8 loads in flight), pass 2 re-reads (from
-// L2) and writes int8 codes.  IEEE single ops only (no fast math):
-// s = amax / 127 (1 if amax == 0), q = clamp(roundf(x / s), -127, 127).
-constexpr int kQuantWarps = 16;
+// A thread-block cluster of CL CTAs owns 16 consecutive tokens; CTA `rank`
+// owns a contiguous 1/CL slice of the K rows.  Each thread loads float4s
+// (4 tokens of one row; 4 threads cover a row's 64 contiguous bytes) into
+// registers, the per-token absmax is reduced warp -> CTA -> cluster (DSMEM),
+// and the codes are written from the registers (rows beyond the register
+// cache are re-read).  IEEE single ops only (no fast math):
+//   s = amax / 127 (1 if amax == 0), q = clamp(roundf(x / s), -127, 127).
+constexpr int kQThreads = 256;   // 64 rows x 4 float4 columns per pass
+constexpr int kQTok = 16;        // tokens per cluster
+constexpr int kQCache = 12;      // float4 register cache per thread
 
-__global__ void __launch_bounds__(kQuantWarps * 32)
+template <bool ALIGNED>
+__device__ __forceinline__ float4 q_load(const float* x, const float* y, int k, int N, int n) {
+  const size_t o = (size_t)k * N + n;
+  float4 a;
+  if (ALIGNED && n + 3 < N) {
+    a = __ldg(reinterpret_cast<const float4*>(x + o));
+    if (y) {
+      const float4 b = __ldg(reinterpret_cast<const float4*>(y + o));
+      a.x = __fmul_rn(a.x, b.x); a.y = __fmul_rn(a.y, b.y);
+      a.z = __fmul_rn(a.z, b.z); a.w = __fmul_rn(a.w, b.w);
+    }
+  } else {
+    float t[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      t[i] = 0.f;
+      if (n + i < N) t[i] = y ? __fmul_rn(__ldg(x + o + i), __ldg(y + o + i)) : __ldg(x + o + i);
+    }
+    a = make_float4(t[0], t[1], t[2], t[3]);
+  }
+  return a;
+}
+
+__device__ __forceinline__ int8_t q_code(float v, float s) {
+  float r = roundf(__fdiv_rn(v, s));
+  r = fminf(fmaxf(r, -127.f), 127.f);
+  return (int8_t)r;
+}
+
+template <bool ALIGNED>
+__global__ void __launch_bounds__(kQThreads)
     vlut_quantize_kernel(const float* __restrict__ x, const float* __restrict__ y, int K, int N,
                          int8_t* __restrict__ q, float* __restrict__ scale) {
-  __shared__ float red[kQuantWarps][32];
-  __shared__ float s_scale[32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int n = blockIdx.x * 32 + lane;
-  const bool ok = n < N;
-  float amax = 0.f;
-  if (ok) {
-    int k = warp;
-    for (; k + 7 * kQuantWarps < K; k += 8 * kQuantWarps) {
-      float v[8];
+  __shared__ float red[kQThreads / 32][kQTok];
+  __shared__ float cta_amax[kQTok];
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CL = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int col = tid & 3;              // float4 column within the 16 tokens
+  const int rsub = tid >> 2;            // row within a 64-row pass
+  const int n = blockIdx.y * kQTok + col * 4;
+  const int k_begin = (int)(((long long)rank * K) / CL);
+  const int k_end = (int)(((long long)(rank + 1) * K) / CL);
+  float4 cache[kQCache];
+  float m[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const size_t o = (size_t)(k + i * kQuantWarps) * N + n;
-        v[i] = y ? __fmul_rn(__ldg(x + o), __ldg(y + o)) : __ldg(x + o);
-      }
+  for (int i = 0; i < kQCache; ++i) {
+    const int k = k_begin + rsub + 64 * i;
+    cache[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (k < k_end && n < N) cache[i] = q_load<ALIGNED>(x, y, k, N, n);
+  }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) amax = fmaxf(amax, fabsf(v[i]));
-    }
-    for (; k < K; k += kQuantWarps) {
+  for (int i = 0; i < kQCache; ++i) {
+    m[0] = fmaxf(m[0], fabsf(cache[i].x)); m[1] = fmaxf(m[1], fabsf(cache[i].y));
+    m[2] = fmaxf(m[2], fabsf(cache[i].z)); m[3] = fmaxf(m[3], fabsf(cache[i].w));
+  }
+  for (int k = k_begin + rsub + 64 * kQCache; k < k_end; k += 64) {
+    if (n >= N) break;
+    const float4 a = q_load<ALIGNED>(x, y, k, N, n);
+    m[0] = fmaxf(m[0], fabsf(a.x)); m[1] = fmaxf(m[1], fabsf(a.y));
+    m[2] = fmaxf(m[2], fabsf(a.z)); m[3] = fmaxf(m[3], fabsf(a.w));
+  }
+  // warp: lanes with equal (lane & 3) share tokens -> reduce over lane bits 2..4
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int d = 4; d < 32; d <<= 1) m[i] = fmaxf(m[i], __shfl_xor_sync(0xffffffffu, m[i], d));
+  if (lane < 4) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) red[warp][lane * 4 + i] = m[i];
+  }
+  __syncthreads();
+  if (tid < kQTok) {
+    float a = red[0][tid];
+#pragma unroll
+    for (int w = 1; w < kQThreads / 32; ++w) a = fmaxf(a, red[w][tid]);
+    cta_amax[tid] = a;
+  }
+  cluster.sync();
+  float s[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float a = 0.f;
+    for (int r = 0; r < CL; ++r) a = fmaxf(a, cluster.map_shared_rank(cta_amax, r)[col * 4 + i]);
+    s[i] = (a == 0.f) ? 1.f : __fdiv_rn(a, 127.f);
+  }
+  if (rank == 0 && rsub == 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (n + i < N) scale[n + i] = s[i];
+  }
+#pragma unroll
+  for (int i = 0; i < kQCache; ++i) {
+    const int k = k_begin + rsub + 64 * i;
+    if (k < k_end && n < N) {
       const size_t o = (size_t)k * N + n;
-      const float v = y ? __fmul_rn(__ldg(x + o), __ldg(y + o)) : __ldg(x + o);
-      amax = fmaxf(amax, fabsf(v));
+      const int8_t c0 = q_code(cache[i].x, s[0]), c1 = q_code(cache[i].y, s[1]);
+      const int8_t c2 = q_code(cache[i].z, s[2]), c3 = q_code(cache[i].w, s[3]);
+      if (ALIGNED && n + 3 < N) {
+        const uint32_t packed = (uint32_t)(uint8_t)c0 | ((uint32_t)(uint8_t)c1 << 8) |
+                                ((uint32_t)(uint8_t)c2 << 16) | ((uint32_t)(uint8_t)c3 << 24);
+        *reinterpret_cast<uint32_t*>(q + o) = packed;
+      } else {
+        const int8_t c[4] = {c0, c1, c2, c3};
+        for (int t = 0; t < 4 && n + t < N; ++t) q[o + t] = c[t];
+      }
     }
   }
-  red[warp][lane] = amax;
-  __syncthreads();
-  if (warp == 0) {
-    float m = red[0][lane];
-#pragma unroll
-    for (int w = 1; w < kQuantWarps; ++w) m = fmaxf(m, red[w][lane]);
-    const float s = (m == 0.f) ? 1.f : __fdiv_rn(m, 127.f);
-    s_scale[lane] = s;
-    if (ok) scale[n] = s;
+  for (int k = k_begin + rsub + 64 * kQCache; k < k_end; k += 64) {
+    if (n >= N) break;
+    const float4 a = q_load<ALIGNED>(x, y, k, N, n);
+    const float v[4] = {a.x, a.y, a.z, a.w};
+    for (int t = 0; t < 4 && n + t < N; ++t) q[(size_t)k * N + n + t] = q_code(v[t], s[t]);
   }
-  __syncthreads();
-  if (!ok) return;
-  const float s = s_scale[lane];
-  for (int k = warp; k < K; k += kQuantWarps) {
-    const size_t o = (size_t)k * N + n;
-    const float v = y ? __fmul_rn(__ldg(x + o), __ldg(y + o)) : __ldg(x + o);
-    float r = roundf(__fdiv_rn(v, s));
-    r = fminf(fmaxf(r, -127.f), 127.f);
-    q[o] = (int8_t)r;
-  }
+  cluster.sync();  // keep cta_amax alive until every CTA of the cluster read it
 }
 
 // ---------------------------------------------------------------- device packer (a1)
