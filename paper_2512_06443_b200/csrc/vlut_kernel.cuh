@@ -3,27 +3,32 @@
 // One CTA owns an (M-block of 32*WARPS rows) x (N-tile of 64 tokens) output
 // tile and a contiguous range of K-tiles (16 weight groups each).  The CTAs
 // of one thread-block cluster (size S along K) split the K range and reduce
-// their int32 partials through distributed shared memory.  Per K-tile:
+// their int32 partials through distributed shared memory.
 //
-//   a2  cp.async stages the K-tile's activation rows A[16g][64] (int8) and
-//       the CTA rows' 16-byte index vectors into shared memory, one K-tile
-//       ahead of use (double-buffered).
-//   a3  every warp builds whole sub-tables T[i][0:64] (Eq. 1) of the
-//       K-tile's groups in shared memory, in the topological order of P:503-513:
-//       one +/- row operation per table row, walking a base-3 reflected Gray
-//       code over the low g-1 trits (the top trit splits a table into three
-//       independent 3^(g-1)-row chains, one per warp task).  Rows are stored
-//       token-contiguous, 128 B per row = 64 tokens x int16, as
-//       biased 16-bit fields two tokens per 32-bit word:  field = T + 128 g.
-//   a4  each thread owns ONE output row and all 64 tokens of the tile.  For
-//       every group it reads its row's index byte and performs the 1->N vector
-//       lookup (Alg. 1) as 8 LDS.128 of the indexed table row,
-//       visiting the 16-byte chunks in the lane-rotated order (lane+s) mod 8:
-//       the 8 lanes of an LDS.128 phase then always hit 8 different bank
-//       groups whatever rows the data-dependent indices select (no bank
-//       conflicts).  Two groups are summed per IADD3 into 16-bit SWAR fields
-//       (INT16 intra-block accumulation); the fields are widened
-//       into int32 registers every 48 groups (48 * 256 g <= 65535).
+//   a2  cp.async stages each K-tile's activation rows A[16g][64] (int8) and
+//       the CTA rows' 16-byte index vectors into shared memory, triple
+//       buffered, one K-tile ahead of its first use.
+//   a3  sub-tables (Eq. 1) are built in shared memory in the
+//       topological order of P:503-513 (one +/- row op per row, along base-3
+//       reflected Gray codes).  Only the upper half of each table is stored:
+//       T[i] = -T[3^g-1-i] (negating all trits negates the dot product), so
+//       rows i >= z = (3^g-1)/2 are kept at position i - z ((3^g+1)/2 rows:
+//       41 for g=4, 122 for g=5) and a lookup of i < z reads position z - i
+//       and negates.  Rows are token-contiguous, 128 B = 64 tokens
+//       x int16, stored as biased 16-bit fields two tokens per 32-bit word:
+//       field = T + 128 g  (in [0, 256 g] for any int8 input).
+//       Tables are double buffered: while the CTA looks up sub-stage u it
+//       builds sub-stage u+1, with ONE barrier per sub-stage.
+//   a4  each thread owns ONE output row and all 64 tokens of the tile.  Per
+//       group it turns its index byte into (position, sign) and performs the
+//       1->N vector lookup (Alg. 1) as 8 LDS.128 of the row, in
+//       the lane-rotated chunk order (lane+s) mod 8: the 8 lanes of an
+//       LDS.128 phase always hit 8 different bank groups, whatever rows the
+//       data-dependent indices select.  Words are accumulated into 16-bit SWAR
+//       fields (INT16 intra-block accumulation): negated lookups
+//       add (w ^ -1) [ALU] or w * -1 [FMA pipe], with a per-row count of
+//       negations that restores 2*bias - field at the widening step; fields
+//       are widened into int32 registers every 48 groups (48 * 256 g < 2^16).
 //   a5  after the K range: int32 tile -> shared memory (XOR-swizzled, conflict
 //       free), cluster barrier, each CTA of the cluster sums 1/S of the rows
 //       over all S CTAs via DSMEM.
@@ -45,34 +50,44 @@ constexpr int kNcta = 64;             // tokens per CTA (N-tile)
 constexpr int kKgTile = 16;           // groups per K-tile (16-byte index vector)
 constexpr int kRowBytes = kNcta * 2;  // one table row: 64 tokens x int16
 constexpr int kFlushTiles = 3;        // widen SWAR fields every 3 K-tiles = 48 groups
+constexpr int kStageBufs = 3;         // A / index staging buffers
 
 __host__ __device__ constexpr int pow3(int g) { return g == 0 ? 1 : 3 * pow3(g - 1); }
 
 template <int G>
 struct Cfg {
-  static constexpr int R = pow3(G);             // table rows 3^g
-  static constexpr int RP = R / 3;              // rows per chain (top trit fixed)
+  static constexpr int R = pow3(G);             // full table rows 3^g
+  static constexpr int ZERO = (R - 1) / 2;      // index of the all-zero pattern
+  static constexpr int HR = (R + 1) / 2;        // stored (half) rows
   static constexpr int GS = (G == 4) ? 16 : 4;  // groups per table sub-stage
   static constexpr int SUBS = kKgTile / GS;     // sub-stages per K-tile
   static constexpr int BIAS = 128 * G;          // field bias: T + BIAS in [0, 256 g]
-  static constexpr int TAB_BYTES = GS * R * kRowBytes;
+  static constexpr int TAB_BYTES = GS * HR * kRowBytes;  // one table buffer
   static constexpr int A_ROWS = kKgTile * G;    // activation rows per K-tile
   static constexpr int A_BYTES = A_ROWS * kNcta;
   static constexpr int IDX_MASK = (G == 4) ? 0x7F : 0xFF;
   static_assert(kFlushTiles * kKgTile * 2 * BIAS <= 65535, "SWAR field overflow");
 };
 
+// WARPS lookup warps (one output row per thread) + kBuilderWarps table
+// builders; threads = 32 * (WARPS + kBuilderWarps).
+constexpr int kBuilderWarps = 4;
+constexpr int kTmemCols = 256;  // int32 accumulators: 64 columns per 4 lookup warps
+
 template <int G, int WARPS>
 struct Layout {
-  static constexpr int THREADS = WARPS * 32;
-  static constexpr int MCTA = THREADS;                    // one output row per thread
+  static constexpr int THREADS = (WARPS + kBuilderWarps) * 32;
+  static constexpr int BUILDER0 = WARPS * 32;             // first builder thread
+  static constexpr int MCTA = WARPS * 32;                 // output rows per CTA
   static constexpr int RED_BYTES = MCTA * kNcta * 4;      // int32 reduction tile
-  static constexpr int TAB_REGION =
-      Cfg<G>::TAB_BYTES > RED_BYTES ? Cfg<G>::TAB_BYTES : RED_BYTES;
+  static constexpr int TAB_REGION = 2 * Cfg<G>::TAB_BYTES > RED_BYTES
+                                        ? 2 * Cfg<G>::TAB_BYTES : RED_BYTES;
   static constexpr int IDX_OFF = TAB_REGION;
   static constexpr int IDX_BYTES = MCTA * 16;
-  static constexpr int A_OFF = IDX_OFF + 2 * IDX_BYTES;
-  static constexpr int SMEM = A_OFF + 2 * Cfg<G>::A_BYTES;
+  static constexpr int A_OFF = IDX_OFF + kStageBufs * IDX_BYTES;
+  static constexpr int MISC_OFF = A_OFF + kStageBufs * Cfg<G>::A_BYTES;  // tmem address
+  static constexpr int SMEM = MISC_OFF + 16;
+  static_assert(WARPS <= 16, "TMEM columns: at most 4 column blocks of 64");
 };
 
 // ---------------------------------------------------------------- Gray walk
@@ -157,6 +172,47 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
+// ---------------------------------------------------------------- named barriers
+// id 0: __syncthreads; 1,2: table buffer FULL; 3,4: table buffer EMPTY;
+// 5: builders only.
+__device__ __forceinline__ void bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+
+// ---------------------------------------------------------------- TMEM helpers
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16};\n" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+
 // ---------------------------------------------------------------- params
 struct Params {
   const uint8_t* payload;  // packed indices [kt][m_pad][16]
@@ -172,24 +228,25 @@ struct Params {
 };
 
 // ---------------------------------------------------------------- staging (a2)
+// Issued by the builder threads (bt in [0, 128)); one commit group per tile.
 template <int G, int WARPS>
 __device__ __forceinline__ void stage_tile(const Params& p, int kt, int buf, int m0, int n0,
-                                           uint8_t* smem) {
+                                           uint8_t* smem, int bt) {
   using C = Cfg<G>;
   using L = Layout<G, WARPS>;
-  const int tid = threadIdx.x;
-  // index vectors: one 16-byte row per thread (rows past m_pad -> zero fill)
-  {
-    const int m = m0 + tid;
+  constexpr int NB = kBuilderWarps * 32;
+  // index vectors: one 16-byte row per CTA row (rows past m_pad -> zero fill)
+  for (int r = bt; r < L::MCTA; r += NB) {
+    const int m = m0 + r;
     const bool ok = m < p.m_pad;
     const uint8_t* src = ok ? p.payload + ((size_t)kt * p.m_pad + m) * 16 : p.payload;
-    cp_async16(smem_u32(smem + L::IDX_OFF + buf * L::IDX_BYTES + tid * 16), src, ok ? 16 : 0);
+    cp_async16(smem_u32(smem + L::IDX_OFF + buf * L::IDX_BYTES + r * 16), src, ok ? 16 : 0);
   }
   // activation rows k0 .. k0 + 16g - 1, tokens n0 .. n0+63 (past K or N -> 0)
   const int k0 = kt * kKgTile * G;
   uint8_t* a_s = smem + L::A_OFF + buf * C::A_BYTES;
   if (p.a_vec == 16) {
-    for (int c = tid; c < C::A_ROWS * 4; c += L::THREADS) {
+    for (int c = bt; c < C::A_ROWS * 4; c += NB) {
       const int row = c >> 2, part = c & 3;
       const int k = k0 + row, n = n0 + part * 16;
       const bool ok = (k < p.K) && (n < p.N);
@@ -197,7 +254,7 @@ __device__ __forceinline__ void stage_tile(const Params& p, int kt, int buf, int
       cp_async16(smem_u32(a_s + row * kNcta + part * 16), src, ok ? 16 : 0);
     }
   } else if (p.a_vec == 4) {
-    for (int c = tid; c < C::A_ROWS * 16; c += L::THREADS) {
+    for (int c = bt; c < C::A_ROWS * 16; c += NB) {
       const int row = c >> 4, part = c & 15;
       const int k = k0 + row, n = n0 + part * 4;
       const bool ok = (k < p.K) && (n < p.N);
@@ -205,71 +262,169 @@ __device__ __forceinline__ void stage_tile(const Params& p, int kt, int buf, int
       cp_async4(smem_u32(a_s + row * kNcta + part * 4), src, ok ? 4 : 0);
     }
   } else {
-    for (int c = tid; c < C::A_ROWS * kNcta; c += L::THREADS) {
+    for (int c = bt; c < C::A_ROWS * kNcta; c += NB) {
       const int row = c / kNcta, col = c % kNcta;
       const int k = k0 + row, n = n0 + col;
       a_s[row * kNcta + col] = (k < p.K && n < p.N) ? (uint8_t)p.A[(size_t)k * p.N + n] : 0;
     }
   }
+  cp_async_commit();
 }
 
 // ---------------------------------------------------------------- table build (a3)
-// Walk the Gray code over the low D = g-1 trits, starting from T (row `base`).
+// Walk the Gray code over D digits from the start row already in T.
 template <int D, int S>
 __device__ __forceinline__ void gray_walk(uint32_t row_addr0, uint32_t T, const uint32_t (&P)[8],
                                           const uint32_t (&Mn)[8]) {
-  constexpr GrayWalk<D> gw{};
-  constexpr int dig = gw.digit[S];
-  constexpr int dir = gw.dir[S];
-  constexpr int idx = gw.idx[S];
-  T += (dir > 0) ? P[dig] : Mn[dig];
-  sts32(row_addr0 + idx * kRowBytes, T);
-  if constexpr (S + 1 < pow3(D)) gray_walk<D, S + 1>(row_addr0, T, P, Mn);
+  if constexpr (D > 0 && S < pow3(D)) {
+    constexpr GrayWalk<D> gw{};
+    constexpr int dig = gw.digit[S];
+    constexpr int dir = gw.dir[S];
+    constexpr int idx = gw.idx[S];
+    T += (dir > 0) ? P[dig] : Mn[dig];
+    sts32(row_addr0 + idx * kRowBytes, T);
+    gray_walk<D, S + 1>(row_addr0, T, P, Mn);
+  }
 }
 
-template <int G, int WARPS>
-__device__ __forceinline__ void build_tables(uint32_t tab_s, uint32_t a_s, int sub) {
+// Half table: position 0 = the zero pattern; block Lv (Lv = 0..g-1) = the
+// patterns whose trits above Lv are 0, trit Lv = +1, trits below free; it
+// occupies positions [(3^Lv+1)/2, (3^(Lv+1)+1)/2), position = (3^Lv+1)/2 +
+// (base-3 value of the free digits d_0..d_{Lv-1}, d = trit + 1).
+template <int G, int Lv>
+__device__ __forceinline__ void build_blocks(uint32_t row0, uint32_t S, const uint32_t (&U)[8],
+                                             const uint32_t (&P)[8], const uint32_t (&Mn)[8]) {
+  if constexpr (Lv < G) {
+    constexpr uint32_t K1 = 0x00010001u;
+    constexpr uint32_t C128 = 128u * K1;
+    // start: trit Lv = +1, trits below = -1:  T = BIAS + a_Lv - sum_{r<Lv} a_r
+    const uint32_t T = (uint32_t)Cfg<G>::BIAS * K1 + U[Lv] - C128 - S + (uint32_t)Lv * C128;
+    const uint32_t base = row0 + (uint32_t)(((pow3(Lv) + 1) / 2) * kRowBytes);
+    sts32(base, T);
+    gray_walk<Lv, 1>(base, T, P, Mn);
+    build_blocks<G, Lv + 1>(row0, S + U[Lv], U, P, Mn);
+  }
+}
+
+// Builder warp bw (of kBuilderWarps) builds the half tables of its groups of
+// sub-stage [grp0, grp0 + GS) of the staged K-tile.
+template <int G>
+__device__ __forceinline__ void build_tables(uint32_t tab_s, uint32_t a_s, int grp0, int bw,
+                                             int lane) {
   using C = Cfg<G>;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr uint32_t K1 = 0x00010001u;
   constexpr uint32_t C128 = 128u * K1;
 #pragma unroll 1
-  for (int u = warp; u < C::GS * 3; u += WARPS) {
-    const int j = u / 3;        // group within sub-stage
-    const int part = u - 3 * j; // value of the top trit
-    const int grp = sub * C::GS + j;  // group within the K-tile
-    uint32_t P[8], Mn[8];
-    uint32_t sumU = 0;
+  for (int j = bw; j < C::GS; j += kBuilderWarps) {
+    uint32_t U[8], P[8], Mn[8];
 #pragma unroll
     for (int r = 0; r < G; ++r) {
-      // tokens 2*lane, 2*lane+1 of activation row grp*g + r
-      uint32_t x = lds_u16(a_s + (grp * G + r) * kNcta + 2 * lane);
+      // tokens 2*lane, 2*lane+1 of activation row (grp0+j)*g + r
+      const uint32_t x = lds_u16(a_s + ((grp0 + j) * G + r) * kNcta + 2 * lane);
       // int8 a -> u = a + 128 (XOR 0x80), spread the two bytes into 16-bit fields
-      uint32_t U = __byte_perm(x ^ 0x8080u, 0u, 0x4140);
-      P[r] = U - C128;   // +a_r as packed arithmetic delta
-      Mn[r] = C128 - U;  // -a_r
-      if (r < G - 1) sumU += U;
+      U[r] = __byte_perm(x ^ 0x8080u, 0u, 0x4140);
+      P[r] = U[r] - C128;   // +a_r as a packed arithmetic delta
+      Mn[r] = C128 - U[r];  // -a_r
     }
-    // start row: trits 0..g-2 = -1, top trit = part - 1
-    //   T = BIAS + sum_{r<g-1} (-a_r) + (part-1) a_{g-1}
-    uint32_t T = (uint32_t)C::BIAS * K1 - sumU + (uint32_t)(G - 1) * C128;
-    if (part == 0) T += Mn[G - 1];
-    if (part == 2) T += P[G - 1];
-    const uint32_t row0 = tab_s + (uint32_t)((j * C::R + part * C::RP) * kRowBytes) + 4 * lane;
-    sts32(row0, T);
-    gray_walk<G - 1, 1>(row0, T, P, Mn);
+    const uint32_t row0 = tab_s + (uint32_t)(j * C::HR * kRowBytes) + 4 * lane;
+    sts32(row0, (uint32_t)C::BIAS * K1);  // the zero pattern
+    build_blocks<G, 0>(row0, 0u, U, P, Mn);
   }
+}
+
+// ---------------------------------------------------------------- lookups (a4)
+// Groups [SUB*GS, SUB*GS+GS) of the K-tile whose index vector is iwa.
+template <int G>
+__device__ __forceinline__ void lookup_sub(const int SUB, uint32_t tab, const uint32_t (&iwa)[4],
+                                           const uint32_t (&rot)[8], uint32_t (&sw)[8][4],
+                                           int32_t& nneg) {
+  using C = Cfg<G>;
+#pragma unroll
+  for (int jp = 0; jp < C::GS / 2; ++jp) {
+    const int b0 = SUB * C::GS + 2 * jp, b1 = b0 + 1;  // index bytes in the K-tile
+    const int i0 = (int)((iwa[b0 >> 2] >> (8 * (b0 & 3))) & C::IDX_MASK);
+    const int i1 = (int)((iwa[b1 >> 2] >> (8 * (b1 & 3))) & C::IDX_MASK);
+    const int d0 = i0 - C::ZERO, d1 = i1 - C::ZERO;
+    const uint32_t m0 = (uint32_t)(d0 >> 31), m1 = (uint32_t)(d1 >> 31);  // 0 or ~0: negate
+    const uint32_t p0 = (uint32_t)((d0 ^ (int)m0) - (int)m0);              // |d|
+    const uint32_t p1 = (uint32_t)((d1 ^ (int)m1) - (int)m1);
+    nneg += (int)m0 + (int)m1;  // minus the number of negated lookups
+    const uint32_t sg0 = m0 | 1u, sg1 = m1 | 1u;  // +1 / -1
+    const uint32_t r0 = tab + (uint32_t)((2 * jp) * C::HR * kRowBytes) + p0 * kRowBytes;
+    const uint32_t r1 = tab + (uint32_t)((2 * jp + 1) * C::HR * kRowBytes) + p1 * kRowBytes;
+    uint4 v0[8], v1[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      v0[s] = lds128(r0 + rot[s]);
+      v1[s] = lds128(r1 + rot[s]);
+    }
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      if (s < 4) {  // ALU pipe: XOR-negate, two groups per IADD3
+        sw[s][0] += (v0[s].x ^ m0) + (v1[s].x ^ m1);
+        sw[s][1] += (v0[s].y ^ m0) + (v1[s].y ^ m1);
+        sw[s][2] += (v0[s].z ^ m0) + (v1[s].z ^ m1);
+        sw[s][3] += (v0[s].w ^ m0) + (v1[s].w ^ m1);
+      } else {      // FMA pipe: multiply-negate
+        sw[s][0] += v0[s].x * sg0 + v1[s].x * sg1;
+        sw[s][1] += v0[s].y * sg0 + v1[s].y * sg1;
+        sw[s][2] += v0[s].z * sg0 + v1[s].z * sg1;
+        sw[s][3] += v0[s].w * sg0 + v1[s].w * sg1;
+      }
+    }
+  }
+}
+
+// Widen the SWAR fields into the int32 accumulators held in TMEM (INT16 ->
+// INT32).  A negated lookup contributed ~w (s < 4) or -w (s >= 4)
+// instead of the packed 2*BIAS - field; add the difference back per negation
+// before splitting the fields.  TMEM column 8*s + t of this thread's lane
+// holds token slot (s, t); `first` initialises instead of accumulating.
+template <int G>
+__device__ __forceinline__ void flush_tmem(uint32_t (&sw)[8][4], int32_t& nneg, uint32_t taddr,
+                                           bool first) {
+  constexpr uint32_t K1 = 0x00010001u;
+  const uint32_t cnt = (uint32_t)(-nneg);
+  const uint32_t corr_xor = cnt * (2u * Cfg<G>::BIAS * K1 + 1u);
+  const uint32_t corr_mul = cnt * (2u * Cfg<G>::BIAS * K1);
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {  // slots 2h, 2h+1 -> 16 columns
+    uint32_t v[16];
+    if (!first) {
+      tmem_ld16(taddr + 16 * h, v);
+      tmem_wait_ld();
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = 0;
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int s = 2 * h + e;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t w = sw[s][q] + (s < 4 ? corr_xor : corr_mul);
+        v[8 * e + 2 * q] += w & 0xFFFFu;
+        v[8 * e + 2 * q + 1] += w >> 16;
+        sw[s][q] = 0;
+      }
+    }
+    tmem_st16(taddr + 16 * h, v);
+  }
+  tmem_wait_st();
+  nneg = 0;
 }
 
 // ---------------------------------------------------------------- the kernel
 template <int G, int WARPS, bool ACC_ONLY>
-__global__ void __launch_bounds__(WARPS * 32, 1) vlut_mpgemm_kernel(const Params p) {
+__global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
+    vlut_mpgemm_kernel(const Params p) {
   using C = Cfg<G>;
   using L = Layout<G, WARPS>;
   extern __shared__ __align__(1024) uint8_t smem[];
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
+  const int warp = tid >> 5;
   const int rank = blockIdx.x;  // split index (== rank in cluster)
   const int n0 = blockIdx.y * kNcta;
   const int m0 = blockIdx.z * L::MCTA;
@@ -277,112 +432,132 @@ __global__ void __launch_bounds__(WARPS * 32, 1) vlut_mpgemm_kernel(const Params
   const int kt_begin = (int)(((long long)rank * p.kg_tiles) / S);
   const int kt_end = (int)(((long long)(rank + 1) * p.kg_tiles) / S);
   const int ntiles = kt_end - kt_begin;
+  const int nsub = ntiles * C::SUBS;
 
   const uint32_t tab_s = smem_u32(smem);
   const uint32_t idx_s = smem_u32(smem + L::IDX_OFF);
   const uint32_t a_s0 = smem_u32(smem + L::A_OFF);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::MISC_OFF);
 
-  // lane-rotated chunk offsets: slot s of this lane holds tokens 8c..8c+7,
-  // c = (lane + s) & 7
-  uint32_t rot[8];
-#pragma unroll
-  for (int s = 0; s < 8; ++s) rot[s] = (uint32_t)(((lane + s) & 7) * 16);
-
-  uint32_t sw[8][4];
-  int32_t acc[8][8];
-#pragma unroll
-  for (int s = 0; s < 8; ++s) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) sw[s][q] = 0;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) acc[s][t] = 0;
+  // ---- TMEM for the int32 accumulators (allocated by warp 0)
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
   }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
 
-  if (ntiles > 0) {
-    stage_tile<G, WARPS>(p, kt_begin, 0, m0, n0, smem);
-    cp_async_commit();
-  }
-  int since_flush = 0;
+  if (warp >= WARPS) {
+    // =========================== builder warps: staging + table builds
+    const int bt = tid - L::BUILDER0;
+    const int bw = warp - WARPS;
+    if (ntiles > 0) stage_tile<G, WARPS>(p, kt_begin, 0, m0, n0, smem, bt);
 #pragma unroll 1
-  for (int t = 0; t < ntiles; ++t) {
-    const int buf = t & 1;
-    cp_async_wait_all();
-    __syncthreads();  // tile t visible; previous lookups done; buffer buf^1 free
-    if (t + 1 < ntiles) {
-      stage_tile<G, WARPS>(p, kt_begin + t + 1, buf ^ 1, m0, n0, smem);
-      cp_async_commit();
-    }
-    const uint4 iw = lds128(idx_s + buf * L::IDX_BYTES + tid * 16);
-    const uint32_t iwa[4] = {iw.x, iw.y, iw.z, iw.w};
-    const uint32_t a_s = a_s0 + buf * C::A_BYTES;
-#pragma unroll
-    for (int sub = 0; sub < C::SUBS; ++sub) {
-      if (sub > 0) __syncthreads();  // lookups of the previous sub-stage done
-      build_tables<G, WARPS>(tab_s, a_s, sub);
-      __syncthreads();               // tables visible
-      // ---- lookup + accumulate (a4)
-#pragma unroll
-      for (int jp = 0; jp < C::GS / 2; ++jp) {
-        constexpr int dummy = 0;
-        (void)dummy;
-        const int b0 = sub * C::GS + 2 * jp, b1 = b0 + 1;  // index bytes in the K-tile
-        const uint32_t i0 = (iwa[b0 >> 2] >> (8 * (b0 & 3))) & C::IDX_MASK;
-        const uint32_t i1 = (iwa[b1 >> 2] >> (8 * (b1 & 3))) & C::IDX_MASK;
-        const uint32_t r0 = tab_s + (uint32_t)((2 * jp) * C::R * kRowBytes) + i0 * kRowBytes;
-        const uint32_t r1 = tab_s + (uint32_t)((2 * jp + 1) * C::R * kRowBytes) + i1 * kRowBytes;
-#pragma unroll
-        for (int s = 0; s < 8; ++s) {
-          const uint4 v0 = lds128(r0 + rot[s]);
-          const uint4 v1 = lds128(r1 + rot[s]);
-          sw[s][0] += v0.x + v1.x;
-          sw[s][1] += v0.y + v1.y;
-          sw[s][2] += v0.z + v1.z;
-          sw[s][3] += v0.w + v1.w;
+    for (int u = 0; u < nsub + 2; ++u) {
+      if (u >= 2) bar_sync(3 + (u & 1), L::THREADS);  // lookups of u-2 done
+      if (u >= nsub) continue;
+      const int T = u / C::SUBS, sub = u - T * C::SUBS;
+      if (sub == 0) {
+        if (T + 1 < ntiles) {
+          stage_tile<G, WARPS>(p, kt_begin + T + 1, (T + 1) % kStageBufs, m0, n0, smem, bt);
+          asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+          cp_async_wait_all();
         }
+        bar_sync(5, kBuilderWarps * 32);  // tile T's A rows visible to all builders
       }
+      build_tables<G>(tab_s + (uint32_t)((u & 1) * C::TAB_BYTES),
+                      a_s0 + (uint32_t)((T % kStageBufs) * C::A_BYTES), sub * C::GS, bw, lane);
+      bar_arrive(1 + (u & 1), L::THREADS);  // table u (and tile T's indices) ready
     }
-    if (++since_flush == kFlushTiles || t + 1 == ntiles) {
-      // widen 16-bit fields into int32 (INT16 -> INT32)
-      since_flush = 0;
+  } else {
+    // =========================== lookup warps: one output row per thread
+    // lane-rotated chunk offsets: slot s of this lane holds tokens 8c..8c+7,
+    // c = (lane + s) & 7
+    uint32_t rot[8];
 #pragma unroll
-      for (int s = 0; s < 8; ++s) {
+    for (int s = 0; s < 8; ++s) rot[s] = (uint32_t)(((lane + s) & 7) * 16);
+    const uint32_t taddr = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+    uint32_t sw[8][4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          acc[s][2 * q] += (int32_t)(sw[s][q] & 0xFFFFu);
-          acc[s][2 * q + 1] += (int32_t)(sw[s][q] >> 16);
-          sw[s][q] = 0;
+    for (int s = 0; s < 8; ++s)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sw[s][q] = 0;
+    int32_t nneg = 0;
+    bool first = true;
+    int since_flush = 0;
+    uint32_t iwa[4] = {0u, 0u, 0u, 0u};
+#pragma unroll 1
+    for (int t = 0; t < ntiles; ++t) {
+#pragma unroll
+      for (int sub = 0; sub < C::SUBS; ++sub) {
+        const int u = t * C::SUBS + sub;
+        bar_sync(1 + (u & 1), L::THREADS);  // table u built
+        if (sub == 0) {
+          const uint4 iw = lds128(idx_s + (t % kStageBufs) * L::IDX_BYTES + tid * 16);
+          iwa[0] = iw.x; iwa[1] = iw.y; iwa[2] = iw.z; iwa[3] = iw.w;
         }
+        lookup_sub<G>(sub, tab_s + (uint32_t)((u & 1) * C::TAB_BYTES), iwa, rot, sw, nneg);
+        bar_arrive(3 + (u & 1), L::THREADS);  // table buffer u & 1 free
+      }
+      if (++since_flush == kFlushTiles || t + 1 == ntiles) {
+        since_flush = 0;
+        flush_tmem<G>(sw, nneg, taddr, first);
+        first = false;
       }
     }
   }
-  // remove the field bias: every group added BIAS to every token
-  const int32_t bias_total = C::BIAS * kKgTile * ntiles;
-#pragma unroll
-  for (int s = 0; s < 8; ++s)
-#pragma unroll
-    for (int t = 0; t < 8; ++t) acc[s][t] -= bias_total;
 
-  // ---- int32 tile -> shared (a5).  Row r (this thread), 16-byte unit u of
-  // the 256-byte row stored at u ^ ((r >> 2) & 1): conflict-free for both the
-  // lane-per-row writes below and the row-contiguous reads after.
-  __syncthreads();  // all table reads done before the region is reused
-  {
+  // ---- int32 tile -> shared (a5).  Row r (lookup thread), 16-byte unit u
+  // of the 256-byte row stored at u ^ ((r >> 2) & 1): conflict-free for both
+  // the lane-per-row writes below and the row-contiguous reads after.
+  tmem_fence_before();
+  __syncthreads();  // every table read done before the region is reused
+  tmem_fence_after();
+  if (warp < WARPS) {
+    const uint32_t taddr = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+    const int32_t bias_total = C::BIAS * kKgTile * ntiles;
     const uint32_t red_s = tab_s;
     const int r = tid;
     const uint32_t swz = (uint32_t)((r >> 2) & 1);
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const uint32_t c = (uint32_t)((lane + s) & 7);
+    for (int h = 0; h < 4; ++h) {
+      uint32_t v[16];
+      if (ntiles > 0) {
+        tmem_ld16(taddr + 16 * h, v);
+        tmem_wait_ld();
+      } else {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t u = (2 * c + h) ^ swz;
-        sts128(red_s + r * 256 + u * 16, (uint32_t)acc[s][4 * h], (uint32_t)acc[s][4 * h + 1],
-               (uint32_t)acc[s][4 * h + 2], (uint32_t)acc[s][4 * h + 3]);
+        for (int i = 0; i < 16; ++i) v[i] = 0;
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int s = 2 * h + e;
+        const uint32_t c = (uint32_t)((lane + s) & 7);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const uint32_t uu = (2 * c + hh) ^ swz;
+          const uint32_t* x = v + 8 * e + 4 * hh;
+          sts128(red_s + r * 256 + uu * 16, x[0] - bias_total, x[1] - bias_total,
+                 x[2] - bias_total, x[3] - bias_total);
+        }
       }
     }
   }
+  tmem_fence_before();
   cg::cluster_group cluster = cg::this_cluster();
   if (S > 1) cluster.sync(); else __syncthreads();
+  if (warp == 0) {
+    tmem_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
+                 "n"(kTmemCols)
+                 : "memory");
+  }
 
   // ---- reduce across the cluster + epilogue (a5, a6)
   {
