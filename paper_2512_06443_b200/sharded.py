@@ -1,0 +1,137 @@
+"""Row-parallel ternary linears and the config-5 layer chain (e).
+
+North star: "Linear layers are sharded by output rows across 1/2/4/8 GPUs of
+one 8xB200 box, with an NCCL all-gather of outputs over NVLink."  Output row m
+depends only on weight row m and all of A, so rank r of G packs the contiguous
+rows [r*Mp, (r+1)*Mp) (Mp = ceil(M/G); the last shard may be short), computes
+its fp32 shard with ``vlut_mpgemm`` and ``all_gather_into_tensor`` assembles
+the token-contiguous [M][N] output on every rank.  The gathered result is
+bit-identical to the 1-GPU result (each output element is computed by exactly
+one rank with the same kernel arithmetic).
+
+PyTorch is plumbing here (device memory, streams, process groups).  The
+per-shard compute defaults to the CUDA path; tests inject other callables
+(e.g. the CPU oracle under gloo) to check the partition / gather logic on CPU.
+"""
+from __future__ import annotations
+
+from typing import Callable, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+__all__ = ["shard_rows", "RowShardedLinear", "LayerChain", "CHAIN_Q_ROWS"]
+
+
+def shard_rows(M: int, world: int, rank: int) -> Tuple[int, int, int]:
+    """(row0, row1, Mp): rank's contiguous row range and the padded shard size."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    Mp = -(-M // world)
+    r0 = min(M, rank * Mp)
+    r1 = min(M, r0 + Mp)
+    return r0, r1, Mp
+
+
+def _dist():
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        return dist
+    return None
+
+
+class RowShardedLinear:
+    """One ternary linear, row-sharded over the default process group.
+
+    W: int8 trits [M][K] (host, full matrix; each rank keeps only its rows),
+    g: 4 or 5, w_scale: per-tensor scale.  ``compute(shard, A, a_scale, out)``
+    fills ``out`` ([rows][N] fp32) -- default: the CUDA kernel.
+    """
+
+    def __init__(self, W: np.ndarray, g: int, w_scale: float, device=None,
+                 compute: Optional[Callable] = None, pack: Optional[Callable] = None):
+        dist = _dist()
+        self.world = dist.get_world_size() if dist else 1
+        self.rank = dist.get_rank() if dist else 0
+        self.M, self.K = W.shape
+        self.g = g
+        self.w_scale = float(w_scale)
+        self.r0, self.r1, self.Mp = shard_rows(self.M, self.world, self.rank)
+        self.rows = self.r1 - self.r0
+        self.device = device
+        W_r = np.ascontiguousarray(W[self.r0:self.r1])
+        if pack is not None:
+            self.shard = pack(W_r, g)
+        else:
+            import paper_2512_06443_b200 as v
+            self.shard = v.pack_weights(W_r, g, device=device) if self.rows else None
+        self._compute = compute or self._cuda_compute
+
+    def _cuda_compute(self, shard, A, a_scale, out):
+        import paper_2512_06443_b200 as v
+        v.mpgemm(shard, A, a_scale, self.w_scale, out=out)
+
+    def __call__(self, A, a_scale, out=None):
+        """A: int8 [K][N] (replicated on every rank), a_scale: fp32 [N] ->
+        fp32 [M][N] on every rank."""
+        import torch
+        N = A.shape[1]
+        dev = A.device
+        if self.world == 1:
+            if out is None:
+                out = torch.empty((self.M, N), dtype=torch.float32, device=dev)
+            if self.rows:
+                self._compute(self.shard, A, a_scale, out)
+            return out
+        local = torch.empty((self.Mp, N), dtype=torch.float32, device=dev)
+        if self.rows:
+            self._compute(self.shard, A, a_scale, local[:self.rows])
+        if self.rows < self.Mp:
+            local[self.rows:].zero_()
+        full = torch.empty((self.Mp * self.world, N), dtype=torch.float32, device=dev)
+        _dist().all_gather_into_tensor(full, local)
+        res = full[:self.M]
+        if out is not None:
+            out.copy_(res)
+            return out
+        return res
+
+
+# Config 5 glue (reading c14): per layer
+#   qkv = L_qkv(x); o = L_o(Q(qkv[0:2560])); u = Q(o);
+#   h = L_gate(u) * L_up(u); x' = Q(L_down(Q(h)))
+CHAIN_Q_ROWS = 2560
+
+
+class LayerChain:
+    """The 30-layer BitNet-2B-shaped prefill of ternary linears (config 5).
+
+    layers: list of 5-tuples of RowShardedLinear (qkv, o, gate, up, down).
+    quantize(x, y=None) -> (q, scale): default the CUDA quantizer (K3).
+    """
+
+    def __init__(self, layers: Sequence[Sequence[RowShardedLinear]], q_rows: int = CHAIN_Q_ROWS,
+                 quantize: Optional[Callable] = None):
+        self.layers = [tuple(l) for l in layers]
+        self.q_rows = q_rows
+        if quantize is None:
+            import paper_2512_06443_b200 as v
+            quantize = v.quantize
+        self.quantize = quantize
+
+    def layer(self, l, xq, xs):
+        L_qkv, L_o, L_gate, L_up, L_down = self.layers[l]
+        qkv = L_qkv(xq, xs)
+        q1, s1 = self.quantize(qkv[:self.q_rows])
+        o = L_o(q1, s1)
+        u, su = self.quantize(o)
+        gate = L_gate(u, su)
+        up = L_up(u, su)
+        hq, hs = self.quantize(gate, up)
+        d = L_down(hq, hs)
+        return self.quantize(d)
+
+    def __call__(self, xq, xs, n_layers: Optional[int] = None):
+        n = len(self.layers) if n_layers is None else n_layers
+        for l in range(n):
+            xq, xs = self.layer(l, xq, xs)
+        return xq, xs

@@ -223,3 +223,27 @@ def test_config4_full_size_sampled(v, N, g):
 def test_config3_linears_sampled(v, j):
     lin = synth.CONFIGS[3].linears[j]
     sampled_rows_check(v, lin.M, lin.K, 1024, 4, seed=3000 + j, rows=8)
+
+
+# ------------------------------------------------------------------ config 5 chain (a7 + a2-a6)
+def test_config5_chain_two_layers_sampled_tokens(v):
+    """Full BitNet-2B-shaped layer weights, N = 2048 tokens on the GPU; the
+    oracle re-runs the chain on sampled token columns (per-token quantization
+    makes columns independent) -- codes and scales bit-exact after each layer."""
+    from paper_2512_06443_b200.sharded import LayerChain, RowShardedLinear
+    cfg = synth.CONFIGS[5]
+    N, n_layers = 2048, 2
+    layers_w = [[w for _, w in synth.config_weights(cfg, l)] for l in range(n_layers)]
+    layers = [[RowShardedLinear(w, 4, synth.W_SCALE, device=dev()) for w in lw]
+              for lw in layers_w]
+    chain = LayerChain(layers)
+    x = synth.activations_f32(2560, N, synth.act_seed(cfg, N))
+    xq, xs = v.quantize(to_dev(x))
+    cols = np.unique(np.concatenate([[0, N - 1], synth.rng(5).integers(0, N, size=14)]))
+    q_ref, s_ref = oracle.quantize(np.ascontiguousarray(x[:, cols]))
+    for l in range(n_layers):
+        xq, xs = chain.layer(l, xq, xs)
+        q_ref, s_ref = oracle.config5_layer(layers_w[l], synth.W_SCALE, q_ref, s_ref, q_rows=2560)
+        torch.cuda.synchronize()
+        assert np.array_equal(xs.cpu().numpy()[cols], s_ref)
+        assert np.array_equal(xq.cpu().numpy()[:, cols], q_ref)

@@ -1,0 +1,96 @@
+"""Multi-rank host logic of the row-sharded path on CPU (gloo, world 2 and 3):
+the row partition, the padded all-gather and the config-5 glue.  The per-shard
+compute is injected (the CPU oracle) -- the CUDA kernels are covered by the
+-m gpu tests; here only the partition / exchange logic is under test."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2512_06443_b200 import synth
+from paper_2512_06443_b200.sharded import LayerChain, RowShardedLinear, shard_rows
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def oracle_compute(w_scale):
+    def f(shard, A, a_scale, out):
+        acc = oracle.gemm_i32(shard, A.numpy())
+        out.copy_(torch.from_numpy(oracle.dequant_f32(acc, a_scale.numpy(), w_scale)))
+    return f
+
+
+def oracle_quantize(x, y=None):
+    xx = x.numpy() if y is None else (x.numpy() * y.numpy()).astype(np.float32)
+    q, s = oracle.quantize(np.ascontiguousarray(xx))
+    return torch.from_numpy(q), torch.from_numpy(s)
+
+
+def test_shard_rows_partition():
+    for M in (1, 7, 256, 6912, 2561):
+        for G in (1, 2, 3, 4, 8):
+            rows = []
+            for r in range(G):
+                a, b, Mp = shard_rows(M, G, r)
+                assert Mp == -(-M // G) and 0 <= b - a <= Mp
+                rows.extend(range(a, b))
+            assert rows == list(range(M))
+
+
+def _worker(rank, world, port, M, K, N, g, result_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        W = synth.ternary_weights(M, K, seed=31)
+        x = synth.activations_f32(K, N, seed=32)
+        q, s = oracle.quantize(x)
+        lin = RowShardedLinear(W, g, synth.W_SCALE, compute=oracle_compute(synth.W_SCALE),
+                               pack=lambda w, gg: w)
+        out = lin(torch.from_numpy(q), torch.from_numpy(s))
+        # config-5 glue on small stand-in shapes, every linear row-sharded
+        Kc = 40
+        Ws = [synth.ternary_weights(60, Kc, 1), synth.ternary_weights(Kc, Kc, 2),
+              synth.ternary_weights(80, Kc, 3), synth.ternary_weights(80, Kc, 4),
+              synth.ternary_weights(Kc, 80, 5)]
+        layer = [RowShardedLinear(w, 4, synth.W_SCALE, compute=oracle_compute(synth.W_SCALE),
+                                  pack=lambda w_, gg: w_) for w in Ws]
+        chain = LayerChain([layer, layer], q_rows=Kc, quantize=oracle_quantize)
+        xq, xs = oracle.quantize(synth.activations_f32(Kc, 6, seed=7))
+        cq, cs = chain(torch.from_numpy(xq), torch.from_numpy(xs))
+        if rank == 0:
+            np.savez(result_path, out=out.numpy(), cq=cq.numpy(), cs=cs.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,M", [(2, 200), (3, 101)])
+def test_gloo_row_sharded_equals_single(tmp_path, world, M):
+    K, N, g = 64, 9, 4
+    path = str(tmp_path / "res.npz")
+    mp.spawn(_worker, args=(world, free_port(), M, K, N, g, path), nprocs=world, join=True)
+    res = np.load(path)
+    W = synth.ternary_weights(M, K, seed=31)
+    q, s = oracle.quantize(synth.activations_f32(K, N, seed=32))
+    ref = oracle.dequant_f32(oracle.gemm_i32(W, q), s, synth.W_SCALE)
+    assert np.array_equal(res["out"].view(np.int32), ref.view(np.int32))
+    # chain == the oracle's own config-5 glue, two layers
+    Kc = 40
+    Ws = (synth.ternary_weights(60, Kc, 1), synth.ternary_weights(Kc, Kc, 2),
+          synth.ternary_weights(80, Kc, 3), synth.ternary_weights(80, Kc, 4),
+          synth.ternary_weights(Kc, 80, 5))
+    xq, xs = oracle.quantize(synth.activations_f32(Kc, 6, seed=7))
+    for _ in range(2):
+        xq, xs = oracle.config5_layer(Ws, synth.W_SCALE, xq, xs, q_rows=Kc)
+    assert np.array_equal(res["cq"], xq) and np.array_equal(res["cs"], xs)
