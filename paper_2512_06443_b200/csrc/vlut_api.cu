@@ -174,13 +174,16 @@ vlut_status launch_k1(const vlut::Params& p, int S, int NT, int MT, cudaStream_t
   cfg.blockDim = dim3(L::THREADS, 1, 1);
   cfg.dynamicSmemBytes = L::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)S;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // programmatic dependent launch: the prologue overlaps the previous kernel
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   VLUT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
   return VLUT_OK;
 }
@@ -263,6 +266,12 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
 extern "C" {
 
 const char* vlut_last_error(void) { return g_err.c_str(); }
+
+#ifdef VLUT_TIMING
+int vlut_debug_set_timing(void* dev_buf) {
+  return (int)cudaMemcpyToSymbol(vlut::g_vlut_timing, &dev_buf, sizeof(void*));
+}
+#endif
 
 const char* vlut_version(void) { return "vlut-b200 0.1 (sm_100a)"; }
 
@@ -424,13 +433,16 @@ vlut_status vlut_quantize(const float* x, const float* y, int K, int N, int8_t* 
   cfg.blockDim = dim3(vlut::kQThreads, 1, 1);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // programmatic dependent launch: the prologue overlaps the previous kernel
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   if (aligned)
     VLUT_CUDA_TRY(cudaLaunchKernelEx(&cfg, vlut::vlut_quantize_kernel<true>, x, y, K, N, q, scale));
   else

@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(kQThreads)
                          int8_t* __restrict__ q, float* __restrict__ scale) {
   __shared__ float red[kQThreads / 32][kQTok];
   __shared__ float cta_amax[kQTok];
+  __shared__ float s_scale[kQTok];
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = (int)cluster.num_blocks();
@@ -63,6 +64,9 @@ __global__ void __launch_bounds__(kQThreads)
   const int n = blockIdx.y * kQTok + col * 4;
   const int k_begin = (int)(((long long)rank * K) / CL);
   const int k_end = (int)(((long long)(rank + 1) * K) / CL);
+  // PDL: x may be the previous kernel's output; let the next kernel launch early
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   float4 cache[kQCache];
   float m[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -99,18 +103,25 @@ __global__ void __launch_bounds__(kQThreads)
     cta_amax[tid] = a;
   }
   cluster.sync();
+  // 16 threads combine the cluster's partial maxima (DSMEM), the rest wait
+  if (tid < kQTok) {
+    float a = 0.f;
+    float part[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) part[r] = (r < CL) ? cluster.map_shared_rank(cta_amax, r)[tid] : 0.f;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) a = fmaxf(a, part[r]);
+    const float sc = (a == 0.f) ? 1.f : __fdiv_rn(a, 127.f);
+    s_scale[tid] = sc;
+    if (rank == 0 && blockIdx.y * kQTok + tid < N) scale[blockIdx.y * kQTok + tid] = sc;
+  }
+  // this CTA's remote reads are done once its 16 readers pass here: arrive
+  // early, wait only before exit (keeps cta_amax alive for the other CTAs)
+  __syncthreads();
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
   float s[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    float a = 0.f;
-    for (int r = 0; r < CL; ++r) a = fmaxf(a, cluster.map_shared_rank(cta_amax, r)[col * 4 + i]);
-    s[i] = (a == 0.f) ? 1.f : __fdiv_rn(a, 127.f);
-  }
-  if (rank == 0 && rsub == 0) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (n + i < N) scale[n + i] = s[i];
-  }
+  for (int i = 0; i < 4; ++i) s[i] = s_scale[col * 4 + i];
 #pragma unroll
   for (int i = 0; i < kQCache; ++i) {
     const int k = k_begin + rsub + 64 * i;
@@ -134,7 +145,7 @@ __global__ void __launch_bounds__(kQThreads)
     const float v[4] = {a.x, a.y, a.z, a.w};
     for (int t = 0; t < 4 && n + t < N; ++t) q[(size_t)k * N + n + t] = q_code(v[t], s[t]);
   }
-  cluster.sync();  // keep cta_amax alive until every CTA of the cluster read it
+  asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
 }
 
 // ---------------------------------------------------------------- device packer (a1)

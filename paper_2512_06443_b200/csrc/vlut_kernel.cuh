@@ -86,7 +86,11 @@ struct Layout {
   static constexpr int IDX_BYTES = MCTA * 16;
   static constexpr int A_OFF = IDX_OFF + kStageBufs * IDX_BYTES;
   static constexpr int MISC_OFF = A_OFF + kStageBufs * Cfg<G>::A_BYTES;  // tmem address
-  static constexpr int SMEM = MISC_OFF + 16;
+  static constexpr int MBAR_OFF = MISC_OFF + 16;  // FULL[2], EMPTY[2] (8 B each)
+  static constexpr int SCALE_OFF = MBAR_OFF + 32;  // fl(a_scale[n] * w_scale), 64 floats
+  static constexpr int SMEM = SCALE_OFF + kNcta * 4;
+  // epilogue: 16-byte output units per thread (upper bound, splits = 1)
+  static constexpr int EPI_UNITS = (MCTA * 16 + THREADS - 1) / THREADS;
   static_assert(WARPS <= 16, "TMEM columns: at most 4 column blocks of 64");
 };
 
@@ -172,14 +176,52 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
-// ---------------------------------------------------------------- named barriers
-// id 0: __syncthreads; 1,2: table buffer FULL; 3,4: table buffer EMPTY;
-// 5: builders only.
+// ---------------------------------------------------------------- debug timing
+// Compiled only with -DVLUT_TIMING (scripts/phase_timing): %globaltimer
+// stamps of CTA phases into g_vlut_timing[cta][8].
+#ifdef VLUT_TIMING
+__device__ unsigned long long* g_vlut_timing;
+#define VLUT_STAMP(i)                                                                      \
+  do {                                                                                     \
+    if (threadIdx.x == 0 && g_vlut_timing) {                                               \
+      unsigned long long t_;                                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                               \
+      const unsigned cta_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
+      g_vlut_timing[cta_ * 8 + (i)] = t_;                                                  \
+    }                                                                                      \
+  } while (0)
+#else
+#define VLUT_STAMP(i) \
+  do {                \
+  } while (0)
+#endif
+
+// ---------------------------------------------------------------- barriers
+// Named barrier 5: builder warps only.  Table handshake: mbarriers (lookup
+// warps wait on FULL without arriving, so they never rendezvous with each
+// other; one elected lane per warp arrives).
 __device__ __forceinline__ void bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(addr), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t addr) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
 }
 
 // ---------------------------------------------------------------- TMEM helpers
@@ -228,20 +270,24 @@ struct Params {
 };
 
 // ---------------------------------------------------------------- staging (a2)
-// Issued by the builder threads (bt in [0, 128)); one commit group per tile.
+// Issued by the builder threads (bt in [0, 128)).  what: 1 = index vectors,
+// 2 = activations, 3 = both; a commit group is closed after the activations.
 template <int G, int WARPS>
 __device__ __forceinline__ void stage_tile(const Params& p, int kt, int buf, int m0, int n0,
-                                           uint8_t* smem, int bt) {
+                                           uint8_t* smem, int bt, int what) {
   using C = Cfg<G>;
   using L = Layout<G, WARPS>;
   constexpr int NB = kBuilderWarps * 32;
-  // index vectors: one 16-byte row per CTA row (rows past m_pad -> zero fill)
-  for (int r = bt; r < L::MCTA; r += NB) {
-    const int m = m0 + r;
-    const bool ok = m < p.m_pad;
-    const uint8_t* src = ok ? p.payload + ((size_t)kt * p.m_pad + m) * 16 : p.payload;
-    cp_async16(smem_u32(smem + L::IDX_OFF + buf * L::IDX_BYTES + r * 16), src, ok ? 16 : 0);
+  if (what & 1) {
+    // index vectors: one 16-byte row per CTA row (rows past m_pad -> zero fill)
+    for (int r = bt; r < L::MCTA; r += NB) {
+      const int m = m0 + r;
+      const bool ok = m < p.m_pad;
+      const uint8_t* src = ok ? p.payload + ((size_t)kt * p.m_pad + m) * 16 : p.payload;
+      cp_async16(smem_u32(smem + L::IDX_OFF + buf * L::IDX_BYTES + r * 16), src, ok ? 16 : 0);
+    }
   }
+  if (!(what & 2)) return;
   // activation rows k0 .. k0 + 16g - 1, tokens n0 .. n0+63 (past K or N -> 0)
   const int k0 = kt * kKgTile * G;
   uint8_t* a_s = smem + L::A_OFF + buf * C::A_BYTES;
@@ -414,6 +460,16 @@ __device__ __forceinline__ void flush_tmem(uint32_t (&sw)[8][4], int32_t& nneg, 
   nneg = 0;
 }
 
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch: the K1 prologue (mbarriers, TMEM, index
+// staging) overlaps the tail of the kernel that produced A / a_scale.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
 // ---------------------------------------------------------------- the kernel
 template <int G, int WARPS, bool ACC_ONLY>
 __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
@@ -421,6 +477,7 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
   using C = Cfg<G>;
   using L = Layout<G, WARPS>;
   extern __shared__ __align__(1024) uint8_t smem[];
+  VLUT_STAMP(0);
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -438,33 +495,43 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
   const uint32_t idx_s = smem_u32(smem + L::IDX_OFF);
   const uint32_t a_s0 = smem_u32(smem + L::A_OFF);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::MISC_OFF);
+  float* scale_s = reinterpret_cast<float*>(smem + L::SCALE_OFF);
+  const uint32_t mbar = smem_u32(smem + L::MBAR_OFF);  // FULL b at +8b, EMPTY b at +16+8b
 
-  // ---- TMEM for the int32 accumulators (allocated by warp 0)
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "n"(kTmemCols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  if (tid == L::BUILDER0) {
+    mbar_init(mbar + 0, kBuilderWarps);
+    mbar_init(mbar + 8, kBuilderWarps);
+    mbar_init(mbar + 16, WARPS);
+    mbar_init(mbar + 24, WARPS);
   }
-  tmem_fence_before();
-  __syncthreads();
-  tmem_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  __syncthreads();  // mbarriers initialised
 
+  uint32_t tmem_base = 0;
   if (warp >= WARPS) {
     // =========================== builder warps: staging + table builds
     const int bt = tid - L::BUILDER0;
     const int bw = warp - WARPS;
-    if (ntiles > 0) stage_tile<G, WARPS>(p, kt_begin, 0, m0, n0, smem, bt);
+    if (ntiles > 0) {
+      // the packed weights do not depend on the previous kernel: stage tile
+      // 0's indices before waiting for it, then its activations
+      stage_tile<G, WARPS>(p, kt_begin, 0, m0, n0, smem, bt, /*what=*/1);
+      pdl_wait();
+      stage_tile<G, WARPS>(p, kt_begin, 0, m0, n0, smem, bt, /*what=*/2);
+    } else {
+      pdl_wait();
+    }
+    if (!ACC_ONLY && bt < kNcta) {
+      const int n = n0 + bt;
+      scale_s[bt] = (n < p.N) ? __fmul_rn(__ldg(p.a_scale + n), p.w_scale) : 0.f;
+    }
 #pragma unroll 1
     for (int u = 0; u < nsub + 2; ++u) {
-      if (u >= 2) bar_sync(3 + (u & 1), L::THREADS);  // lookups of u-2 done
+      if (u >= 2) mbar_wait(mbar + 16 + 8 * (u & 1), ((u >> 1) - 1) & 1);  // lookups of u-2 done
       if (u >= nsub) continue;
       const int T = u / C::SUBS, sub = u - T * C::SUBS;
       if (sub == 0) {
         if (T + 1 < ntiles) {
-          stage_tile<G, WARPS>(p, kt_begin + T + 1, (T + 1) % kStageBufs, m0, n0, smem, bt);
+          stage_tile<G, WARPS>(p, kt_begin + T + 1, (T + 1) % kStageBufs, m0, n0, smem, bt, 3);
           asm volatile("cp.async.wait_group 1;\n" ::: "memory");
         } else {
           cp_async_wait_all();
@@ -473,10 +540,25 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
       }
       build_tables<G>(tab_s + (uint32_t)((u & 1) * C::TAB_BYTES),
                       a_s0 + (uint32_t)((T % kStageBufs) * C::A_BYTES), sub * C::GS, bw, lane);
-      bar_arrive(1 + (u & 1), L::THREADS);  // table u (and tile T's indices) ready
+      __syncwarp();
+      if (lane == 0) mbar_arrive(mbar + 8 * (u & 1));  // table u (and tile T's indices) ready
     }
   } else {
     // =========================== lookup warps: one output row per thread
+    // TMEM for the int32 accumulators: allocated by warp 0 while the
+    // builders already stage and build (lookup warps only wait for it)
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(kTmemCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    tmem_fence_before();
+    bar_sync(6, L::MCTA);
+    tmem_fence_after();
+    tmem_base = *tmem_slot;
+    VLUT_STAMP(1);
     // lane-rotated chunk offsets: slot s of this lane holds tokens 8c..8c+7,
     // c = (lane + s) & 7
     uint32_t rot[8];
@@ -490,32 +572,39 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
       for (int q = 0; q < 4; ++q) sw[s][q] = 0;
     int32_t nneg = 0;
     bool first = true;
-    int since_flush = 0;
+    int since_flush = warp % kFlushTiles;  // stagger the widening across warps
     uint32_t iwa[4] = {0u, 0u, 0u, 0u};
 #pragma unroll 1
     for (int t = 0; t < ntiles; ++t) {
 #pragma unroll
       for (int sub = 0; sub < C::SUBS; ++sub) {
         const int u = t * C::SUBS + sub;
-        bar_sync(1 + (u & 1), L::THREADS);  // table u built
+        mbar_wait(mbar + 8 * (u & 1), (u >> 1) & 1);  // table u built
+        if (u == 0) VLUT_STAMP(2);
         if (sub == 0) {
           const uint4 iw = lds128(idx_s + (t % kStageBufs) * L::IDX_BYTES + tid * 16);
           iwa[0] = iw.x; iwa[1] = iw.y; iwa[2] = iw.z; iwa[3] = iw.w;
         }
         lookup_sub<G>(sub, tab_s + (uint32_t)((u & 1) * C::TAB_BYTES), iwa, rot, sw, nneg);
-        bar_arrive(3 + (u & 1), L::THREADS);  // table buffer u & 1 free
+        __syncwarp();
+        if (lane == 0) mbar_arrive(mbar + 16 + 8 * (u & 1));  // table buffer u & 1 free
       }
-      if (++since_flush == kFlushTiles || t + 1 == ntiles) {
+      if (++since_flush >= kFlushTiles || t + 1 == ntiles) {
         since_flush = 0;
         flush_tmem<G>(sw, nneg, taddr, first);
         first = false;
       }
     }
+    pdl_wait();  // (no-op by now) formally orders the epilogue's a_scale reads
   }
+  // allow the next kernel in the stream to start its own prologue
+  pdl_launch_dependents();
 
+  VLUT_STAMP(3);
   // ---- int32 tile -> shared (a5).  Row r (lookup thread), 16-byte unit u
   // of the 256-byte row stored at u ^ ((r >> 2) & 1): conflict-free for both
   // the lane-per-row writes below and the row-contiguous reads after.
+  const int rows_per = L::MCTA / S;
   tmem_fence_before();
   __syncthreads();  // every table read done before the region is reused
   tmem_fence_after();
@@ -525,33 +614,40 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
     const uint32_t red_s = tab_s;
     const int r = tid;
     const uint32_t swz = (uint32_t)((r >> 2) & 1);
+    uint32_t v[4][16];
+    if (ntiles > 0) {
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      uint32_t v[16];
-      if (ntiles > 0) {
-        tmem_ld16(taddr + 16 * h, v);
-        tmem_wait_ld();
-      } else {
+      for (int h = 0; h < 4; ++h) tmem_ld16(taddr + 16 * h, v[h]);
+      tmem_wait_ld();
+    } else {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = 0;
-      }
+      for (int h = 0; h < 4; ++h)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int s = 2 * h + e;
-        const uint32_t c = (uint32_t)((lane + s) & 7);
+        for (int i = 0; i < 16; ++i) v[h][i] = 0;
+    }
+    {
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const uint32_t uu = (2 * c + hh) ^ swz;
-          const uint32_t* x = v + 8 * e + 4 * hh;
-          sts128(red_s + r * 256 + uu * 16, x[0] - bias_total, x[1] - bias_total,
-                 x[2] - bias_total, x[3] - bias_total);
+      for (int h = 0; h < 4; ++h) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int s = 2 * h + e;
+          const uint32_t c = (uint32_t)((lane + s) & 7);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const uint32_t uu = (2 * c + hh) ^ swz;
+            const uint32_t* x = v[h] + 8 * e + 4 * hh;
+            sts128(red_s + r * 256 + uu * 16, x[0] - bias_total, x[1] - bias_total,
+                   x[2] - bias_total, x[3] - bias_total);
+          }
         }
       }
     }
   }
+  VLUT_STAMP(4);
   tmem_fence_before();
   cg::cluster_group cluster = cg::this_cluster();
   if (S > 1) cluster.sync(); else __syncthreads();
+  VLUT_STAMP(5);
   if (warp == 0) {
     tmem_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
@@ -559,54 +655,79 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
                  : "memory");
   }
 
-  // ---- reduce across the cluster + epilogue (a5, a6)
+  // ---- reduce across the cluster + epilogue (a5, a6): all loads of a
+  // thread's units first (latency overlapped), then convert + store
   {
-    const int rows_per = L::MCTA / S;
     const int r_begin = rank * rows_per;
     const int units = rows_per * 16;
     const int4* red_local = reinterpret_cast<const int4*>(smem);
-#pragma unroll 1
-    for (int e = tid; e < units; e += L::THREADS) {
-      const int r = r_begin + (e >> 4);
-      const int u = e & 15;
-      const int pu = u ^ ((r >> 2) & 1);
-      const int off = r * 16 + pu;  // in int4 units
-      int4 v = red_local[off];
-      for (int q = 0; q < S; ++q) {
-        if (q == rank) continue;
-        const int4* rem = cluster.map_shared_rank(red_local, q);
-        const int4 w = rem[off];
-        v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+    int4 acc4[L::EPI_UNITS];
+#pragma unroll
+    for (int i = 0; i < L::EPI_UNITS; ++i) {
+      const int e = tid + i * L::THREADS;
+      acc4[i] = make_int4(0, 0, 0, 0);
+      if (e < units) {
+        const int r = r_begin + (e >> 4);
+        const int off = r * 16 + ((e & 15) ^ ((r >> 2) & 1));  // in int4 units
+        acc4[i] = red_local[off];
       }
-      const int m = m0 + r;
+    }
+    {
+      for (int q = 1; q < S; ++q) {
+        const int4* rem = cluster.map_shared_rank(red_local, (rank + q) % S);
+        int4 w4[L::EPI_UNITS];
+#pragma unroll
+        for (int i = 0; i < L::EPI_UNITS; ++i) {
+          const int e = tid + i * L::THREADS;
+          w4[i] = make_int4(0, 0, 0, 0);
+          if (e < units) {
+            const int r = r_begin + (e >> 4);
+            w4[i] = rem[r * 16 + ((e & 15) ^ ((r >> 2) & 1))];
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < L::EPI_UNITS; ++i) {
+          acc4[i].x += w4[i].x; acc4[i].y += w4[i].y; acc4[i].z += w4[i].z; acc4[i].w += w4[i].w;
+        }
+      }
+      // remote reads done: arrive now, wait only before exit (the peers keep
+      // their shared memory until every CTA of the cluster has read it)
+      if (S > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+    }
+    VLUT_STAMP(6);
+#pragma unroll
+    for (int i = 0; i < L::EPI_UNITS; ++i) {
+      const int e = tid + i * L::THREADS;
+      if (e >= units) continue;
+      const int u = e & 15;
+      const int m = m0 + r_begin + (e >> 4);
       const int n = n0 + 4 * u;
       if (m >= p.M || n >= p.N) continue;
+      const int4 vv4 = acc4[i];
       if constexpr (ACC_ONLY) {
         int32_t* o = reinterpret_cast<int32_t*>(p.out) + (size_t)m * p.N + n;
         if (p.out_vec4 && n + 3 < p.N) {
-          *reinterpret_cast<int4*>(o) = v;
+          *reinterpret_cast<int4*>(o) = vv4;
         } else {
-          const int vv[4] = {v.x, v.y, v.z, v.w};
-          for (int i = 0; i < 4 && n + i < p.N; ++i) o[i] = vv[i];
+          const int vv[4] = {vv4.x, vv4.y, vv4.z, vv4.w};
+          for (int k = 0; k < 4 && n + k < p.N; ++k) o[k] = vv[k];
         }
       } else {
         float* o = p.out + (size_t)m * p.N + n;
-        const int vv[4] = {v.x, v.y, v.z, v.w};
+        const int vv[4] = {vv4.x, vv4.y, vv4.z, vv4.w};
         float f[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float sc = (n + i < p.N) ? __fmul_rn(__ldg(p.a_scale + n + i), p.w_scale) : 0.f;
-          f[i] = __fmul_rn((float)vv[i], sc);
-        }
+        for (int k = 0; k < 4; ++k) f[k] = __fmul_rn((float)vv[k], scale_s[4 * u + k]);
         if (p.out_vec4 && n + 3 < p.N) {
           *reinterpret_cast<float4*>(o) = make_float4(f[0], f[1], f[2], f[3]);
         } else {
-          for (int i = 0; i < 4 && n + i < p.N; ++i) o[i] = f[i];
+          for (int k = 0; k < 4 && n + k < p.N; ++k) o[k] = f[k];
         }
       }
     }
   }
-  if (S > 1) cluster.sync();  // keep this CTA's shared memory alive for readers
+  VLUT_STAMP(7);
+  if (S > 1) asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
 }
 
 }  // namespace vlut

@@ -1,0 +1,139 @@
+// k1_ablate.cu -- development ablation of K1's main loop on one B200:
+// reuses the device functions of csrc/vlut_kernel.cuh (lookup_sub,
+// build_tables, flush_tmem) on synthetic indices and measures shared-memory
+// bytes/clk/SM for progressively more of the real loop:
+//   mode 0: lookups only (12 lookup warps, random indices, XOR/IMAD negation)
+//   mode 1: + FULL/EMPTY named-barrier handshake with 4 idle builder warps
+//   mode 2: + builders really build the half tables (Gray walks, STS)
+//   mode 3: + TMEM flush every 3 K-tiles
+//   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o k1_ablate k1_ablate.cu
+#include <cstdio>
+#include "../paper_2512_06443_b200/csrc/vlut_kernel.cuh"
+
+using namespace vlut;
+constexpr int G = 4, W = 12;
+using C = Cfg<G>;
+constexpr int THREADS = (W + kBuilderWarps) * 32;
+
+template <int MODE>
+__global__ void __launch_bounds__(THREADS, 1) ablate(int ntiles, unsigned long long* cyc, uint32_t* sink) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t tab_s = smem_u32(smem);
+  const uint32_t a_s = smem_u32(smem + 2 * C::TAB_BYTES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 2 * C::TAB_BYTES + C::A_BYTES);
+  const uint32_t mbar = smem_u32(smem + 2 * C::TAB_BYTES + C::A_BYTES + 16);
+  if (tid == 32) {
+    mbar_init(mbar + 0, kBuilderWarps); mbar_init(mbar + 8, kBuilderWarps);
+    mbar_init(mbar + 16, W); mbar_init(mbar + 24, W);
+  }
+  for (int i = tid; i < (2 * C::TAB_BYTES + C::A_BYTES) / 4; i += THREADS)
+    reinterpret_cast<uint32_t*>(smem)[i] = (i * 2654435761u) & 0x01FF01FFu;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(tmem_slot)), "n"(kTmemCols) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const long long t0 = clock64();
+  uint32_t out = 0;
+  if (warp >= W) {
+    const int bw = warp - W;
+    for (int u = 0; u < ntiles + 2; ++u) {
+      if (MODE >= 1 && u >= 2) mbar_wait(mbar + 16 + 8 * (u & 1), ((u >> 1) - 1) & 1);
+      if (u >= ntiles) continue;
+      if (MODE >= 2) build_tables<G>(tab_s + (u & 1) * C::TAB_BYTES, a_s, 0, bw, lane);
+      if (MODE >= 1) { __syncwarp(); if (lane == 0) mbar_arrive(mbar + 8 * (u & 1)); }
+    }
+  } else {
+    uint32_t rot[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) rot[s] = (uint32_t)(((lane + s) & 7) * 16);
+    const uint32_t taddr = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+    uint32_t sw[8][4];
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sw[s][q] = 0;
+    int32_t nneg = 0;
+    uint32_t x = 12345u + tid * 747796405u;
+    int since = 0;
+    bool first = true;
+    for (int t = 0; t < ntiles; ++t) {
+      if (MODE >= 1) mbar_wait(mbar + 8 * (t & 1), (t >> 1) & 1);
+      uint32_t iwa[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        x = x * 1664525u + 1013904223u;
+        // four random indices in [0, 81)
+        uint32_t w = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) w |= (((x >> (7 * b)) & 127u) % 81u) << (8 * b);
+        iwa[i] = w;
+      }
+      lookup_sub<G>(0, tab_s + (t & 1) * C::TAB_BYTES, iwa, rot, sw, nneg);
+      if (MODE >= 1) { __syncwarp(); if (lane == 0) mbar_arrive(mbar + 16 + 8 * (t & 1)); }
+      if (MODE >= 3 && (++since == 3 || t + 1 == ntiles)) {
+        since = 0;
+        flush_tmem<G>(sw, nneg, taddr, first);
+        first = false;
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) out += sw[s][q];
+  }
+  const long long t1 = clock64();
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tmem_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "n"(kTmemCols) : "memory");
+  }
+  sink[blockIdx.x * THREADS + tid] = out;
+  if (tid == 0) cyc[blockIdx.x] = (unsigned long long)(t1 - t0);
+}
+
+template <int MODE>
+void run(int sms, int ntiles) {
+  const int smem = 2 * C::TAB_BYTES + C::A_BYTES + 48;
+  cudaFuncSetAttribute(ablate<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  unsigned long long* cyc;
+  uint32_t* sink;
+  cudaMalloc(&cyc, sms * 8);
+  cudaMalloc(&sink, sms * THREADS * 4);
+  ablate<MODE><<<sms, THREADS, smem>>>(4, cyc, sink);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  ablate<MODE><<<sms, THREADS, smem>>>(ntiles, cyc, sink);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  unsigned long long h[1024];
+  cudaMemcpy(h, cyc, sms * 8, cudaMemcpyDeviceToHost);
+  double mc = 0;
+  for (int i = 0; i < sms; ++i) mc += h[i];
+  mc /= sms;
+  const double lookup_bytes = (double)W * 32 * ntiles * 16 * 128;  // rows x groups x 128 B
+  const double build_bytes = (MODE >= 2) ? (double)ntiles * 16 * C::HR * 128 : 0;
+  printf("mode=%d: lookups %.1f B/clk/SM, lookups+build %.1f B/clk/SM  (%.3f ms, %.0f MHz) err=%s\n",
+         MODE, lookup_bytes / mc, (lookup_bytes + build_bytes) / mc, ms, mc / (ms * 1e-3) / 1e6,
+         cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  run<0>(sms, 400);
+  run<1>(sms, 400);
+  run<2>(sms, 400);
+  run<3>(sms, 400);
+  return 0;
+}
