@@ -221,13 +221,15 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-sweep", action="store_true", help="skip the config 3/4 sweep")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-chain", action="store_true", help="skip the config-5 30-layer chain")
+    ap.add_argument("--chain-layers", type=int, default=30)
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no clock warm-up loop, no cpu/sweep/e2e legs")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
     if args.profile:
-        args.no_cpu = args.no_sweep = args.no_e2e = True
+        args.no_cpu = args.no_sweep = args.no_e2e = args.no_chain = True
 
     import torch
     import torch.distributed as dist
@@ -344,6 +346,8 @@ def main():
                "ms_per_step": e2e_ms / e2e_steps}
 
     if rank != 0:
+        if not args.no_chain:
+            chain_bench(v, dev, world, rank, args)
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
@@ -405,11 +409,59 @@ def main():
     if world == 1 and not args.no_sweep:
         line["sweep"] = sweep(v, dev, stream, flush)
 
+    if not args.no_chain:
+        line["config5"] = chain_bench(v, dev, world, rank, args)
+
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     print(json.dumps(line), flush=True)
     return 0
+
+
+def chain_bench(v, dev, world, rank, args, reps=3):
+    """BASELINE.json configs[4]: 30 BitNet-2B-shaped layers of ternary linears
+    (QKV, O, gate, up, down), N = 2048 tokens, every linear row-sharded over
+    the N GPUs with an NCCL all-gather (north star), int8 re-quantization
+    between linears (reading c14).  Weights: seeded numpy ternary, packed on
+    the device.  Times whole forwards with CUDA events, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2512_06443_b200.sharded import LayerChain, RowShardedLinear
+    cfg = synth.CONFIGS[5]
+    N = cfg.N[0]
+    L = args.chain_layers
+    layers = []
+    for l in range(L):
+        layers.append([RowShardedLinear(w, 4, synth.W_SCALE, device=dev, device_pack=True)
+                       for _, w in synth.config_weights(cfg, l)])
+    chain = LayerChain(layers)
+    x = torch.from_numpy(synth.activations_f32(2560, N, synth.act_seed(cfg, N))).to(dev)
+    xq, xs = v.quantize(x)
+    chain(xq, xs)  # warm-up forward
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        chain(xq, xs)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    t = float(np.median(ts))
+    if world > 1:
+        tt = torch.tensor([t], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt[0])
+    lookups = L * N * sum(lin.M * lin.K // 4 for lin in cfg.linears)
+    R_LU = SM_COUNT * 64 * SM_MAX_MHZ_FALLBACK * 1e6
+    return {"config": 5, "layers": L, "N": N, "n_gpus": world, "ms_per_forward": t,
+            "tokens_s": N / (t * 1e-3),
+            "frac_smem_roofline": lookups / (R_LU * world) / (t * 1e-3),
+            "step": "per layer: 5 row-sharded Vec-LUT linears (+ all-gather when n_gpus > 1) "
+                    "and 4 int8 re-quantizations; weights packed once before timing"}
 
 
 def sweep(v, dev, stream, flush, reps=10):

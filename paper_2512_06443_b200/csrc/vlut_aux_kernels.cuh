@@ -3,6 +3,7 @@
 #include <cstdint>
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
+#include "vlut_kernel.cuh"  // VLUT_STAMP (debug timing only)
 
 namespace vlut {
 
@@ -64,8 +65,10 @@ __global__ void __launch_bounds__(kQThreads)
   const int n = blockIdx.y * kQTok + col * 4;
   const int k_begin = (int)(((long long)rank * K) / CL);
   const int k_end = (int)(((long long)(rank + 1) * K) / CL);
+  VLUT_STAMP(0);
   // PDL: x may be the previous kernel's output; let the next kernel launch early
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  VLUT_STAMP(1);
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   float4 cache[kQCache];
   float m[4] = {0.f, 0.f, 0.f, 0.f};
@@ -86,6 +89,7 @@ __global__ void __launch_bounds__(kQThreads)
     m[0] = fmaxf(m[0], fabsf(a.x)); m[1] = fmaxf(m[1], fabsf(a.y));
     m[2] = fmaxf(m[2], fabsf(a.z)); m[3] = fmaxf(m[3], fabsf(a.w));
   }
+  VLUT_STAMP(2);
   // warp: lanes with equal (lane & 3) share tokens -> reduce over lane bits 2..4
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -102,7 +106,9 @@ __global__ void __launch_bounds__(kQThreads)
     for (int w = 1; w < kQThreads / 32; ++w) a = fmaxf(a, red[w][tid]);
     cta_amax[tid] = a;
   }
+  VLUT_STAMP(3);
   cluster.sync();
+  VLUT_STAMP(4);
   // 16 threads combine the cluster's partial maxima (DSMEM), the rest wait
   if (tid < kQTok) {
     float a = 0.f;
@@ -118,6 +124,7 @@ __global__ void __launch_bounds__(kQThreads)
   // this CTA's remote reads are done once its 16 readers pass here: arrive
   // early, wait only before exit (keeps cta_amax alive for the other CTAs)
   __syncthreads();
+  VLUT_STAMP(5);
   asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
   float s[4];
 #pragma unroll
@@ -145,7 +152,9 @@ __global__ void __launch_bounds__(kQThreads)
     const float v[4] = {a.x, a.y, a.z, a.w};
     for (int t = 0; t < 4 && n + t < N; ++t) q[(size_t)k * N + n + t] = q_code(v[t], s[t]);
   }
+  VLUT_STAMP(6);
   asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+  VLUT_STAMP(7);
 }
 
 // ---------------------------------------------------------------- device packer (a1)

@@ -47,8 +47,9 @@ class RowShardedLinear:
     fills ``out`` ([rows][N] fp32) -- default: the CUDA kernel.
     """
 
-    def __init__(self, W: np.ndarray, g: int, w_scale: float, device=None,
-                 compute: Optional[Callable] = None, pack: Optional[Callable] = None):
+    def __init__(self, W, g: int, w_scale: float, device=None,
+                 compute: Optional[Callable] = None, pack: Optional[Callable] = None,
+                 device_pack: bool = False):
         dist = _dist()
         self.world = dist.get_world_size() if dist else 1
         self.rank = dist.get_rank() if dist else 0
@@ -58,12 +59,22 @@ class RowShardedLinear:
         self.r0, self.r1, self.Mp = shard_rows(self.M, self.world, self.rank)
         self.rows = self.r1 - self.r0
         self.device = device
-        W_r = np.ascontiguousarray(W[self.r0:self.r1])
+        W_r = W[self.r0:self.r1]
         if pack is not None:
-            self.shard = pack(W_r, g)
+            self.shard = pack(np.ascontiguousarray(W_r), g)
+        elif not self.rows:
+            self.shard = None
+        elif device_pack:
+            # upload the trits and pack on the GPU (large weights; no validation)
+            import torch
+            import paper_2512_06443_b200 as v
+            wd = torch.as_tensor(W_r, device=device or "cuda").contiguous()
+            self.shard = v.pack_weights_device(wd, g)
+            torch.cuda.current_stream().synchronize()
+            del wd
         else:
             import paper_2512_06443_b200 as v
-            self.shard = v.pack_weights(W_r, g, device=device) if self.rows else None
+            self.shard = v.pack_weights(np.ascontiguousarray(W_r), g, device=device)
         self._compute = compute or self._cuda_compute
 
     def _cuda_compute(self, shard, A, a_scale, out):
