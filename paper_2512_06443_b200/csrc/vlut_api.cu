@@ -99,6 +99,35 @@ vlut_status check_desc(const vlut_packed_weights* W, int M, int K) {
   return VLUT_OK;
 }
 
+// ------------------------------------------------------------ TMA descriptor
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+vlut_status encode_a_map(CUtensorMap* map, const int8_t* A, int K, int N, int g) {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  static cudaError_t get_err = cudaSuccess;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    get_err = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
+    if (get_err == cudaSuccess && q == cudaDriverEntryPointSuccess) fn = (EncodeTiledFn)f;
+  });
+  if (!fn) return fail(VLUT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (%s)", cudaGetErrorString(get_err));
+  const cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)K};
+  const cuuint64_t strides[1] = {(cuuint64_t)N};
+  const cuuint32_t box[2] = {(cuuint32_t)vlut::kNcta, (cuuint32_t)(vlut::kKgTile * g)};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)A, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(VLUT_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return VLUT_OK;
+}
+
 // ------------------------------------------------------------ planner
 int smem_bytes_for(int g, int warps) {
   if (g == 4) {
@@ -235,6 +264,7 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
     return fail(VLUT_ERR_UNSUPPORTED, "needs %d B shared memory, device allows %d", smem,
                 d.smem_optin);
   vlut::Params p;
+  memset(&p, 0, sizeof(p));
   p.payload = static_cast<const uint8_t*>(W->payload);
   p.A = A;
   p.a_scale = a_scale;
@@ -248,6 +278,10 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
   p.splits = plan.splits;
   const uintptr_t ap = (uintptr_t)A;
   p.a_vec = (N % 16 == 0 && (ap & 15) == 0) ? 16 : ((N % 4 == 0 && (ap & 3) == 0) ? 4 : 1);
+  if (p.a_vec == 16) {
+    st = encode_a_map(&p.a_map, A, K, N, W->g);
+    if (st != VLUT_OK) return st;
+  }
   p.out_vec4 = (N % 4 == 0 && (((uintptr_t)out) & 15) == 0) ? 1 : 0;
   const int mcta = 32 * plan.warps;
   const long long NT = (N + vlut::kNcta - 1) / vlut::kNcta;

@@ -40,6 +40,7 @@
 #pragma once
 #include <cstdint>
 #include <cooperative_groups.h>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace vlut {
@@ -86,8 +87,8 @@ struct Layout {
   static constexpr int IDX_BYTES = MCTA * 16;
   static constexpr int A_OFF = IDX_OFF + kStageBufs * IDX_BYTES;
   static constexpr int MISC_OFF = A_OFF + kStageBufs * Cfg<G>::A_BYTES;  // tmem address
-  static constexpr int MBAR_OFF = MISC_OFF + 16;  // FULL[2], EMPTY[2] (8 B each)
-  static constexpr int SCALE_OFF = MBAR_OFF + 32;  // fl(a_scale[n] * w_scale), 64 floats
+  static constexpr int MBAR_OFF = MISC_OFF + 16;  // FULL[2], EMPTY[2], STAGE[3] (8 B each)
+  static constexpr int SCALE_OFF = MBAR_OFF + 64;  // fl(a_scale[n] * w_scale), 64 floats
   static constexpr int SMEM = SCALE_OFF + kNcta * 4;
   // epilogue: 16-byte output units per thread (upper bound, splits = 1)
   static constexpr int EPI_UNITS = (MCTA * 16 + THREADS - 1) / THREADS;
@@ -256,7 +257,8 @@ __device__ __forceinline__ void tmem_fence_after() {
 }
 
 // ---------------------------------------------------------------- params
-struct Params {
+struct alignas(64) Params {
+  CUtensorMap a_map;       // 2D TMA map of A [K][N] int8, box 64 x 16g (a_vec == 16)
   const uint8_t* payload;  // packed indices [kt][m_pad][16]
   const int8_t* A;         // [K][N]
   const float* a_scale;    // [N]
@@ -265,7 +267,7 @@ struct Params {
   int M, K, N;
   int m_pad, kg_tiles;
   int splits;              // cluster size along K
-  int a_vec;               // 16, 4 or 1: activation staging width
+  int a_vec;               // 16 (TMA), 4 or 1: activation staging width
   int out_vec4;            // 1 if out rows allow aligned 16-byte stores
 };
 
@@ -315,6 +317,66 @@ __device__ __forceinline__ void stage_tile(const Params& p, int kt, int buf, int
     }
   }
   cp_async_commit();
+}
+
+// TMA bulk staging (N % 16 == 0, 16-byte aligned A): builder warp 0 issues one
+// bulk copy for the CTA's index rows of the tile (contiguous in the payload)
+// and one per activation row; completion is counted on the stage's mbarrier.
+// Rows past K / m_pad and columns past N are zero-filled with plain stores
+// (disjoint bytes; ordered for the consumers by barrier 5 / FULL).
+__device__ __forceinline__ void mbar_expect_tx(uint32_t addr, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(addr), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(mbar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar)
+      : "memory");
+}
+
+template <int G, int WARPS>
+__device__ __forceinline__ void stage_tile_bulk(const Params& p, int kt, int buf, int m0, int n0,
+                                                uint8_t* smem, int bt, uint32_t stg_mbar,
+                                                bool do_idx, bool do_act, bool arm) {
+  using C = Cfg<G>;
+  using L = Layout<G, WARPS>;
+  constexpr int NB = kBuilderWarps * 32;
+  const int idx_rows = max(0, min(L::MCTA, p.m_pad - m0));
+  const int k0 = kt * kKgTile * G;
+  const int a_rows = max(0, min(C::A_ROWS, p.K - k0));
+  const int a_cols = max(0, min(kNcta, p.N - n0));  // multiple of 16 (N % 16 == 0)
+  uint8_t* idx_dst = smem + L::IDX_OFF + buf * L::IDX_BYTES;
+  uint8_t* a_dst = smem + L::A_OFF + buf * C::A_BYTES;
+  // zero fill of the parts no copy covers (tails only)
+  if (do_idx)
+    for (int i = idx_rows * 16 + bt * 16; i < L::MCTA * 16; i += NB * 16)
+      *reinterpret_cast<uint4*>(idx_dst + i) = make_uint4(0, 0, 0, 0);
+  (void)a_cols; (void)a_rows;
+  if (bt < 32) {
+    if (arm && bt == 0) {
+      // the A box always delivers 16g x 64 bytes (out-of-range elements are
+      // zero-filled by the TMA unit and count toward the transaction)
+      const uint32_t bytes = (uint32_t)(idx_rows * 16 + C::A_BYTES);
+      mbar_expect_tx(stg_mbar, bytes);
+    }
+    __syncwarp();
+    if (do_idx && bt == 0 && idx_rows > 0)
+      bulk_g2s(smem_u32(idx_dst), p.payload + ((size_t)kt * p.m_pad + m0) * 16,
+               (uint32_t)(idx_rows * 16), stg_mbar);
+    if (do_act && bt == 0) tma_load_2d(smem_u32(a_dst), &p.a_map, n0, k0, stg_mbar);
+  }
 }
 
 // ---------------------------------------------------------------- table build (a3)
@@ -473,7 +535,7 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 // ---------------------------------------------------------------- the kernel
 template <int G, int WARPS, bool ACC_ONLY>
 __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
-    vlut_mpgemm_kernel(const Params p) {
+    vlut_mpgemm_kernel(const __grid_constant__ Params p) {
   using C = Cfg<G>;
   using L = Layout<G, WARPS>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -503,6 +565,10 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
     mbar_init(mbar + 8, kBuilderWarps);
     mbar_init(mbar + 16, WARPS);
     mbar_init(mbar + 24, WARPS);
+    mbar_init(mbar + 32, 1);  // STAGE[0..2]: bulk-copy completion of a staged tile
+    mbar_init(mbar + 40, 1);
+    mbar_init(mbar + 48, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();  // mbarriers initialised
 
@@ -511,12 +577,19 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
     // =========================== builder warps: staging + table builds
     const int bt = tid - L::BUILDER0;
     const int bw = warp - WARPS;
+    const bool bulk = (p.a_vec == 16);
     if (ntiles > 0) {
       // the packed weights do not depend on the previous kernel: stage tile
       // 0's indices before waiting for it, then its activations
-      stage_tile<G, WARPS>(p, kt_begin, 0, m0, n0, smem, bt, /*what=*/1);
-      pdl_wait();
-      stage_tile<G, WARPS>(p, kt_begin, 0, m0, n0, smem, bt, /*what=*/2);
+      if (bulk) {
+        stage_tile_bulk<G, WARPS>(p, kt_begin, 0, m0, n0, smem, bt, mbar + 32, true, false, true);
+        pdl_wait();
+        stage_tile_bulk<G, WARPS>(p, kt_begin, 0, m0, n0, smem, bt, mbar + 32, false, true, false);
+      } else {
+        stage_tile<G, WARPS>(p, kt_begin, 0, m0, n0, smem, bt, /*what=*/1);
+        pdl_wait();
+        stage_tile<G, WARPS>(p, kt_begin, 0, m0, n0, smem, bt, /*what=*/2);
+      }
     } else {
       pdl_wait();
     }
@@ -530,7 +603,14 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
       if (u >= nsub) continue;
       const int T = u / C::SUBS, sub = u - T * C::SUBS;
       if (sub == 0) {
-        if (T + 1 < ntiles) {
+        if (bulk) {
+          if (T + 1 < ntiles) {
+            const int b1 = (T + 1) % kStageBufs;
+            stage_tile_bulk<G, WARPS>(p, kt_begin + T + 1, b1, m0, n0, smem, bt, mbar + 32 + 8 * b1,
+                                      true, true, true);
+          }
+          mbar_wait(mbar + 32 + 8 * (T % kStageBufs), (T / kStageBufs) & 1);
+        } else if (T + 1 < ntiles) {
           stage_tile<G, WARPS>(p, kt_begin + T + 1, (T + 1) % kStageBufs, m0, n0, smem, bt, 3);
           asm volatile("cp.async.wait_group 1;\n" ::: "memory");
         } else {

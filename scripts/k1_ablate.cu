@@ -6,6 +6,8 @@
 //   mode 1: + FULL/EMPTY named-barrier handshake with 4 idle builder warps
 //   mode 2: + builders really build the half tables (Gray walks, STS)
 //   mode 3: + TMEM flush every 3 K-tiles
+//   mode 4: + builders stage A and index tiles from HBM with cp.async (Params)
+//   mode 5: + lookup warps take their indices from the staged tiles
 //   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o k1_ablate k1_ablate.cu
 #include <cstdio>
 #include "../paper_2512_06443_b200/csrc/vlut_kernel.cuh"
@@ -14,9 +16,13 @@ using namespace vlut;
 constexpr int G = 4, W = 12;
 using C = Cfg<G>;
 constexpr int THREADS = (W + kBuilderWarps) * 32;
+// staging buffers live after the tables (the kernel layout's IDX/A offsets,
+// rebased so that they start at STAGE_BASE + IDX_OFF)
+constexpr int STAGE_BASE = 2 * Cfg<G>::TAB_BYTES + Cfg<G>::A_BYTES + 64 - Layout<G, W>::IDX_OFF;
 
 template <int MODE>
-__global__ void __launch_bounds__(THREADS, 1) ablate(int ntiles, unsigned long long* cyc, uint32_t* sink) {
+__global__ void __launch_bounds__(THREADS, 1) ablate(int ntiles, unsigned long long* cyc, uint32_t* sink,
+                                                      Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t tab_s = smem_u32(smem);
@@ -45,7 +51,18 @@ __global__ void __launch_bounds__(THREADS, 1) ablate(int ntiles, unsigned long l
     for (int u = 0; u < ntiles + 2; ++u) {
       if (MODE >= 1 && u >= 2) mbar_wait(mbar + 16 + 8 * (u & 1), ((u >> 1) - 1) & 1);
       if (u >= ntiles) continue;
-      if (MODE >= 2) build_tables<G>(tab_s + (u & 1) * C::TAB_BYTES, a_s, 0, bw, lane);
+      if (MODE >= 4) {
+        if (u + 1 < ntiles) {
+          if (MODE != 6) stage_tile<G, W>(p, u + 1, (u + 1) % kStageBufs, 0, 0, smem + STAGE_BASE, tid - W * 32, 3);
+          if (MODE != 7) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+          if (MODE != 7) cp_async_wait_all();
+        }
+        if (MODE != 7) bar_sync(5, kBuilderWarps * 32);
+      }
+      if (MODE >= 2) build_tables<G>(tab_s + (u & 1) * C::TAB_BYTES,
+                                     MODE >= 4 ? smem_u32(smem + STAGE_BASE + Layout<G, W>::A_OFF + (u % kStageBufs) * C::A_BYTES) : a_s,
+                                     0, bw, lane);
       if (MODE >= 1) { __syncwarp(); if (lane == 0) mbar_arrive(mbar + 8 * (u & 1)); }
     }
   } else {
@@ -65,6 +82,10 @@ __global__ void __launch_bounds__(THREADS, 1) ablate(int ntiles, unsigned long l
     for (int t = 0; t < ntiles; ++t) {
       if (MODE >= 1) mbar_wait(mbar + 8 * (t & 1), (t >> 1) & 1);
       uint32_t iwa[4];
+      if (MODE == 5) {
+        const uint4 iw = lds128(smem_u32(smem + STAGE_BASE + Layout<G, W>::IDX_OFF) + (t % kStageBufs) * Layout<G, W>::IDX_BYTES + tid * 16);
+        iwa[0] = iw.x % 81u; iwa[1] = iw.y; iwa[2] = iw.z; iwa[3] = iw.w;
+      } else
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         x = x * 1664525u + 1013904223u;
@@ -100,18 +121,28 @@ __global__ void __launch_bounds__(THREADS, 1) ablate(int ntiles, unsigned long l
 
 template <int MODE>
 void run(int sms, int ntiles) {
-  const int smem = 2 * C::TAB_BYTES + C::A_BYTES + 48;
+  const int smem = 2 * C::TAB_BYTES + C::A_BYTES + 64 + 3 * Layout<G, W>::IDX_BYTES + 3 * C::A_BYTES;
   cudaFuncSetAttribute(ablate<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   unsigned long long* cyc;
   uint32_t* sink;
   cudaMalloc(&cyc, sms * 8);
   cudaMalloc(&sink, sms * THREADS * 4);
-  ablate<MODE><<<sms, THREADS, smem>>>(4, cyc, sink);
+  // a real packed-index / activation stream in HBM (values random, in range)
+  Params p = {};
+  const int M = W * 32, K = ntiles * 16 * G, N = 64;
+  uint8_t* payload; int8_t* A;
+  cudaMalloc(&payload, (size_t)ntiles * M * 16);
+  cudaMalloc(&A, (size_t)K * N);
+  cudaMemset(payload, 40, (size_t)ntiles * M * 16);
+  cudaMemset(A, 3, (size_t)K * N);
+  p.payload = payload; p.A = A; p.M = M; p.K = K; p.N = N; p.m_pad = M; p.kg_tiles = ntiles;
+  p.splits = 1; p.a_vec = 16; p.out_vec4 = 1;
+  ablate<MODE><<<sms, THREADS, smem>>>(4, cyc, sink, p);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   cudaEventRecord(a);
-  ablate<MODE><<<sms, THREADS, smem>>>(ntiles, cyc, sink);
+  ablate<MODE><<<sms, THREADS, smem>>>(ntiles, cyc, sink, p);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms;
@@ -135,5 +166,9 @@ int main() {
   run<1>(sms, 400);
   run<2>(sms, 400);
   run<3>(sms, 400);
+  run<4>(sms, 400);
+  run<5>(sms, 400);
+  run<6>(sms, 400);
+  run<7>(sms, 400);
   return 0;
 }

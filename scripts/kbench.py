@@ -58,7 +58,8 @@ def main():
             for sp in (1, 2, 4):
                 rows.append(time_one(6912, 2560, 256, 4, plan=v.LaunchPlan(w, sp)))
     for r in rows:
-        print(json.dumps(r))
+        print(f"M={r['M']:6d} K={r['K']:6d} N={r['N']:5d} g={r['g']} plan={r['plan'][:48]:48s} "
+              f"us={r['us']:9.2f} frac={r['frac_roof']:.3f}")
 
 
 if __name__ == "__main__":
