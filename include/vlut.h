@@ -91,7 +91,7 @@ typedef struct {
  */
 typedef struct {
   int32_t warps;        /* 8, 12 or 16                                      */
-  int32_t splits;       /* 1, 2 or 4 (cluster size along K)                  */
+  int32_t splits;       /* 1..8 with (32*warps) % splits == 0 (cluster size along K) */
   int32_t m_cta;        /* 32 * warps                                       */
   int32_t n_cta;        /* 64                                               */
   int32_t grid_ctas;    /* total CTAs launched                              */

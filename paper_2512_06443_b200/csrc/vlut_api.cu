@@ -140,39 +140,106 @@ int smem_bytes_for(int g, int warps) {
   return vlut::Layout<5, 16>::SMEM;
 }
 
-// Cost model (shared-memory cycles per CTA):
-//   lookups   m_cta * 64 tokens * 2 B per group  /128 B/clk
-//   build     3^g * 128 B per group               /128 B/clk
-//   reduce    (S-1)/S * m_cta * 256 B over DSMEM   / ~20 B/clk
-// total = waves * per-CTA, waves = ceil(CTAs / slots), slots = SMs (cluster
-// sizes <= 2) or 132 (cluster 4, which strands SMs on some GPCs).
+// ------------------------------------------------------------ occupancy
+template <int G, int WARPS, bool ACC>
+cudaError_t prepare_kernel() {
+  using L = vlut::Layout<G, WARPS>;
+  static std::once_flag flags[64];
+  static cudaError_t errs[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::call_once(flags[dev & 63], [&] {
+    errs[dev & 63] = cudaFuncSetAttribute(vlut::vlut_mpgemm_kernel<G, WARPS, ACC>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+  });
+  return errs[dev & 63];
+}
+
+// Co-resident clusters of size S for a variant (cudaOccupancyMaxActiveClusters,
+// cached per device): clusters larger than 2 can strand SMs of a GPC.
+template <int G, int WARPS>
+int active_clusters(int S) {
+  using L = vlut::Layout<G, WARPS>;
+  static std::mutex mu;
+  static int cache[64][9];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || S < 1 || S > 8) return 0;
+  std::lock_guard<std::mutex> lk(mu);
+  int& c = cache[dev & 63][S];
+  if (c == 0) {
+    if (prepare_kernel<G, WARPS, false>() != cudaSuccess) return 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)S, 1, 1);
+    cfg.blockDim = dim3(L::THREADS, 1, 1);
+    cfg.dynamicSmemBytes = L::SMEM;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)S;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, vlut::vlut_mpgemm_kernel<G, WARPS, false>, &cfg) !=
+            cudaSuccess ||
+        n <= 0) {
+      cudaGetLastError();
+      n = -1;  // cluster size unusable
+    }
+    c = n;
+  }
+  return c;
+}
+
+int active_clusters_for(int g, int warps, int S) {
+  if (g == 4) {
+    if (warps == 8) return active_clusters<4, 8>(S);
+    if (warps == 12) return active_clusters<4, 12>(S);
+    return active_clusters<4, 16>(S);
+  }
+  if (warps == 8) return active_clusters<5, 8>(S);
+  if (warps == 12) return active_clusters<5, 12>(S);
+  return active_clusters<5, 16>(S);
+}
+
+inline bool valid_split(int warps, int S) { return S >= 1 && S <= 8 && (32 * warps) % S == 0; }
+
+// Cost model in shared-memory cycles (DESIGN.md §4 planner):
+//   per K-tile   16 groups x (m_cta lookup rows + (3^g+1)/2 half-table rows)
+//                (one 128-B wavefront per row and group)
+//   per CTA      tiles x per-tile + fixed start/epilogue + DSMEM reduction of
+//                (S-1)/S of the m_cta x 256 B int32 tile at ~16 B/clk
+//   total        waves x per-CTA, waves = ceil(CTAs / (active clusters x S))
 void plan_for(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
   const int KG = K / g;
   const int kgt = (KG + VLUT_KG_TILE - 1) / VLUT_KG_TILE;
   const int NT = (N + vlut::kNcta - 1) / vlut::kNcta;
-  const int rows = pow3i(g);
+  const int half_rows = (pow3i(g) + 1) / 2;
   double best_cost = 1e300;
   const int warps_opts[3] = {16, 12, 8};
-  const int split_opts[3] = {1, 2, 4};
+  const int split_opts[6] = {1, 2, 3, 4, 6, 8};
   for (int wi = 0; wi < 3; ++wi) {
     const int warps = warps_opts[wi];
     const int mcta = 32 * warps;
     const long long MT = (M + mcta - 1) / mcta;
-    for (int si = 0; si < 3; ++si) {
+    for (int si = 0; si < 6; ++si) {
       const int S = split_opts[si];
-      if (S > kgt) continue;
+      if (!valid_split(warps, S) || S > kgt) continue;
       const long long ctas = MT * NT * S;
       if (ctas > 65535LL * 65535LL) continue;
-      const int slots = (S <= 2) ? (sms / S) * S : (sms * 132 / 148 / S) * S;
+      int clusters = active_clusters_for(g, warps, S);
+      if (clusters < 0) continue;
+      if (clusters == 0) clusters = sms / S;  // no device query possible
+      const long long slots = (long long)clusters * S;
       if (slots <= 0) continue;
       const long long waves = (ctas + slots - 1) / slots;
       const double tiles = (double)((kgt + S - 1) / S);
-      const double per_group = (double)mcta * 128.0 / 128.0 + rows;  // SMEM cycles
-      double per_cta = tiles * VLUT_KG_TILE * per_group;
-      per_cta += 2000.0;  // prologue / epilogue
-      if (S > 1) per_cta += (double)(S - 1) / S * mcta * 256.0 / 20.0;
+      double per_cta = tiles * VLUT_KG_TILE * (double)(mcta + half_rows);
+      per_cta += 6000.0;  // start (first tile + table) and epilogue
+      if (S > 1) per_cta += (double)(S - 1) / S * mcta * 256.0 / 16.0;
       const double cost = waves * per_cta;
-      if (cost < best_cost * 0.999) {
+      if (cost < best_cost * 0.995) {
         best_cost = cost;
         best->warps = warps;
         best->splits = S;
@@ -190,14 +257,7 @@ template <int G, int WARPS, bool ACC>
 vlut_status launch_k1(const vlut::Params& p, int S, int NT, int MT, cudaStream_t st) {
   using L = vlut::Layout<G, WARPS>;
   auto kern = vlut::vlut_mpgemm_kernel<G, WARPS, ACC>;
-  static std::once_flag flags[64];
-  int dev = 0;
-  VLUT_CUDA_TRY(cudaGetDevice(&dev));
-  cudaError_t attr_err = cudaSuccess;
-  std::call_once(flags[dev & 63], [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
-  });
-  VLUT_CUDA_TRY(attr_err);
+  VLUT_CUDA_TRY((prepare_kernel<G, WARPS, ACC>()));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)S, (unsigned)NT, (unsigned)MT);
   cfg.blockDim = dim3(L::THREADS, 1, 1);
@@ -252,7 +312,7 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
   if (plan_in) {
     plan = *plan_in;
     if (!(plan.warps == 8 || plan.warps == 12 || plan.warps == 16) ||
-        !(plan.splits == 1 || plan.splits == 2 || plan.splits == 4))
+        !valid_split(plan.warps, plan.splits))
       return fail(VLUT_ERR_INVALID_ARGUMENT, "invalid plan warps=%d splits=%d", plan.warps,
                   plan.splits);
   } else {
