@@ -515,6 +515,31 @@ def sweep(v, dev, stream, flush, reps=10):
                     "us": t * 1e6, "frac_smem_roofline": lk / R_LU / t})
     res.append({"config": 3, "linear": "all 5 in sequence", "N": 1024, "us": tot * 1e6,
                 "tokens_s": 1024 / tot})
+    # mixed g=5/g=4 schedule (f2) on config 3's K = 4096 / 14336 linears
+    for j in (0, 4):
+        lin = c3.linears[j]
+        W = synth.ternary_weights(lin.M, lin.K, synth.weight_seed(c3, 0, j))
+        pm = v.pack_weights_mixed(W, device=dev)
+        x = torch.from_numpy(synth.activations_f32(lin.K, 1024, synth.act_seed(c3, 1024, j))).to(dev)
+        A, sc = v.quantize(x)
+        out = torch.empty((lin.M, 1024), dtype=torch.float32, device=dev)
+        for _ in range(2):
+            v.mpgemm_mixed(pm, A, sc, synth.W_SCALE, out=out, stream=stream)
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            v.mpgemm_mixed(pm, A, sc, synth.W_SCALE, out=out, stream=stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) * 1e-3)
+        t = float(np.median(ts))
+        k5, k4 = v.group_schedule(lin.K)
+        lk = lin.M * (k5 // 5 + k4 // 4) * 1024
+        res.append({"config": 3, "linear": lin.name + " (mixed g5/g4)", "M": lin.M, "K": lin.K,
+                    "N": 1024, "k5": k5, "k4": k4, "bpw": 8.0 * (k5 / 5 + k4 / 4) / lin.K,
+                    "us": t * 1e6, "frac_smem_roofline": lk / R_LU / t})
     return res
 
 

@@ -169,6 +169,24 @@ vlut_status vlut_mpgemm_acc(const vlut_packed_weights* W, const int8_t* A,
                             const vlut_launch_plan* plan, void* stream);
 
 /*
+ * Flexible sub-2-bit packing: split K into b groups of
+ * g=5 followed by a groups of g=4, 5b + 4a = K, b maximal.  k5 = 5b, k4 = 4a
+ * features.  VLUT_ERR_SHAPE if K has no such split (K in {1,2,3,6,7,11}).
+ */
+vlut_status vlut_group_schedule(int K, int* k5, int* k4);
+
+/*
+ * mpGeMM over a mixed schedule: W5 packs features [0, k5) with g=5 (NULL if
+ * k5 == 0), W4 packs features [k5, K) with g=4 (NULL if k4 == 0); both have
+ * M rows.  Same result and contract as vlut_mpgemm on the whole K (two
+ * launches: the g=5 part writes raw int32 partials into `out`, the g=4 part
+ * adds them before the fp32 epilogue).
+ */
+vlut_status vlut_mpgemm_mixed(const vlut_packed_weights* W5, const vlut_packed_weights* W4,
+                              const int8_t* A, const float* a_scale, float w_scale, float* out,
+                              int M, int K, int N, void* stream);
+
+/*
  * Per-token absmax int8 quantizer (a7; w1.6A8 named at P:102; formula
  * S:339-347, reading c8), IEEE single precision throughout:
  *   x'[k][n] = x[k][n] * (y ? y[k][n] : 1)      (fp32 multiply, config 5's

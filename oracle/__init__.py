@@ -272,3 +272,22 @@ def config5_layer(Ws, w_scale: float, x_q: np.ndarray, x_s: np.ndarray,
     hq, hs = quantize(h)
     d = mpgemm_f32(W_down, hq, hs, w_scale)
     return quantize(d)
+
+
+def group_schedule(K: int):
+    """Flexible sub-2-bit packing: split K into b groups
+    of 5 followed by a groups of 4 with 5b + 4a = K, maximising b (reading of
+    the footnote's condition).  Returns (b, a).  ValueError if no
+    non-negative (a, b) exists (e.g. K in {1, 2, 3, 6, 7, 11})."""
+    if K < 4:
+        raise ValueError("unrepresentable K")
+    for b in range(K // 5, -1, -1):
+        if (K - 5 * b) % 4 == 0:
+            return b, (K - 5 * b) // 4
+    raise ValueError("unrepresentable K")
+
+
+def mixed_bits_per_weight(K: int) -> float:
+    """8 * (number of groups) / K for the mixed schedule."""
+    b, a = group_schedule(K)
+    return 8.0 * (a + b) / K

@@ -23,7 +23,8 @@ import numpy as np
 __all__ = [
     "VlutError", "PackedWeights", "LaunchPlan", "lib", "lib_path", "packed_bytes",
     "pack_weights", "pack_weights_device", "unpack_weights_host", "plan", "mpgemm",
-    "mpgemm_ex", "mpgemm_acc", "quantize", "last_error", "EXPORTS",
+    "mpgemm_ex", "mpgemm_acc", "quantize", "last_error", "EXPORTS", "group_schedule",
+    "MixedPackedWeights", "pack_weights_mixed", "mpgemm_mixed",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -86,6 +87,11 @@ EXPORTS = {
                          ctypes.c_void_p], ctypes.c_int),
     "vlut_quantize": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "vlut_group_schedule": ([ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                             ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "vlut_mpgemm_mixed": ([ctypes.POINTER(_Desc), ctypes.POINTER(_Desc), ctypes.c_void_p,
+                           ctypes.c_void_p, ctypes.c_float, ctypes.c_void_p, ctypes.c_int,
+                           ctypes.c_int, ctypes.c_int, ctypes.c_void_p], ctypes.c_int),
     "vlut_launches_per_mpgemm": ([], ctypes.c_int),
     "vlut_last_error": ([], ctypes.c_char_p),
     "vlut_version": ([], ctypes.c_char_p),
@@ -285,3 +291,45 @@ def quantize(x, y=None, q=None, scale=None, stream=None):
     _check(lib().vlut_quantize(_dev_ptr(x), _dev_ptr(y), K, N, _dev_ptr(q), _dev_ptr(scale),
                                _stream_ptr(stream)))
     return q, scale
+
+
+# ---------------------------------------------------------------- mixed g=5/g=4 (f2)
+def group_schedule(K: int):
+    """(k5, k4): features packed with g=5 first, then g=4."""
+    k5, k4 = ctypes.c_int(0), ctypes.c_int(0)
+    _check(lib().vlut_group_schedule(K, ctypes.byref(k5), ctypes.byref(k4)))
+    return k5.value, k4.value
+
+
+class MixedPackedWeights:
+    """A (g=5 part, g=4 part) pair covering K = k5 + k4 (either may be None)."""
+
+    def __init__(self, w5: Optional[PackedWeights], w4: Optional[PackedWeights], M: int, K: int):
+        self.w5, self.w4, self.M, self.K = w5, w4, M, K
+
+    @property
+    def nbytes(self):
+        return sum(w.nbytes for w in (self.w5, self.w4) if w is not None)
+
+
+def pack_weights_mixed(w_trits: np.ndarray, device=None, stream=None) -> MixedPackedWeights:
+    """Host trits int8 [M][K] -> the mixed g=5/g=4 packing (~1.6 BPW for any
+    representable K)."""
+    w = np.ascontiguousarray(w_trits, dtype=np.int8)
+    M, K = w.shape
+    k5, k4 = group_schedule(K)
+    w5 = pack_weights(np.ascontiguousarray(w[:, :k5]), 5, device, stream) if k5 else None
+    w4 = pack_weights(np.ascontiguousarray(w[:, k5:]), 4, device, stream) if k4 else None
+    return MixedPackedWeights(w5, w4, M, K)
+
+
+def mpgemm_mixed(W: MixedPackedWeights, A, a_scale, w_scale: float, out=None, stream=None):
+    import torch
+    K, N = A.shape
+    if out is None:
+        out = torch.empty((W.M, N), dtype=torch.float32, device=A.device)
+    d5 = ctypes.byref(W.w5.desc) if W.w5 is not None else ctypes.POINTER(_Desc)()
+    d4 = ctypes.byref(W.w4.desc) if W.w4 is not None else ctypes.POINTER(_Desc)()
+    _check(lib().vlut_mpgemm_mixed(d5, d4, _dev_ptr(A), _dev_ptr(a_scale), float(w_scale),
+                                   _dev_ptr(out), W.M, K, N, _stream_ptr(stream)))
+    return out

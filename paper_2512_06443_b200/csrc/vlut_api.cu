@@ -294,7 +294,8 @@ vlut_status dispatch(int g, int warps, const vlut::Params& p, int S, int NT, int
 
 vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,
                        float w_scale, void* out, int M, int K, int N,
-                       const vlut_launch_plan* plan_in, void* stream, bool acc_only) {
+                       const vlut_launch_plan* plan_in, void* stream, bool acc_only,
+                       const int32_t* acc_in = nullptr) {
   if (M < 0 || K <= 0 || N < 0) return fail(VLUT_ERR_INVALID_ARGUMENT, "bad sizes M=%d K=%d N=%d", M, K, N);
   if (M == 0 || N == 0) return ok();
   vlut_status st = check_desc(W, M, K);
@@ -330,6 +331,7 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
   p.a_scale = a_scale;
   p.w_scale = w_scale;
   p.out = static_cast<float*>(out);
+  p.acc_in = acc_in;
   p.M = M;
   p.K = K;
   p.N = N;
@@ -504,6 +506,40 @@ vlut_status vlut_mpgemm_ex(const vlut_packed_weights* W, const int8_t* A, const 
 vlut_status vlut_mpgemm_acc(const vlut_packed_weights* W, const int8_t* A, int32_t* acc_out,
                             int M, int K, int N, const vlut_launch_plan* plan, void* stream) {
   return run_mpgemm(W, A, nullptr, 0.f, acc_out, M, K, N, plan, stream, true);
+}
+
+vlut_status vlut_group_schedule(int K, int* k5, int* k4) {
+  if (!k5 || !k4) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL argument");
+  for (int b = K / 5; b >= 0 && K >= 4; --b) {
+    if ((K - 5 * b) % 4 == 0) {
+      *k5 = 5 * b;
+      *k4 = K - 5 * b;
+      return ok();
+    }
+  }
+  return fail(VLUT_ERR_SHAPE, "K=%d is not 5b + 4a with a, b >= 0", K);
+}
+
+vlut_status vlut_mpgemm_mixed(const vlut_packed_weights* W5, const vlut_packed_weights* W4,
+                              const int8_t* A, const float* a_scale, float w_scale, float* out,
+                              int M, int K, int N, void* stream) {
+  int k5 = 0, k4 = 0;
+  vlut_status st = vlut_group_schedule(K, &k5, &k4);
+  if (st != VLUT_OK) return st;
+  if (M == 0 || N == 0) return ok();
+  if (k5 && (!W5 || W5->g != 5 || W5->K != k5))
+    return fail(VLUT_ERR_SHAPE, "W5 must hold the first %d features with g=5", k5);
+  if (k4 && (!W4 || W4->g != 4 || W4->K != k4))
+    return fail(VLUT_ERR_SHAPE, "W4 must hold the last %d features with g=4", k4);
+  if (!A) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL A");
+  if (k4 == 0) return run_mpgemm(W5, A, a_scale, w_scale, out, M, k5, N, nullptr, stream, false);
+  if (k5 == 0) return run_mpgemm(W4, A, a_scale, w_scale, out, M, k4, N, nullptr, stream, false);
+  // g=5 groups first: raw int32 partial into `out` (same size), then the g=4
+  // groups on the remaining activation rows add it before the fp32 epilogue
+  st = run_mpgemm(W5, A, nullptr, 0.f, out, M, k5, N, nullptr, stream, true);
+  if (st != VLUT_OK) return st;
+  return run_mpgemm(W4, A + (size_t)k5 * N, a_scale, w_scale, out, M, k4, N, nullptr, stream,
+                    false, reinterpret_cast<const int32_t*>(out));
 }
 
 vlut_status vlut_quantize(const float* x, const float* y, int K, int N, int8_t* q, float* scale,

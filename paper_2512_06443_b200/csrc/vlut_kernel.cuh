@@ -264,6 +264,7 @@ struct alignas(64) Params {
   const float* a_scale;    // [N]
   float w_scale;
   float* out;              // [M][N] fp32 (or int32 when ACC_ONLY)
+  const int32_t* acc_in;   // optional int32 [M][N] added before the epilogue (may alias out)
   int M, K, N;
   int m_pad, kg_tiles;
   int splits;              // cluster size along K
@@ -783,7 +784,18 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
       const int m = m0 + r_begin + (e >> 4);
       const int n = n0 + 4 * u;
       if (m >= p.M || n >= p.N) continue;
-      const int4 vv4 = acc4[i];
+      int4 vv4 = acc4[i];
+      if (p.acc_in) {  // chained K ranges (mixed g=5/g=4 schedule): add the prior partial
+        const int32_t* src = p.acc_in + (size_t)m * p.N + n;
+        if (p.out_vec4 && n + 3 < p.N) {
+          const int4 w = __ldcg(reinterpret_cast<const int4*>(src));
+          vv4.x += w.x; vv4.y += w.y; vv4.z += w.z; vv4.w += w.w;
+        } else {
+          int t4[4] = {0, 0, 0, 0};
+          for (int k = 0; k < 4 && n + k < p.N; ++k) t4[k] = __ldcg(src + k);
+          vv4.x += t4[0]; vv4.y += t4[1]; vv4.z += t4[2]; vv4.w += t4[3];
+        }
+      }
       if constexpr (ACC_ONLY) {
         int32_t* o = reinterpret_cast<int32_t*>(p.out) + (size_t)m * p.N + n;
         if (p.out_vec4 && n + 3 < p.N) {

@@ -186,3 +186,14 @@ def test_reduction_tile_swizzle_is_conflict_free():
             u = lane % 16
             addrs.append(r * 256 + (u ^ ((r >> 2) & 1)) * 16)
         assert wavefronts_128(addrs) == 4
+
+
+def test_group_schedule_abi_matches_oracle():
+    for K in list(range(4, 200)) + [2560, 4096, 6912, 14336, 23040]:
+        try:
+            b, a = oracle.group_schedule(K)
+        except ValueError:
+            with pytest.raises(v.VlutError):
+                v.group_schedule(K)
+            continue
+        assert v.group_schedule(K) == (5 * b, 4 * a)

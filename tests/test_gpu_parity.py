@@ -247,3 +247,23 @@ def test_config5_chain_two_layers_sampled_tokens(v):
         torch.cuda.synchronize()
         assert np.array_equal(xs.cpu().numpy()[cols], s_ref)
         assert np.array_equal(xq.cpu().numpy()[:, cols], q_ref)
+
+
+# ------------------------------------------------------------------ mixed g=5/g=4 schedule (f2)
+@pytest.mark.parametrize("M,K,N", [(300, 4096, 130), (77, 22, 5), (500, 6912, 64), (64, 20, 16),
+                                   (128, 16, 32)])
+def test_mpgemm_mixed_matches_oracle(v, M, K, N):
+    W = synth.ternary_weights(M, K, seed=K)
+    x = synth.activations_f32(K, N, seed=N)
+    q, s = oracle.quantize(x)
+    pw = v.pack_weights_mixed(W, device=dev())
+    k5, k4 = v.group_schedule(K)
+    assert (pw.w5 is None) == (k5 == 0) and (pw.w4 is None) == (k4 == 0)
+    out = v.mpgemm_mixed(pw, to_dev(q), to_dev(s), synth.W_SCALE)
+    torch.cuda.synchronize()
+    check_fp32(out.cpu().numpy(), oracle.gemm_i32(W, q), s, synth.W_SCALE)
+    # bits per weight of the logical mixed packing (near 1.6 for common shapes)
+    bpw = 8.0 * (k5 / 5 + k4 / 4) / K
+    assert bpw == pytest.approx(oracle.mixed_bits_per_weight(K))
+    if K >= 100:
+        assert bpw < 1.61

@@ -322,3 +322,31 @@ def test_config5_layer_smoke():
     q, s = oracle.config5_layer(Ws, synth.W_SCALE, xq, xs, q_rows=K)
     assert q.shape == (K, N) and s.shape == (N,)
     assert np.all(s > 0) and np.abs(q.astype(int)).max() <= 127
+
+
+# ------------------------------------------------------------------ mixed g=5/g=4 schedule (f2)
+def test_group_schedule_examples():
+    # (K=20, I1) -> all 5s; K=4096 mixed -> 816 fives then 4 fours,
+    # BPW = 8*820/4096 ~ 1.6016; K=7 unrepresentable
+    assert oracle.group_schedule(20) == (4, 0)
+    assert oracle.group_schedule(4096) == (816, 4)
+    assert oracle.mixed_bits_per_weight(4096) == pytest.approx(8 * 820 / 4096)
+    assert round(oracle.mixed_bits_per_weight(4096), 4) == 1.6016
+    for bad in (1, 2, 3, 6, 7, 11):
+        with pytest.raises(ValueError):
+            oracle.group_schedule(bad)
+
+
+def test_group_schedule_properties():
+    for K in range(12, 3000):
+        b, a = oracle.group_schedule(K)
+        assert 5 * b + 4 * a == K and a >= 0 and b >= 0
+        # maximal b: one more 5-group never leaves a multiple of 4
+        assert all((K - 5 * bb) % 4 for bb in range(b + 1, K // 5 + 1))
+        bpw = oracle.mixed_bits_per_weight(K)
+        assert 1.6 <= bpw <= 2.0
+        if K >= 100:
+            assert bpw < 1.7
+    # the paper's shapes that 5 does not divide (P:445-447 motivation)
+    for K in (4096, 6912, 14336):
+        assert K % 5 and oracle.group_schedule(K)[0] > 0
