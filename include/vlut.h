@@ -187,6 +187,29 @@ vlut_status vlut_mpgemm_mixed(const vlut_packed_weights* W5, const vlut_packed_w
                               int M, int K, int N, void* stream);
 
 /*
+ * Fused feature-major transpositions: frameworks hold activations
+ * and outputs as [N][K] / [N][M] (feature axis contiguous).
+ *   flags & VLUT_OUT_FEATURE_MAJOR: `out` is written as [N][M] (the K1
+ *   epilogue writes the transposed tile; same values as vlut_mpgemm).
+ */
+#define VLUT_OUT_FEATURE_MAJOR 1
+vlut_status vlut_mpgemm_layout(const vlut_packed_weights* W, const int8_t* A,
+                               const float* a_scale, float w_scale, float* out, int M, int K,
+                               int N, int flags, void* stream);
+
+/* vlut_quantize on feature-major input: x, y device fp32 [N][K] (y may be
+ * NULL) -> q device int8 [K][N] (token-contiguous, the layout the mpGeMM
+ * consumes) and scale [N]; same codes and scales as vlut_quantize(x^T). */
+vlut_status vlut_quantize_t(const float* x, const float* y, int K, int N, int8_t* q,
+                            float* scale, void* stream);
+
+/* A framework-layout ternary linear: y[N][M] = dequant(W x quant(x)^T) for
+ * x fp32 [N][K]; q_ws (int8 [K][N]) and s_ws (fp32 [N]) are caller-provided
+ * device workspaces.  Two launches (vlut_quantize_t, vlut_mpgemm_layout). */
+vlut_status vlut_linear(const vlut_packed_weights* W, const float* x, float w_scale, float* y,
+                        int M, int K, int N, int8_t* q_ws, float* s_ws, void* stream);
+
+/*
  * Per-token absmax int8 quantizer (a7; w1.6A8 named at P:102; formula
  * S:339-347, reading c8), IEEE single precision throughout:
  *   x'[k][n] = x[k][n] * (y ? y[k][n] : 1)      (fp32 multiply, config 5's

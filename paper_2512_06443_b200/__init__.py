@@ -24,7 +24,8 @@ __all__ = [
     "VlutError", "PackedWeights", "LaunchPlan", "lib", "lib_path", "packed_bytes",
     "pack_weights", "pack_weights_device", "unpack_weights_host", "plan", "mpgemm",
     "mpgemm_ex", "mpgemm_acc", "quantize", "last_error", "EXPORTS", "group_schedule",
-    "MixedPackedWeights", "pack_weights_mixed", "mpgemm_mixed",
+    "MixedPackedWeights", "pack_weights_mixed", "mpgemm_mixed", "mpgemm_layout", "quantize_t",
+    "linear",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -92,6 +93,14 @@ EXPORTS = {
     "vlut_mpgemm_mixed": ([ctypes.POINTER(_Desc), ctypes.POINTER(_Desc), ctypes.c_void_p,
                            ctypes.c_void_p, ctypes.c_float, ctypes.c_void_p, ctypes.c_int,
                            ctypes.c_int, ctypes.c_int, ctypes.c_void_p], ctypes.c_int),
+    "vlut_mpgemm_layout": ([ctypes.POINTER(_Desc), ctypes.c_void_p, ctypes.c_void_p,
+                            ctypes.c_float, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                            ctypes.c_int, ctypes.c_int, ctypes.c_void_p], ctypes.c_int),
+    "vlut_quantize_t": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "vlut_linear": ([ctypes.POINTER(_Desc), ctypes.c_void_p, ctypes.c_float, ctypes.c_void_p,
+                     ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                     ctypes.c_void_p], ctypes.c_int),
     "vlut_launches_per_mpgemm": ([], ctypes.c_int),
     "vlut_last_error": ([], ctypes.c_char_p),
     "vlut_version": ([], ctypes.c_char_p),
@@ -333,3 +342,52 @@ def mpgemm_mixed(W: MixedPackedWeights, A, a_scale, w_scale: float, out=None, st
     _check(lib().vlut_mpgemm_mixed(d5, d4, _dev_ptr(A), _dev_ptr(a_scale), float(w_scale),
                                    _dev_ptr(out), W.M, K, N, _stream_ptr(stream)))
     return out
+
+
+# ---------------------------------------------------------------- feature-major layouts (f3)
+OUT_FEATURE_MAJOR = 1
+
+
+def mpgemm_layout(W: PackedWeights, A, a_scale, w_scale: float, out=None, feature_major=True,
+                  stream=None):
+    """vlut_mpgemm with the fused output transposition: out [N][M] if feature_major."""
+    import torch
+    K, N = A.shape
+    M = W.M
+    if out is None:
+        shape = (N, M) if feature_major else (M, N)
+        out = torch.empty(shape, dtype=torch.float32, device=A.device)
+    _check(lib().vlut_mpgemm_layout(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(a_scale),
+                                    float(w_scale), _dev_ptr(out), M, K, N,
+                                    OUT_FEATURE_MAJOR if feature_major else 0,
+                                    _stream_ptr(stream)))
+    return out
+
+
+def quantize_t(x_nk, y_nk=None, q=None, scale=None, stream=None):
+    """Per-token quantizer of feature-major fp32 [N][K] -> (int8 [K][N], fp32 [N])."""
+    import torch
+    N, K = x_nk.shape
+    if q is None:
+        q = torch.empty((K, N), dtype=torch.int8, device=x_nk.device)
+    if scale is None:
+        scale = torch.empty((N,), dtype=torch.float32, device=x_nk.device)
+    _check(lib().vlut_quantize_t(_dev_ptr(x_nk), _dev_ptr(y_nk), K, N, _dev_ptr(q),
+                                 _dev_ptr(scale), _stream_ptr(stream)))
+    return q, scale
+
+
+def linear(W: PackedWeights, x_nk, w_scale: float, y=None, q_ws=None, s_ws=None, stream=None):
+    """Framework-layout ternary linear: x fp32 [N][K] -> y fp32 [N][M]."""
+    import torch
+    N, K = x_nk.shape
+    dev = x_nk.device
+    if y is None:
+        y = torch.empty((N, W.M), dtype=torch.float32, device=dev)
+    if q_ws is None:
+        q_ws = torch.empty((K, N), dtype=torch.int8, device=dev)
+    if s_ws is None:
+        s_ws = torch.empty((N,), dtype=torch.float32, device=dev)
+    _check(lib().vlut_linear(ctypes.byref(W.desc), _dev_ptr(x_nk), float(w_scale), _dev_ptr(y),
+                             W.M, K, N, _dev_ptr(q_ws), _dev_ptr(s_ws), _stream_ptr(stream)))
+    return y

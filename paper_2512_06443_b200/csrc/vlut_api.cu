@@ -295,7 +295,7 @@ vlut_status dispatch(int g, int warps, const vlut::Params& p, int S, int NT, int
 vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,
                        float w_scale, void* out, int M, int K, int N,
                        const vlut_launch_plan* plan_in, void* stream, bool acc_only,
-                       const int32_t* acc_in = nullptr) {
+                       const int32_t* acc_in = nullptr, int out_t = 0) {
   if (M < 0 || K <= 0 || N < 0) return fail(VLUT_ERR_INVALID_ARGUMENT, "bad sizes M=%d K=%d N=%d", M, K, N);
   if (M == 0 || N == 0) return ok();
   vlut_status st = check_desc(W, M, K);
@@ -344,7 +344,8 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
     st = encode_a_map(&p.a_map, A, K, N, W->g);
     if (st != VLUT_OK) return st;
   }
-  p.out_vec4 = (N % 4 == 0 && (((uintptr_t)out) & 15) == 0) ? 1 : 0;
+  p.out_t = out_t;
+  p.out_vec4 = ((out_t ? M : N) % 4 == 0 && (((uintptr_t)out) & 15) == 0) ? 1 : 0;
   const int mcta = 32 * plan.warps;
   const long long NT = (N + vlut::kNcta - 1) / vlut::kNcta;
   const long long MT = (M + mcta - 1) / mcta;
@@ -540,6 +541,62 @@ vlut_status vlut_mpgemm_mixed(const vlut_packed_weights* W5, const vlut_packed_w
   if (st != VLUT_OK) return st;
   return run_mpgemm(W4, A + (size_t)k5 * N, a_scale, w_scale, out, M, k4, N, nullptr, stream,
                     false, reinterpret_cast<const int32_t*>(out));
+}
+
+vlut_status vlut_mpgemm_layout(const vlut_packed_weights* W, const int8_t* A,
+                               const float* a_scale, float w_scale, float* out, int M, int K,
+                               int N, int flags, void* stream) {
+  if (flags & ~VLUT_OUT_FEATURE_MAJOR) return fail(VLUT_ERR_INVALID_ARGUMENT, "unknown flags %d", flags);
+  return run_mpgemm(W, A, a_scale, w_scale, out, M, K, N, nullptr, stream, false, nullptr,
+                    (flags & VLUT_OUT_FEATURE_MAJOR) ? 1 : 0);
+}
+
+vlut_status vlut_quantize_t(const float* x, const float* y, int K, int N, int8_t* q,
+                            float* scale, void* stream) {
+  if (K < 0 || N < 0) return fail(VLUT_ERR_INVALID_ARGUMENT, "bad sizes");
+  if (K == 0 || N == 0) return ok();
+  if (!x || !q || !scale) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long long tok_blocks = (N + vlut::kQtTok - 1) / vlut::kQtTok;
+  if (tok_blocks > 65535) return fail(VLUT_ERR_SHAPE, "N too large");
+  // cluster size along K: >= 2 waves of CTAs when possible, slices <= 2048 rows
+  int CL = 1;
+  while (CL < 8 && (tok_blocks * CL < 296 || (long long)K > (long long)CL * 2048)) CL *= 2;
+  while (CL > 1 && K < 4 * CL) CL /= 2;  // at least one float4 per CTA
+  const int slice_max = (K + CL - 1) / CL + 4;
+  const size_t smem = (size_t)slice_max * vlut::kQtTok;
+  if (smem > 200 * 1024) return fail(VLUT_ERR_SHAPE, "K too large for vlut_quantize_t");
+  static std::once_flag once;
+  static cudaError_t attr = cudaSuccess;
+  std::call_once(once, [] {
+    attr = cudaFuncSetAttribute(vlut::vlut_quantize_t_kernel,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  });
+  VLUT_CUDA_TRY(attr);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)CL, (unsigned)tok_blocks, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  VLUT_CUDA_TRY(cudaLaunchKernelEx(&cfg, vlut::vlut_quantize_t_kernel, x, y, K, N, q, scale));
+  return ok();
+}
+
+vlut_status vlut_linear(const vlut_packed_weights* W, const float* x, float w_scale, float* y,
+                        int M, int K, int N, int8_t* q_ws, float* s_ws, void* stream) {
+  if (!q_ws || !s_ws) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL workspace");
+  vlut_status st = vlut_quantize_t(x, nullptr, K, N, q_ws, s_ws, stream);
+  if (st != VLUT_OK) return st;
+  return vlut_mpgemm_layout(W, q_ws, s_ws, w_scale, y, M, K, N, VLUT_OUT_FEATURE_MAJOR, stream);
 }
 
 vlut_status vlut_quantize(const float* x, const float* y, int K, int N, int8_t* q, float* scale,

@@ -157,6 +157,98 @@ __global__ void __launch_bounds__(kQThreads)
   VLUT_STAMP(7);
 }
 
+// ---------------------------------------------------------------- K3t: fused transposition (f3)
+// Feature-major input (frameworks hold activations [N][K]; the
+// transposition to the token-contiguous [K][N] int8 layout is fused into the
+// quantization pass).  A cluster of CL CTAs owns 16 tokens, CTA `rank` a
+// contiguous K slice.  Phase 1: each warp owns 2 tokens and reduces |x| over
+// its slice with coalesced float4 loads along K; the per-token maxima are
+// combined over the cluster (DSMEM).  Phase 2: the slice is re-read (L2),
+// quantized and transposed through shared memory into 16-byte rows of q.
+constexpr int kQtTok = 16;
+
+__global__ void __launch_bounds__(256)
+    vlut_quantize_t_kernel(const float* __restrict__ x, const float* __restrict__ y, int K, int N,
+                           int8_t* __restrict__ q, float* __restrict__ scale) {
+  extern __shared__ __align__(16) uint8_t qt_smem[];  // [slice][16] int8 codes
+  __shared__ float cta_amax[kQtTok];
+  __shared__ float s_scale[kQtTok];
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CL = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n0 = blockIdx.y * kQtTok;
+  const bool vec = ((K & 3) == 0) && ((((uintptr_t)x) | ((uintptr_t)(y ? y : x))) & 15) == 0;
+  // K split in whole float4s when vectorised
+  const int gran = vec ? 4 : 1;
+  const int units = K / gran;
+  const int k_begin = gran * (int)(((long long)rank * units) / CL);
+  const int k_end = gran * (int)(((long long)(rank + 1) * units) / CL);
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  auto load = [&](int n, int k) -> float {
+    const size_t o = (size_t)n * K + k;
+    return y ? __fmul_rn(__ldg(x + o), __ldg(y + o)) : __ldg(x + o);
+  };
+  // ---- phase 1: per-token |x| max over this CTA's K slice
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int t = 2 * warp + h, n = n0 + t;
+    float m = 0.f;
+    if (n < N) {
+      if (vec) {
+        for (int k = k_begin + 4 * lane; k < k_end; k += 128) {
+          const size_t o = (size_t)n * K + k;
+          float4 a = __ldg(reinterpret_cast<const float4*>(x + o));
+          if (y) {
+            const float4 b = __ldg(reinterpret_cast<const float4*>(y + o));
+            a.x = __fmul_rn(a.x, b.x); a.y = __fmul_rn(a.y, b.y);
+            a.z = __fmul_rn(a.z, b.z); a.w = __fmul_rn(a.w, b.w);
+          }
+          m = fmaxf(fmaxf(m, fabsf(a.x)), fmaxf(fabsf(a.y), fmaxf(fabsf(a.z), fabsf(a.w))));
+        }
+      } else {
+        for (int k = k_begin + lane; k < k_end; k += 32) m = fmaxf(m, fabsf(load(n, k)));
+      }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, d));
+    if (lane == 0) cta_amax[t] = m;
+  }
+  cluster.sync();
+  if (tid < kQtTok) {
+    float a = 0.f;
+    for (int r = 0; r < CL; ++r) a = fmaxf(a, cluster.map_shared_rank(cta_amax, r)[tid]);
+    const float sc = (a == 0.f) ? 1.f : __fdiv_rn(a, 127.f);
+    s_scale[tid] = sc;
+    if (rank == 0 && n0 + tid < N) scale[n0 + tid] = sc;
+  }
+  __syncthreads();
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+  // ---- phase 2: quantize into the shared [slice][16] tile (coalesced reads
+  // along K per token), then 16-byte rows of q[k][n0 .. n0+15]
+  const int slice = k_end - k_begin;
+  for (int e = tid; e < slice * kQtTok; e += blockDim.x) {
+    const int t = e / slice, kk = e - t * slice;
+    const int n = n0 + t;
+    int8_t c = 0;
+    if (n < N) c = q_code(load(n, k_begin + kk), s_scale[t]);
+    qt_smem[kk * kQtTok + t] = (uint8_t)c;
+  }
+  __syncthreads();
+  const bool full16 = (n0 + kQtTok <= N) && ((N & 15) == 0) && ((((uintptr_t)q) & 15) == 0);
+  for (int kk = tid; kk < slice; kk += blockDim.x) {
+    int8_t* dst = q + (size_t)(k_begin + kk) * N + n0;
+    if (full16) {
+      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(qt_smem + kk * kQtTok);
+    } else {
+      for (int t = 0; t < kQtTok && n0 + t < N; ++t) dst[t] = (int8_t)qt_smem[kk * kQtTok + t];
+    }
+  }
+  asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+}
+
 // ---------------------------------------------------------------- device packer (a1)
 // One thread per payload byte [kt][m][j]: index = sum_r (w_r + 1) 3^r of
 // group kt*16 + j of row m; padding -> the zero index.

@@ -270,6 +270,7 @@ struct alignas(64) Params {
   int splits;              // cluster size along K
   int a_vec;               // 16 (TMA), 4 or 1: activation staging width
   int out_vec4;            // 1 if out rows allow aligned 16-byte stores
+  int out_t;               // 1: out is [N][M] (feature-major, fused output transposition)
 };
 
 // ---------------------------------------------------------------- staging (a2)
@@ -706,7 +707,19 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[h][i] = 0;
     }
-    {
+    if (p.out_t) {
+      // token-major tile T[n][row]: lanes write consecutive rows (bank = lane)
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = (lane + 2 * h + e) & 7;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            sts32(red_s + (uint32_t)(((8 * c + j) * L::MCTA + r) * 4), v[h][8 * e + j] - bias_total);
+        }
+      }
+    } else {
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
 #pragma unroll
@@ -742,16 +755,21 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
     const int r_begin = rank * rows_per;
     const int units = rows_per * 16;
     const int4* red_local = reinterpret_cast<const int4*>(smem);
+    // unit e -> int4 offset in the tile:
+    //   [M][N] out: row r_begin + e/16, tokens 4(e%16)..+3 (XOR-swizzled row)
+    //   [N][M] out: token e / (rows_per/4), rows r_begin + 4(e % (rows_per/4))..+3
+    const int rq = rows_per >> 2;
+    auto tile_off = [&](int e) -> int {
+      if (p.out_t) return ((e / rq) * L::MCTA + r_begin) / 4 + (e % rq);
+      const int r = r_begin + (e >> 4);
+      return r * 16 + ((e & 15) ^ ((r >> 2) & 1));
+    };
     int4 acc4[L::EPI_UNITS];
 #pragma unroll
     for (int i = 0; i < L::EPI_UNITS; ++i) {
       const int e = tid + i * L::THREADS;
       acc4[i] = make_int4(0, 0, 0, 0);
-      if (e < units) {
-        const int r = r_begin + (e >> 4);
-        const int off = r * 16 + ((e & 15) ^ ((r >> 2) & 1));  // in int4 units
-        acc4[i] = red_local[off];
-      }
+      if (e < units) acc4[i] = red_local[tile_off(e)];
     }
     {
       for (int q = 1; q < S; ++q) {
@@ -761,10 +779,7 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
         for (int i = 0; i < L::EPI_UNITS; ++i) {
           const int e = tid + i * L::THREADS;
           w4[i] = make_int4(0, 0, 0, 0);
-          if (e < units) {
-            const int r = r_begin + (e >> 4);
-            w4[i] = rem[r * 16 + ((e & 15) ^ ((r >> 2) & 1))];
-          }
+          if (e < units) w4[i] = rem[tile_off(e)];
         }
 #pragma unroll
         for (int i = 0; i < L::EPI_UNITS; ++i) {
@@ -776,6 +791,33 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
       if (S > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     }
     VLUT_STAMP(6);
+    if (p.out_t) {
+      // fused output transposition: out[n][m .. m+3], one token scale
+#pragma unroll
+      for (int i = 0; i < L::EPI_UNITS; ++i) {
+        const int e = tid + i * L::THREADS;
+        if (e >= units) continue;
+        const int nl = e / rq;
+        const int n = n0 + nl;
+        const int m = m0 + r_begin + 4 * (e % rq);
+        if (n >= p.N || m >= p.M) continue;
+        const int4 vv4 = acc4[i];
+        const int vv[4] = {vv4.x, vv4.y, vv4.z, vv4.w};
+        if constexpr (ACC_ONLY) {
+          int32_t* o = reinterpret_cast<int32_t*>(p.out) + (size_t)n * p.M + m;
+          if (p.out_vec4 && m + 3 < p.M) *reinterpret_cast<int4*>(o) = vv4;
+          else for (int k = 0; k < 4 && m + k < p.M; ++k) o[k] = vv[k];
+        } else {
+          float* o = p.out + (size_t)n * p.M + m;
+          const float sc = scale_s[nl];
+          float f[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) f[k] = __fmul_rn((float)vv[k], sc);
+          if (p.out_vec4 && m + 3 < p.M) *reinterpret_cast<float4*>(o) = make_float4(f[0], f[1], f[2], f[3]);
+          else for (int k = 0; k < 4 && m + k < p.M; ++k) o[k] = f[k];
+        }
+      }
+    } else
 #pragma unroll
     for (int i = 0; i < L::EPI_UNITS; ++i) {
       const int e = tid + i * L::THREADS;

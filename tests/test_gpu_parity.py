@@ -267,3 +267,34 @@ def test_mpgemm_mixed_matches_oracle(v, M, K, N):
     assert bpw == pytest.approx(oracle.mixed_bits_per_weight(K))
     if K >= 100:
         assert bpw < 1.61
+
+
+# ------------------------------------------------------------------ fused transpositions (f3)
+@pytest.mark.parametrize("K,N", [(2560, 256), (6912, 40), (17, 3), (4096, 1000), (14336, 64)])
+def test_quantize_t_feature_major_input(v, K, N):
+    x = synth.rng(K + N).standard_normal((N, K), dtype=np.float32)  # framework layout [N][K]
+    if N > 2:
+        x[1] = 0.0
+    q, s = v.quantize_t(to_dev(x))
+    qr, sr = oracle.quantize(np.ascontiguousarray(x.T))
+    assert np.array_equal(s.cpu().numpy().view(np.int32), sr.view(np.int32))
+    assert np.array_equal(q.cpu().numpy(), qr)
+    y = synth.rng(K).standard_normal((N, K), dtype=np.float32)
+    q2, s2 = v.quantize_t(to_dev(x), to_dev(y))
+    qr2, sr2 = oracle.quantize(np.ascontiguousarray((x * y).astype(np.float32).T))
+    assert np.array_equal(s2.cpu().numpy(), sr2) and np.array_equal(q2.cpu().numpy(), qr2)
+
+
+@pytest.mark.parametrize("M,K,N", [(6912, 2560, 256), (385, 1024, 130), (100, 512, 9)])
+def test_mpgemm_feature_major_output_and_linear(v, M, K, N):
+    W = synth.ternary_weights(M, K, seed=M + 1)
+    x_nk = synth.rng(N).standard_normal((N, K), dtype=np.float32)
+    pw = v.pack_weights(W, 4, device=dev())
+    qr, sr = oracle.quantize(np.ascontiguousarray(x_nk.T))
+    ref32 = oracle.dequant_f32(oracle.gemm_i32(W, qr), sr, synth.W_SCALE)  # [M][N]
+    out_t = v.mpgemm_layout(pw, to_dev(qr), to_dev(sr), synth.W_SCALE, feature_major=True)
+    y = v.linear(pw, to_dev(x_nk), synth.W_SCALE)
+    torch.cuda.synchronize()
+    assert out_t.shape == (N, M) and y.shape == (N, M)
+    assert np.array_equal(out_t.cpu().numpy().view(np.int32), np.ascontiguousarray(ref32.T).view(np.int32))
+    assert np.array_equal(y.cpu().numpy().view(np.int32), np.ascontiguousarray(ref32.T).view(np.int32))
