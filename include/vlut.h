@@ -91,7 +91,7 @@ typedef struct {
  */
 typedef struct {
   int32_t warps;        /* 8, 12 or 16                                      */
-  int32_t splits;       /* 1..8 with (32*warps) % splits == 0 (cluster size along K) */
+  int32_t splits;       /* 1..8 (cluster size along K)                        */
   int32_t m_cta;        /* 32 * warps                                       */
   int32_t n_cta;        /* 64                                               */
   int32_t grid_ctas;    /* total CTAs launched                              */
@@ -132,6 +132,11 @@ vlut_status vlut_pack_weights_device(const int8_t* w_trits_dev, int M, int K, in
  * S:164).  Padding bytes are not inspected. */
 vlut_status vlut_unpack_weights_host(const vlut_packed_weights* desc,
                                      const uint8_t* payload_host, int8_t* w_trits_host);
+
+/* Planner input: co-resident thread-block clusters of `splits` K1 CTAs of
+ * the (g, warps) variant on the current device (cudaOccupancyMaxActiveClusters);
+ * -1 if that cluster size cannot run, 0 on bad arguments. */
+int vlut_active_clusters(int g, int warps, int splits);
 
 /* The heuristic launch plan for (M, K, N, g) on the current device. */
 vlut_status vlut_plan(int M, int K, int N, int g, vlut_launch_plan* plan);

@@ -102,6 +102,7 @@ EXPORTS = {
                      ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                      ctypes.c_void_p], ctypes.c_int),
     "vlut_launches_per_mpgemm": ([], ctypes.c_int),
+    "vlut_active_clusters": ([ctypes.c_int, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "vlut_last_error": ([], ctypes.c_char_p),
     "vlut_version": ([], ctypes.c_char_p),
 }

@@ -203,7 +203,7 @@ int active_clusters_for(int g, int warps, int S) {
   return active_clusters<5, 16>(S);
 }
 
-inline bool valid_split(int warps, int S) { return S >= 1 && S <= 8 && (32 * warps) % S == 0; }
+inline bool valid_split(int warps, int S) { return warps > 0 && S >= 1 && S <= 8; }
 
 // Cost model in shared-memory cycles (DESIGN.md §4 planner):
 //   per K-tile   16 groups x (m_cta lookup rows + (3^g+1)/2 half-table rows)
@@ -218,12 +218,12 @@ void plan_for(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
   const int half_rows = (pow3i(g) + 1) / 2;
   double best_cost = 1e300;
   const int warps_opts[3] = {16, 12, 8};
-  const int split_opts[6] = {1, 2, 3, 4, 6, 8};
+  const int split_opts[8] = {1, 2, 3, 4, 5, 6, 7, 8};
   for (int wi = 0; wi < 3; ++wi) {
     const int warps = warps_opts[wi];
     const int mcta = 32 * warps;
     const long long MT = (M + mcta - 1) / mcta;
-    for (int si = 0; si < 6; ++si) {
+    for (int si = 0; si < 8; ++si) {
       const int S = split_opts[si];
       if (!valid_split(warps, S) || S > kgt) continue;
       const long long ctas = MT * NT * S;
@@ -373,6 +373,12 @@ int vlut_debug_set_timing(void* dev_buf) {
 const char* vlut_version(void) { return "vlut-b200 0.1 (sm_100a)"; }
 
 int vlut_launches_per_mpgemm(void) { return 1; }
+
+int vlut_active_clusters(int g, int warps, int splits) {
+  if (!valid_g(g) || !(warps == 8 || warps == 12 || warps == 16) || !valid_split(warps, splits))
+    return 0;
+  return active_clusters_for(g, warps, splits);
+}
 
 size_t vlut_packed_bytes(int M, int K, int g) {
   int mp = 0, kgt = 0;

@@ -686,7 +686,9 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
   // ---- int32 tile -> shared (a5).  Row r (lookup thread), 16-byte unit u
   // of the 256-byte row stored at u ^ ((r >> 2) & 1): conflict-free for both
   // the lane-per-row writes below and the row-contiguous reads after.
-  const int rows_per = L::MCTA / S;
+  // epilogue rows of each cluster rank: rows_per (a multiple of 4), the last
+  // rank(s) may own fewer
+  const int rows_per = ((L::MCTA + S - 1) / S + 3) & ~3;
   tmem_fence_before();
   __syncthreads();  // every table read done before the region is reused
   tmem_fence_after();
@@ -752,13 +754,14 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
   // ---- reduce across the cluster + epilogue (a5, a6): all loads of a
   // thread's units first (latency overlapped), then convert + store
   {
-    const int r_begin = rank * rows_per;
-    const int units = rows_per * 16;
+    const int r_begin = min(L::MCTA, rank * rows_per);
+    const int my_rows = min(rows_per, L::MCTA - r_begin);
+    const int units = my_rows * 16;
     const int4* red_local = reinterpret_cast<const int4*>(smem);
     // unit e -> int4 offset in the tile:
     //   [M][N] out: row r_begin + e/16, tokens 4(e%16)..+3 (XOR-swizzled row)
-    //   [N][M] out: token e / (rows_per/4), rows r_begin + 4(e % (rows_per/4))..+3
-    const int rq = rows_per >> 2;
+    //   [N][M] out: token e / (my_rows/4), rows r_begin + 4(e % (my_rows/4))..+3
+    const int rq = max(1, my_rows >> 2);
     auto tile_off = [&](int e) -> int {
       if (p.out_t) return ((e / rq) * L::MCTA + r_begin) / 4 + (e % rq);
       const int r = r_begin + (e >> 4);

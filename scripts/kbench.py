@@ -55,9 +55,7 @@ def main():
         rows.append(time_one(lin.M, lin.K, 1024, 4))
     if a.plans:
         for w in (8, 12, 16):
-            for sp in (1, 2, 3, 4, 6, 8):
-                if (32 * w) % sp:
-                    continue
+            for sp in (1, 2, 3, 4, 5, 6, 7, 8):
                 rows.append(time_one(6912, 2560, 256, 4, plan=v.LaunchPlan(w, sp)))
     for r in rows:
         print(f"M={r['M']:6d} K={r['K']:6d} N={r['N']:5d} g={r['g']} plan={r['plan'][:48]:48s} "
