@@ -96,6 +96,7 @@ typedef struct {
   int32_t n_cta;        /* 64                                               */
   int32_t grid_ctas;    /* total CTAs launched                              */
   int32_t smem_bytes;   /* dynamic shared memory per CTA                    */
+  int32_t streamk;      /* 1: stream-K persistent schedule (needs a workspace) */
 } vlut_launch_plan;
 
 /* Payload bytes for an M x K ternary matrix packed with group size g
@@ -166,6 +167,28 @@ vlut_status vlut_mpgemm_ex(const vlut_packed_weights* W, const int8_t* A,
                            const float* a_scale, float w_scale, float* out,
                            int M, int K, int N, const vlut_launch_plan* plan,
                            void* stream);
+
+/*
+ * Stream-K persistent schedule (one CTA per SM; every SM gets the same number
+ * of K-tile work units whatever the tile count; split tiles are combined
+ * through int32 partials in a caller-provided workspace).  Same results as
+ * vlut_mpgemm.  The planner picks stream-K or the cluster split-K schedule by
+ * its cost model (plan == NULL) unless plan->streamk forces it.
+ *   workspace : device, >= vlut_workspace_bytes() bytes, 16-B aligned, ZEROED
+ *               ONCE before its first use (flags are per-launch epochs), and
+ *               used by one stream at a time.
+ * vlut_workspace_bytes() returns 0 without a CUDA device.
+ */
+size_t vlut_workspace_bytes(void);
+vlut_status vlut_mpgemm_ws(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,
+                           float w_scale, float* out, int M, int K, int N,
+                           const vlut_launch_plan* plan, void* workspace, size_t ws_bytes,
+                           void* stream);
+vlut_status vlut_mpgemm_acc_ws(const vlut_packed_weights* W, const int8_t* A, int32_t* acc_out,
+                               int M, int K, int N, const vlut_launch_plan* plan,
+                               void* workspace, size_t ws_bytes, void* stream);
+/* The plan vlut_mpgemm_ws would choose (stream-K or cluster split-K). */
+vlut_status vlut_plan_ws(int M, int K, int N, int g, vlut_launch_plan* plan);
 
 /* Raw int32 accumulators, no scales (bit-exact test hook):
  *   acc_out : device int32 [M][N].  Other arguments as vlut_mpgemm_ex. */

@@ -25,7 +25,7 @@ __all__ = [
     "pack_weights", "pack_weights_device", "unpack_weights_host", "plan", "mpgemm",
     "mpgemm_ex", "mpgemm_acc", "quantize", "last_error", "EXPORTS", "group_schedule",
     "MixedPackedWeights", "pack_weights_mixed", "mpgemm_mixed", "mpgemm_layout", "quantize_t",
-    "linear",
+    "linear", "workspace", "plan_ws", "mpgemm_ws", "mpgemm_acc_ws",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -61,7 +61,8 @@ class _Desc(ctypes.Structure):
 class _Plan(ctypes.Structure):
     _fields_ = [("warps", ctypes.c_int32), ("splits", ctypes.c_int32),
                 ("m_cta", ctypes.c_int32), ("n_cta", ctypes.c_int32),
-                ("grid_ctas", ctypes.c_int32), ("smem_bytes", ctypes.c_int32)]
+                ("grid_ctas", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
+                ("streamk", ctypes.c_int32)]
 
 
 # Every symbol include/vlut.h declares (tests check the .so exports them all).
@@ -101,6 +102,16 @@ EXPORTS = {
     "vlut_linear": ([ctypes.POINTER(_Desc), ctypes.c_void_p, ctypes.c_float, ctypes.c_void_p,
                      ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                      ctypes.c_void_p], ctypes.c_int),
+    "vlut_workspace_bytes": ([], ctypes.c_size_t),
+    "vlut_mpgemm_ws": ([ctypes.POINTER(_Desc), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_float,
+                        ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                        ctypes.POINTER(_Plan), ctypes.c_void_p, ctypes.c_size_t,
+                        ctypes.c_void_p], ctypes.c_int),
+    "vlut_mpgemm_acc_ws": ([ctypes.POINTER(_Desc), ctypes.c_void_p, ctypes.c_void_p,
+                            ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_Plan),
+                            ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p], ctypes.c_int),
+    "vlut_plan_ws": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                      ctypes.POINTER(_Plan)], ctypes.c_int),
     "vlut_launches_per_mpgemm": ([], ctypes.c_int),
     "vlut_active_clusters": ([ctypes.c_int, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "vlut_last_error": ([], ctypes.c_char_p),
@@ -156,15 +167,16 @@ def _dev_ptr(t) -> ctypes.c_void_p:
 @dataclass
 class LaunchPlan:
     warps: int
-    splits: int
+    splits: int = 1
     m_cta: int = 0
     n_cta: int = 64
     grid_ctas: int = 0
     smem_bytes: int = 0
+    streamk: int = 0
 
     def _c(self) -> _Plan:
         return _Plan(self.warps, self.splits, self.m_cta, self.n_cta, self.grid_ctas,
-                     self.smem_bytes)
+                     self.smem_bytes, self.streamk)
 
 
 class PackedWeights:
@@ -239,7 +251,7 @@ def unpack_weights_host(pw: PackedWeights) -> np.ndarray:
 def plan(M: int, K: int, N: int, g: int) -> LaunchPlan:
     p = _Plan()
     _check(lib().vlut_plan(M, K, N, g, ctypes.byref(p)))
-    return LaunchPlan(p.warps, p.splits, p.m_cta, p.n_cta, p.grid_ctas, p.smem_bytes)
+    return LaunchPlan(p.warps, p.splits, p.m_cta, p.n_cta, p.grid_ctas, p.smem_bytes, p.streamk)
 
 
 def _plan_ptr(p: Optional[LaunchPlan]):
@@ -392,3 +404,62 @@ def linear(W: PackedWeights, x_nk, w_scale: float, y=None, q_ws=None, s_ws=None,
     _check(lib().vlut_linear(ctypes.byref(W.desc), _dev_ptr(x_nk), float(w_scale), _dev_ptr(y),
                              W.M, K, N, _dev_ptr(q_ws), _dev_ptr(s_ws), _stream_ptr(stream)))
     return y
+
+
+# ---------------------------------------------------------------- stream-K workspace
+_WS = {}
+
+
+def workspace(device=None):
+    """The per-device stream-K workspace (zeroed once; one stream at a time)."""
+    import torch
+    dev = torch.device(device or "cuda")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    ws = _WS.get(dev.index)
+    if ws is None:
+        with torch.cuda.device(dev):
+            nb = int(lib().vlut_workspace_bytes())
+        if nb == 0:
+            raise VlutError(7, "no CUDA device for the stream-K workspace")
+        ws = torch.zeros(nb, dtype=torch.uint8, device=dev)
+        _WS[dev.index] = ws
+    return ws
+
+
+def plan_ws(M: int, K: int, N: int, g: int) -> LaunchPlan:
+    p = _Plan()
+    _check(lib().vlut_plan_ws(M, K, N, g, ctypes.byref(p)))
+    return LaunchPlan(p.warps, p.splits, p.m_cta, p.n_cta, p.grid_ctas, p.smem_bytes, p.streamk)
+
+
+def mpgemm_ws(W: PackedWeights, A, a_scale, w_scale: float, out=None,
+              plan: Optional[LaunchPlan] = None, ws=None, stream=None):
+    """vlut_mpgemm with a workspace: the planner may pick the stream-K schedule."""
+    import torch
+    K, N = A.shape
+    M = W.M
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    if ws is None:
+        ws = workspace(A.device)
+    keep, pp = _plan_ptr(plan)
+    _check(lib().vlut_mpgemm_ws(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(a_scale),
+                                float(w_scale), _dev_ptr(out), M, K, N, pp, _dev_ptr(ws),
+                                ws.numel(), _stream_ptr(stream)))
+    return out
+
+
+def mpgemm_acc_ws(W: PackedWeights, A, out=None, plan: Optional[LaunchPlan] = None, ws=None,
+                  stream=None):
+    import torch
+    K, N = A.shape
+    M = W.M
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.int32, device=A.device)
+    if ws is None:
+        ws = workspace(A.device)
+    keep, pp = _plan_ptr(plan)
+    _check(lib().vlut_mpgemm_acc_ws(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(out), M, K, N,
+                                    pp, _dev_ptr(ws), ws.numel(), _stream_ptr(stream)))
+    return out

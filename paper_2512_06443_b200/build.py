@@ -1,6 +1,7 @@
 """Build libvlut.so in-tree with nvcc for sm_100a (no torch JIT cache)."""
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
@@ -9,9 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libvlut.so")
 SOURCES = [os.path.join(HERE, "csrc", "vlut_api.cu")]
-DEPS = SOURCES + [
-    os.path.join(HERE, "csrc", "vlut_kernel.cuh"),
-    os.path.join(HERE, "csrc", "vlut_aux_kernels.cuh"),
+DEPS = SOURCES + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [
     os.path.join(ROOT, "include", "vlut.h"),
 ]
 NVCC_FLAGS = [

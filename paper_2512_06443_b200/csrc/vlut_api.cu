@@ -11,6 +11,8 @@
 #include "../../include/vlut.h"
 #include "vlut_aux_kernels.cuh"
 #include "vlut_kernel.cuh"
+#include "vlut_kernel_sk.cuh"
+#include <atomic>
 
 namespace {
 
@@ -205,13 +207,49 @@ int active_clusters_for(int g, int warps, int S) {
 
 inline bool valid_split(int warps, int S) { return warps > 0 && S >= 1 && S <= 8; }
 
+// Stream-K workspace: int32 partials [sms][512 x 64] + flags.
+size_t sk_workspace_bytes(int sms) { return (size_t)sms * 512 * 64 * 4 + 4096; }
+
+// Best stream-K plan (persistent, grid = #SMs): every CTA gets ceil(U / sms)
+// K-tile units; cost in the same SMEM-cycle units as plan_for.
+double plan_sk(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
+  const int KG = K / g;
+  const int kgt = (KG + VLUT_KG_TILE - 1) / VLUT_KG_TILE;
+  const int NT = (N + vlut::kNcta - 1) / vlut::kNcta;
+  const int half_rows = (pow3i(g) + 1) / 2;
+  double best_cost = 1e300;
+  const int warps_opts[3] = {16, 12, 8};
+  for (int wi = 0; wi < 3; ++wi) {
+    const int warps = warps_opts[wi];
+    const int mcta = 32 * warps;
+    const long long MT = (M + mcta - 1) / mcta;
+    const long long U = MT * NT * kgt;
+    const long long grid = U < sms ? U : sms;
+    const double units = (double)((U + grid - 1) / grid);
+    double cost = units * VLUT_KG_TILE * (double)(mcta + half_rows);
+    cost += 6000.0;                             // start + last epilogue
+    cost += (double)mcta * 256.0 * 3.0 / 64.0;  // partial write + read + output
+    if (cost < best_cost * 0.995) {
+      best_cost = cost;
+      best->warps = warps;
+      best->splits = 1;
+      best->m_cta = mcta;
+      best->n_cta = vlut::kNcta;
+      best->grid_ctas = (int)grid;
+      best->smem_bytes = smem_bytes_for(g, warps);
+      best->streamk = 1;
+    }
+  }
+  return best_cost;
+}
+
 // Cost model in shared-memory cycles (DESIGN.md §4 planner):
 //   per K-tile   16 groups x (m_cta lookup rows + (3^g+1)/2 half-table rows)
 //                (one 128-B wavefront per row and group)
 //   per CTA      tiles x per-tile + fixed start/epilogue + DSMEM reduction of
 //                (S-1)/S of the m_cta x 256 B int32 tile at ~16 B/clk
 //   total        waves x per-CTA, waves = ceil(CTAs / (active clusters x S))
-void plan_for(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
+double plan_for(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
   const int KG = K / g;
   const int kgt = (KG + VLUT_KG_TILE - 1) / VLUT_KG_TILE;
   const int NT = (N + vlut::kNcta - 1) / vlut::kNcta;
@@ -247,9 +285,11 @@ void plan_for(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
         best->n_cta = vlut::kNcta;
         best->grid_ctas = (int)ctas;
         best->smem_bytes = smem_bytes_for(g, warps);
+        best->streamk = 0;
       }
     }
   }
+  return best_cost;
 }
 
 // ------------------------------------------------------------ launches
@@ -277,6 +317,48 @@ vlut_status launch_k1(const vlut::Params& p, int S, int NT, int MT, cudaStream_t
   return VLUT_OK;
 }
 
+template <int G, int WARPS, bool ACC>
+vlut_status launch_sk(const vlut::Params& p, const vlut::SkParams& sk, int grid,
+                      cudaStream_t st) {
+  using L = vlut::Layout<G, WARPS>;
+  auto kern = vlut::vlut_mpgemm_sk_kernel<G, WARPS, ACC>;
+  static std::once_flag flags[64];
+  static cudaError_t errs[64];
+  int dev = 0;
+  VLUT_CUDA_TRY(cudaGetDevice(&dev));
+  std::call_once(flags[dev & 63], [&] {
+    errs[dev & 63] = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+  });
+  VLUT_CUDA_TRY(errs[dev & 63]);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid, 1, 1);
+  cfg.blockDim = dim3(L::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = L::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  VLUT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p, sk));
+  return VLUT_OK;
+}
+
+template <bool ACC>
+vlut_status dispatch_sk(int g, int warps, const vlut::Params& p, const vlut::SkParams& sk,
+                        int grid, cudaStream_t st) {
+  if (g == 4) {
+    if (warps == 8) return launch_sk<4, 8, ACC>(p, sk, grid, st);
+    if (warps == 12) return launch_sk<4, 12, ACC>(p, sk, grid, st);
+    if (warps == 16) return launch_sk<4, 16, ACC>(p, sk, grid, st);
+  } else {
+    if (warps == 8) return launch_sk<5, 8, ACC>(p, sk, grid, st);
+    if (warps == 12) return launch_sk<5, 12, ACC>(p, sk, grid, st);
+    if (warps == 16) return launch_sk<5, 16, ACC>(p, sk, grid, st);
+  }
+  return fail(VLUT_ERR_UNSUPPORTED, "no stream-K variant for g=%d warps=%d", g, warps);
+}
+
 template <bool ACC>
 vlut_status dispatch(int g, int warps, const vlut::Params& p, int S, int NT, int MT,
                      cudaStream_t st) {
@@ -295,7 +377,8 @@ vlut_status dispatch(int g, int warps, const vlut::Params& p, int S, int NT, int
 vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,
                        float w_scale, void* out, int M, int K, int N,
                        const vlut_launch_plan* plan_in, void* stream, bool acc_only,
-                       const int32_t* acc_in = nullptr, int out_t = 0) {
+                       const int32_t* acc_in = nullptr, int out_t = 0, void* ws = nullptr,
+                       size_t ws_bytes = 0) {
   if (M < 0 || K <= 0 || N < 0) return fail(VLUT_ERR_INVALID_ARGUMENT, "bad sizes M=%d K=%d N=%d", M, K, N);
   if (M == 0 || N == 0) return ok();
   vlut_status st = check_desc(W, M, K);
@@ -316,9 +399,20 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
         !valid_split(plan.warps, plan.splits))
       return fail(VLUT_ERR_INVALID_ARGUMENT, "invalid plan warps=%d splits=%d", plan.warps,
                   plan.splits);
+    if (plan.streamk && (!ws || acc_in || out_t))
+      return fail(VLUT_ERR_INVALID_ARGUMENT, "stream-K plan needs a workspace and [M][N] output");
   } else {
-    plan_for(M, K, N, W->g, d.sms, &plan);
+    const double c_cl = plan_for(M, K, N, W->g, d.sms, &plan);
+    if (ws && !acc_in && !out_t) {
+      vlut_launch_plan sk_plan = {};
+      const double c_sk = plan_sk(M, K, N, W->g, d.sms, &sk_plan);
+      if (c_sk < c_cl) plan = sk_plan;
+    }
   }
+  if (plan.streamk && ws_bytes < sk_workspace_bytes(d.sms))
+    return fail(VLUT_ERR_BUFFER_TOO_SMALL, "stream-K workspace needs %zu bytes",
+                sk_workspace_bytes(d.sms));
+  if (plan.streamk && (((uintptr_t)ws) & 15)) return fail(VLUT_ERR_MISALIGNED, "workspace not 16-B aligned");
   if (plan.splits > W->kg_tiles) plan.splits = 1;
   const int smem = smem_bytes_for(W->g, plan.warps);
   if (smem > d.smem_optin)
@@ -351,6 +445,23 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
   const long long MT = (M + mcta - 1) / mcta;
   if (NT > 65535 || MT > 65535) return fail(VLUT_ERR_SHAPE, "grid too large");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (plan.streamk) {
+    static std::atomic<unsigned> epoch{0};
+    vlut::SkParams sk;
+    sk.NT = (int)NT;
+    sk.MT = (int)MT;
+    sk.U = MT * NT * (long long)W->kg_tiles;
+    sk.ws = static_cast<int32_t*>(ws);
+    sk.flags = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + (size_t)d.sms * 512 * 64 * 4);
+    unsigned e = ++epoch;
+    if (e == 0) e = ++epoch;
+    sk.epoch = e;
+    const int grid = (int)(sk.U < d.sms ? sk.U : d.sms);
+    st = acc_only ? dispatch_sk<true>(W->g, plan.warps, p, sk, grid, s)
+                  : dispatch_sk<false>(W->g, plan.warps, p, sk, grid, s);
+    if (st != VLUT_OK) return st;
+    return ok();
+  }
   st = acc_only ? dispatch<true>(W->g, plan.warps, p, plan.splits, (int)NT, (int)MT, s)
                 : dispatch<false>(W->g, plan.warps, p, plan.splits, (int)NT, (int)MT, s);
   if (st != VLUT_OK) return st;
@@ -513,6 +624,41 @@ vlut_status vlut_mpgemm_ex(const vlut_packed_weights* W, const int8_t* A, const 
 vlut_status vlut_mpgemm_acc(const vlut_packed_weights* W, const int8_t* A, int32_t* acc_out,
                             int M, int K, int N, const vlut_launch_plan* plan, void* stream) {
   return run_mpgemm(W, A, nullptr, 0.f, acc_out, M, K, N, plan, stream, true);
+}
+
+size_t vlut_workspace_bytes(void) {
+  DeviceInfo d;
+  if (device_info(&d) != VLUT_OK) return 0;
+  return sk_workspace_bytes(d.sms);
+}
+
+vlut_status vlut_mpgemm_ws(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,
+                           float w_scale, float* out, int M, int K, int N,
+                           const vlut_launch_plan* plan, void* workspace, size_t ws_bytes,
+                           void* stream) {
+  return run_mpgemm(W, A, a_scale, w_scale, out, M, K, N, plan, stream, false, nullptr, 0,
+                    workspace, ws_bytes);
+}
+
+vlut_status vlut_mpgemm_acc_ws(const vlut_packed_weights* W, const int8_t* A, int32_t* acc_out,
+                               int M, int K, int N, const vlut_launch_plan* plan,
+                               void* workspace, size_t ws_bytes, void* stream) {
+  return run_mpgemm(W, A, nullptr, 0.f, acc_out, M, K, N, plan, stream, true, nullptr, 0,
+                    workspace, ws_bytes);
+}
+
+vlut_status vlut_plan_ws(int M, int K, int N, int g, vlut_launch_plan* plan) {
+  if (!plan) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL plan");
+  if (M <= 0 || K <= 0 || N <= 0 || !valid_g(g)) return fail(VLUT_ERR_INVALID_ARGUMENT, "bad sizes");
+  if (K % g) return fail(VLUT_ERR_SHAPE, "g=%d does not divide K=%d", g, K);
+  DeviceInfo d;
+  vlut_status st = device_info(&d);
+  if (st != VLUT_OK) return st;
+  memset(plan, 0, sizeof(*plan));
+  vlut_launch_plan skp = {};
+  const double c_cl = plan_for(M, K, N, g, d.sms, plan);
+  if (plan_sk(M, K, N, g, d.sms, &skp) < c_cl) *plan = skp;
+  return ok();
 }
 
 vlut_status vlut_group_schedule(int K, int* k5, int* k4) {

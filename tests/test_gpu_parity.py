@@ -298,3 +298,36 @@ def test_mpgemm_feature_major_output_and_linear(v, M, K, N):
     assert out_t.shape == (N, M) and y.shape == (N, M)
     assert np.array_equal(out_t.cpu().numpy().view(np.int32), np.ascontiguousarray(ref32.T).view(np.int32))
     assert np.array_equal(y.cpu().numpy().view(np.int32), np.ascontiguousarray(ref32.T).view(np.int32))
+
+
+# ------------------------------------------------------------------ stream-K schedule
+@pytest.mark.parametrize("M,K,N,g", SHAPES + [(6912, 2560, 256, 4), (2560, 2560, 2048, 4)])
+@pytest.mark.parametrize("warps", [8, 12, 16])
+def test_streamk_acc_bit_exact(v, M, K, N, g, warps):
+    W = synth.ternary_weights(M, K, seed=5 * M + K)
+    A = synth.int8_activations(K, N, seed=N + 3)
+    pw = v.pack_weights_device(to_dev(W), g)
+    acc = v.mpgemm_acc_ws(pw, to_dev(A), plan=v.LaunchPlan(warps, 1, streamk=1))
+    torch.cuda.synchronize()
+    if M * N * K > 2e9:  # large case: sampled rows
+        pick = np.unique(synth.rng(1).integers(0, M, size=24))
+        assert np.array_equal(acc.cpu().numpy()[pick], oracle.gemm_i32(W[pick], A))
+    else:
+        assert np.array_equal(acc.cpu().numpy(), oracle.gemm_i32(W, A))
+
+
+@pytest.mark.parametrize("M,K,N,g", [(6912, 2560, 256, 4), (3072, 23040, 1024, 5), (385, 1024, 130, 4)])
+def test_streamk_fp32_and_planner_identity(v, M, K, N, g):
+    W = synth.ternary_weights(M, K, seed=M)
+    x = synth.activations_f32(K, N, seed=N)
+    q, s = oracle.quantize(x)
+    pw = v.pack_weights_device(to_dev(W), g)
+    qd, sd = to_dev(q), to_dev(s)
+    o_sk = v.mpgemm_ws(pw, qd, sd, synth.W_SCALE, plan=v.LaunchPlan(12, 1, streamk=1))
+    o_auto = v.mpgemm_ws(pw, qd, sd, synth.W_SCALE)
+    o_cl = v.mpgemm(pw, qd, sd, synth.W_SCALE)
+    torch.cuda.synchronize()
+    assert torch.equal(o_sk.view(torch.int32), o_cl.view(torch.int32))
+    assert torch.equal(o_auto.view(torch.int32), o_cl.view(torch.int32))
+    pick = np.unique(np.concatenate([[0, M - 1], synth.rng(2).integers(0, M, size=16)]))
+    check_fp32(o_sk.cpu().numpy()[pick], oracle.gemm_i32(W[pick], q), s, synth.W_SCALE)
