@@ -263,11 +263,13 @@ def main():
     out_r = torch.empty((Ms, N), dtype=torch.float32, device=dev)
     out_full = torch.empty((M, N), dtype=torch.float32, device=dev) if world > 1 else out_r
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
-    plan = v.plan(Ms, K, N, g)
+
+    ws = v.workspace(dev)
+    plan = v.plan_ws(Ms, K, N, g)
 
     def step():
         v.quantize(x, q=q, scale=s, stream=stream)
-        v.mpgemm(pw, q, s, synth.W_SCALE, out=out_r, stream=stream)
+        v.mpgemm_ws(pw, q, s, synth.W_SCALE, out=out_r, ws=ws, stream=stream)
         if world > 1:
             dist.all_gather_into_tensor(out_full, out_r)
 
@@ -293,7 +295,7 @@ def main():
             e[0].record(stream)
             v.quantize(x, q=q, scale=s, stream=stream)
             e[1].record(stream)
-            v.mpgemm(pw, q, s, synth.W_SCALE, out=out_r, stream=stream)
+            v.mpgemm_ws(pw, q, s, synth.W_SCALE, out=out_r, ws=ws, stream=stream)
             e[2].record(stream)
             if world > 1:
                 dist.all_gather_into_tensor(out_full, out_r)
@@ -471,15 +473,17 @@ def sweep(v, dev, stream, flush, reps=10):
     R_LU = SM_COUNT * 64 * SM_MAX_MHZ_FALLBACK * 1e6
     res = []
 
+    ws = v.workspace(dev)
+
     def timeit(pw, A, sc, out):
         for _ in range(2):
-            v.mpgemm(pw, A, sc, synth.W_SCALE, out=out, stream=stream)
+            v.mpgemm_ws(pw, A, sc, synth.W_SCALE, out=out, ws=ws, stream=stream)
         ts = []
         for _ in range(reps):
             flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            v.mpgemm(pw, A, sc, synth.W_SCALE, out=out, stream=stream)
+            v.mpgemm_ws(pw, A, sc, synth.W_SCALE, out=out, ws=ws, stream=stream)
             b.record(stream)
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b) * 1e-3)
@@ -496,7 +500,9 @@ def sweep(v, dev, stream, flush, reps=10):
             out = torch.empty((lin.M, N), dtype=torch.float32, device=dev)
             t = timeit(pw, A, sc, out)
             lk = lin.M * (lin.K // g) * N
+            pl = v.plan_ws(lin.M, lin.K, N, g)
             res.append({"config": 4, "M": lin.M, "K": lin.K, "N": N, "g": g, "us": t * 1e6,
+                        "plan": f"warps={pl.warps} splits={pl.splits} streamk={pl.streamk}",
                         "tokens_s": N / t, "gops": 2 * lin.M * lin.K * N / t / 1e9,
                         "frac_smem_roofline": lk / R_LU / t})
         del pw
@@ -524,13 +530,13 @@ def sweep(v, dev, stream, flush, reps=10):
         A, sc = v.quantize(x)
         out = torch.empty((lin.M, 1024), dtype=torch.float32, device=dev)
         for _ in range(2):
-            v.mpgemm_mixed(pm, A, sc, synth.W_SCALE, out=out, stream=stream)
+            v.mpgemm_mixed(pm, A, sc, synth.W_SCALE, out=out, ws=ws, stream=stream)
         ts = []
         for _ in range(reps):
             flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            v.mpgemm_mixed(pm, A, sc, synth.W_SCALE, out=out, stream=stream)
+            v.mpgemm_mixed(pm, A, sc, synth.W_SCALE, out=out, ws=ws, stream=stream)
             b.record(stream)
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b) * 1e-3)

@@ -213,6 +213,11 @@ vlut_status vlut_group_schedule(int K, int* k5, int* k4);
 vlut_status vlut_mpgemm_mixed(const vlut_packed_weights* W5, const vlut_packed_weights* W4,
                               const int8_t* A, const float* a_scale, float w_scale, float* out,
                               int M, int K, int N, void* stream);
+/* Same with a stream-K workspace (see vlut_mpgemm_ws; may be NULL). */
+vlut_status vlut_mpgemm_mixed_ws(const vlut_packed_weights* W5, const vlut_packed_weights* W4,
+                                 const int8_t* A, const float* a_scale, float w_scale,
+                                 float* out, int M, int K, int N, void* ws, size_t ws_bytes,
+                                 void* stream);
 
 /*
  * Fused feature-major transpositions: frameworks hold activations

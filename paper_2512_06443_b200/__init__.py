@@ -112,6 +112,10 @@ EXPORTS = {
                             ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p], ctypes.c_int),
     "vlut_plan_ws": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                       ctypes.POINTER(_Plan)], ctypes.c_int),
+    "vlut_mpgemm_mixed_ws": ([ctypes.POINTER(_Desc), ctypes.POINTER(_Desc), ctypes.c_void_p,
+                              ctypes.c_void_p, ctypes.c_float, ctypes.c_void_p, ctypes.c_int,
+                              ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
+                              ctypes.c_void_p], ctypes.c_int),
     "vlut_launches_per_mpgemm": ([], ctypes.c_int),
     "vlut_active_clusters": ([ctypes.c_int, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "vlut_last_error": ([], ctypes.c_char_p),
@@ -345,15 +349,17 @@ def pack_weights_mixed(w_trits: np.ndarray, device=None, stream=None) -> MixedPa
     return MixedPackedWeights(w5, w4, M, K)
 
 
-def mpgemm_mixed(W: MixedPackedWeights, A, a_scale, w_scale: float, out=None, stream=None):
+def mpgemm_mixed(W: MixedPackedWeights, A, a_scale, w_scale: float, out=None, ws=None,
+                 stream=None):
     import torch
     K, N = A.shape
     if out is None:
         out = torch.empty((W.M, N), dtype=torch.float32, device=A.device)
     d5 = ctypes.byref(W.w5.desc) if W.w5 is not None else ctypes.POINTER(_Desc)()
     d4 = ctypes.byref(W.w4.desc) if W.w4 is not None else ctypes.POINTER(_Desc)()
-    _check(lib().vlut_mpgemm_mixed(d5, d4, _dev_ptr(A), _dev_ptr(a_scale), float(w_scale),
-                                   _dev_ptr(out), W.M, K, N, _stream_ptr(stream)))
+    wsp, wsn = (_dev_ptr(ws), ws.numel()) if ws is not None else (ctypes.c_void_p(0), 0)
+    _check(lib().vlut_mpgemm_mixed_ws(d5, d4, _dev_ptr(A), _dev_ptr(a_scale), float(w_scale),
+                                      _dev_ptr(out), W.M, K, N, wsp, wsn, _stream_ptr(stream)))
     return out
 
 

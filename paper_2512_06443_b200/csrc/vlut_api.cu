@@ -673,9 +673,21 @@ vlut_status vlut_group_schedule(int K, int* k5, int* k4) {
   return fail(VLUT_ERR_SHAPE, "K=%d is not 5b + 4a with a, b >= 0", K);
 }
 
+vlut_status vlut_mpgemm_mixed_ws(const vlut_packed_weights* W5, const vlut_packed_weights* W4,
+                                 const int8_t* A, const float* a_scale, float w_scale,
+                                 float* out, int M, int K, int N, void* ws, size_t ws_bytes,
+                                 void* stream);
+
 vlut_status vlut_mpgemm_mixed(const vlut_packed_weights* W5, const vlut_packed_weights* W4,
                               const int8_t* A, const float* a_scale, float w_scale, float* out,
                               int M, int K, int N, void* stream) {
+  return vlut_mpgemm_mixed_ws(W5, W4, A, a_scale, w_scale, out, M, K, N, nullptr, 0, stream);
+}
+
+vlut_status vlut_mpgemm_mixed_ws(const vlut_packed_weights* W5, const vlut_packed_weights* W4,
+                                 const int8_t* A, const float* a_scale, float w_scale,
+                                 float* out, int M, int K, int N, void* ws, size_t ws_bytes,
+                                 void* stream) {
   int k5 = 0, k4 = 0;
   vlut_status st = vlut_group_schedule(K, &k5, &k4);
   if (st != VLUT_OK) return st;
@@ -685,11 +697,16 @@ vlut_status vlut_mpgemm_mixed(const vlut_packed_weights* W5, const vlut_packed_w
   if (k4 && (!W4 || W4->g != 4 || W4->K != k4))
     return fail(VLUT_ERR_SHAPE, "W4 must hold the last %d features with g=4", k4);
   if (!A) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL A");
-  if (k4 == 0) return run_mpgemm(W5, A, a_scale, w_scale, out, M, k5, N, nullptr, stream, false);
-  if (k5 == 0) return run_mpgemm(W4, A, a_scale, w_scale, out, M, k4, N, nullptr, stream, false);
+  if (k4 == 0)
+    return run_mpgemm(W5, A, a_scale, w_scale, out, M, k5, N, nullptr, stream, false, nullptr, 0,
+                      ws, ws_bytes);
+  if (k5 == 0)
+    return run_mpgemm(W4, A, a_scale, w_scale, out, M, k4, N, nullptr, stream, false, nullptr, 0,
+                      ws, ws_bytes);
   // g=5 groups first: raw int32 partial into `out` (same size), then the g=4
   // groups on the remaining activation rows add it before the fp32 epilogue
-  st = run_mpgemm(W5, A, nullptr, 0.f, out, M, k5, N, nullptr, stream, true);
+  st = run_mpgemm(W5, A, nullptr, 0.f, out, M, k5, N, nullptr, stream, true, nullptr, 0, ws,
+                  ws_bytes);
   if (st != VLUT_OK) return st;
   return run_mpgemm(W4, A + (size_t)k5 * N, a_scale, w_scale, out, M, k4, N, nullptr, stream,
                     false, reinterpret_cast<const int32_t*>(out));

@@ -78,8 +78,9 @@ class RowShardedLinear:
         self._compute = compute or self._cuda_compute
 
     def _cuda_compute(self, shard, A, a_scale, out):
+        # workspace path: the planner may pick the stream-K schedule
         import paper_2512_06443_b200 as v
-        v.mpgemm(shard, A, a_scale, self.w_scale, out=out)
+        v.mpgemm_ws(shard, A, a_scale, self.w_scale, out=out)
 
     def __call__(self, A, a_scale, out=None):
         """A: int8 [K][N] (replicated on every rank), a_scale: fp32 [N] ->
