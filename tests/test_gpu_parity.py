@@ -260,8 +260,10 @@ def test_mpgemm_mixed_matches_oracle(v, M, K, N):
     k5, k4 = v.group_schedule(K)
     assert (pw.w5 is None) == (k5 == 0) and (pw.w4 is None) == (k4 == 0)
     out = v.mpgemm_mixed(pw, to_dev(q), to_dev(s), synth.W_SCALE)
+    out_ws = v.mpgemm_mixed(pw, to_dev(q), to_dev(s), synth.W_SCALE, ws=v.workspace(dev()))
     torch.cuda.synchronize()
     check_fp32(out.cpu().numpy(), oracle.gemm_i32(W, q), s, synth.W_SCALE)
+    assert torch.equal(out.view(torch.int32), out_ws.view(torch.int32))
     # bits per weight of the logical mixed packing (near 1.6 for common shapes)
     bpw = 8.0 * (k5 / 5 + k4 / 4) / K
     assert bpw == pytest.approx(oracle.mixed_bits_per_weight(K))
