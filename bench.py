@@ -453,17 +453,35 @@ def chain_bench(v, dev, world, rank, args, reps=3):
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     t = float(np.median(ts))
+    # f1: fused re-quantization (epilogue maxima, int8 gathers, gate (.) up fused)
+    fchain = LayerChain(layers, fused=True)
+    fchain(xq, xs)
+    torch.cuda.synchronize()
     if world > 1:
-        tt = torch.tensor([t], device=dev)
+        dist.barrier()
+    tf = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fchain(xq, xs)
+        b.record()
+        torch.cuda.synchronize()
+        tf.append(a.elapsed_time(b))
+    t_f = float(np.median(tf))
+    if world > 1:
+        tt = torch.tensor([t, t_f], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t = float(tt[0])
+        t, t_f = float(tt[0]), float(tt[1])
     lookups = L * N * sum(lin.M * lin.K // 4 for lin in cfg.linears)
     R_LU = SM_COUNT * 64 * SM_MAX_MHZ_FALLBACK * 1e6
     return {"config": 5, "layers": L, "N": N, "n_gpus": world, "ms_per_forward": t,
             "tokens_s": N / (t * 1e-3),
             "frac_smem_roofline": lookups / (R_LU * world) / (t * 1e-3),
+            "fused_requant": {"ms_per_forward": t_f, "tokens_s": N / (t_f * 1e-3),
+                              "frac_smem_roofline": lookups / (R_LU * world) / (t_f * 1e-3)},
             "step": "per layer: 5 row-sharded Vec-LUT linears (+ all-gather when n_gpus > 1) "
-                    "and 4 int8 re-quantizations; weights packed once before timing"}
+                    "and 4 int8 re-quantizations; weights packed once before timing; "
+                    "fused_requant = f1 (epilogue maxima, int8 all-gathers)"}
 
 
 def sweep(v, dev, stream, flush, reps=10):

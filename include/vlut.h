@@ -243,6 +243,25 @@ vlut_status vlut_linear(const vlut_packed_weights* W, const float* x, float w_sc
                         int M, int K, int N, int8_t* q_ws, float* s_ws, void* stream);
 
 /*
+ * Fused re-quantization (f1): vlut_mpgemm_ws (ws may be NULL: cluster schedule
+ * only; plan may be NULL: the planner chooses, as in vlut_mpgemm_ws) whose epilogue
+ * optionally multiplies the fp32 output element-wise by mul_in [M][N]
+ * (config 5's gate (.) up glue: out = fl(out * mul_in)) and atomically maxes
+ * |out| of rows m < amax_rows into amax_out[N] (IEEE float bits as unsigned;
+ * the caller zeroes amax_out before the call).  mul_in / amax_out may be NULL.
+ * vlut_quantize_amax then quantizes x [K][N] with those maxima in one pass
+ * (s = amax/127, 1 if 0; q = clamp(roundf(x/s), +-127)) -- the same codes and
+ * scales as vlut_quantize(x).  In the row-sharded path the per-rank maxima
+ * are all-reduced (MAX) before quantizing, and int8 shards are gathered.
+ */
+vlut_status vlut_mpgemm_fused(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,
+                              float w_scale, float* out, int M, int K, int N, const float* mul_in,
+                              unsigned* amax_out, int amax_rows, const vlut_launch_plan* plan,
+                              void* ws, size_t ws_bytes, void* stream);
+vlut_status vlut_quantize_amax(const float* x, const unsigned* amax, int K, int N, int8_t* q,
+                               float* scale, void* stream);
+
+/*
  * Per-token absmax int8 quantizer (a7; w1.6A8 named at P:102; formula
  * S:339-347, reading c8), IEEE single precision throughout:
  *   x'[k][n] = x[k][n] * (y ? y[k][n] : 1)      (fp32 multiply, config 5's

@@ -25,7 +25,8 @@ __all__ = [
     "pack_weights", "pack_weights_device", "unpack_weights_host", "plan", "mpgemm",
     "mpgemm_ex", "mpgemm_acc", "quantize", "last_error", "EXPORTS", "group_schedule",
     "MixedPackedWeights", "pack_weights_mixed", "mpgemm_mixed", "mpgemm_layout", "quantize_t",
-    "linear", "workspace", "plan_ws", "mpgemm_ws", "mpgemm_acc_ws",
+    "linear", "workspace", "plan_ws", "mpgemm_ws", "mpgemm_acc_ws", "mpgemm_fused",
+    "quantize_amax",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -116,6 +117,13 @@ EXPORTS = {
                               ctypes.c_void_p, ctypes.c_float, ctypes.c_void_p, ctypes.c_int,
                               ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
                               ctypes.c_void_p], ctypes.c_int),
+    "vlut_mpgemm_fused": ([ctypes.POINTER(_Desc), ctypes.c_void_p, ctypes.c_void_p,
+                           ctypes.c_float, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                           ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                           ctypes.POINTER(_Plan), ctypes.c_void_p, ctypes.c_size_t,
+                           ctypes.c_void_p], ctypes.c_int),
+    "vlut_quantize_amax": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "vlut_launches_per_mpgemm": ([], ctypes.c_int),
     "vlut_active_clusters": ([ctypes.c_int, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "vlut_last_error": ([], ctypes.c_char_p),
@@ -469,3 +477,37 @@ def mpgemm_acc_ws(W: PackedWeights, A, out=None, plan: Optional[LaunchPlan] = No
     _check(lib().vlut_mpgemm_acc_ws(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(out), M, K, N,
                                     pp, _dev_ptr(ws), ws.numel(), _stream_ptr(stream)))
     return out
+
+
+# ---------------------------------------------------------------- fused re-quantization (f1)
+def mpgemm_fused(W: PackedWeights, A, a_scale, w_scale: float, out=None, mul_in=None,
+                 amax=None, amax_rows: Optional[int] = None,
+                 plan: Optional[LaunchPlan] = None, ws=None, stream=None):
+    """mpGeMM whose epilogue multiplies by mul_in ([M][N] fp32, optional) and
+    atomically maxes |out| over rows < amax_rows into amax (int32 [N] viewed
+    as float bits; zero it first).  Returns out."""
+    import torch
+    K, N = A.shape
+    M = W.M
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    rows = M if amax_rows is None else amax_rows
+    wsp, wsn = (_dev_ptr(ws), ws.numel()) if ws is not None else (ctypes.c_void_p(0), 0)
+    keep, pp = _plan_ptr(plan)
+    _check(lib().vlut_mpgemm_fused(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(a_scale),
+                                   float(w_scale), _dev_ptr(out), M, K, N, _dev_ptr(mul_in),
+                                   _dev_ptr(amax), int(rows), pp, wsp, wsn, _stream_ptr(stream)))
+    return out
+
+
+def quantize_amax(x, amax, q=None, scale=None, stream=None):
+    """Quantize fp32 [K][N] with per-token maxima already known (f1)."""
+    import torch
+    K, N = x.shape
+    if q is None:
+        q = torch.empty((K, N), dtype=torch.int8, device=x.device)
+    if scale is None:
+        scale = torch.empty((N,), dtype=torch.float32, device=x.device)
+    _check(lib().vlut_quantize_amax(_dev_ptr(x), _dev_ptr(amax), K, N, _dev_ptr(q),
+                                    _dev_ptr(scale), _stream_ptr(stream)))
+    return q, scale

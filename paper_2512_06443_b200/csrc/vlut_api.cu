@@ -378,7 +378,8 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
                        float w_scale, void* out, int M, int K, int N,
                        const vlut_launch_plan* plan_in, void* stream, bool acc_only,
                        const int32_t* acc_in = nullptr, int out_t = 0, void* ws = nullptr,
-                       size_t ws_bytes = 0) {
+                       size_t ws_bytes = 0, const float* mul_in = nullptr,
+                       unsigned* amax_out = nullptr, int amax_rows = 0) {
   if (M < 0 || K <= 0 || N < 0) return fail(VLUT_ERR_INVALID_ARGUMENT, "bad sizes M=%d K=%d N=%d", M, K, N);
   if (M == 0 || N == 0) return ok();
   vlut_status st = check_desc(W, M, K);
@@ -439,6 +440,9 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
     if (st != VLUT_OK) return st;
   }
   p.out_t = out_t;
+  p.mul_in = mul_in;
+  p.amax_out = amax_out;
+  p.amax_rows = amax_rows;
   p.out_vec4 = ((out_t ? M : N) % 4 == 0 && (((uintptr_t)out) & 15) == 0) ? 1 : 0;
   const int mcta = 32 * plan.warps;
   const long long NT = (N + vlut::kNcta - 1) / vlut::kNcta;
@@ -658,6 +662,40 @@ vlut_status vlut_plan_ws(int M, int K, int N, int g, vlut_launch_plan* plan) {
   vlut_launch_plan skp = {};
   const double c_cl = plan_for(M, K, N, g, d.sms, plan);
   if (plan_sk(M, K, N, g, d.sms, &skp) < c_cl) *plan = skp;
+  return ok();
+}
+
+vlut_status vlut_mpgemm_fused(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,
+                              float w_scale, float* out, int M, int K, int N, const float* mul_in,
+                              unsigned* amax_out, int amax_rows, const vlut_launch_plan* plan,
+                              void* ws, size_t ws_bytes, void* stream) {
+  if ((mul_in && (((uintptr_t)mul_in) & 3)) || (amax_out && (((uintptr_t)amax_out) & 3)))
+    return fail(VLUT_ERR_MISALIGNED, "mul_in / amax_out not 4-B aligned");
+  return run_mpgemm(W, A, a_scale, w_scale, out, M, K, N, plan, stream, false, nullptr, 0,
+                    ws, ws_bytes, mul_in, amax_out, amax_rows < 0 ? 0 : amax_rows);
+}
+
+vlut_status vlut_quantize_amax(const float* x, const unsigned* amax, int K, int N, int8_t* q,
+                               float* scale, void* stream) {
+  if (K < 0 || N < 0) return fail(VLUT_ERR_INVALID_ARGUMENT, "bad sizes");
+  if (K == 0 || N == 0) return ok();
+  if (!x || !amax || !q || !scale) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
+  DeviceInfo d;
+  vlut_status st = device_info(&d);
+  if (st != VLUT_OK) return st;
+  const long long total = (long long)K * ((N + 3) / 4);
+  long long blocks = (total + 255) / 256;
+  if (blocks > (long long)d.sms * 8) blocks = (long long)d.sms * 8;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)blocks, 1, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  VLUT_CUDA_TRY(cudaLaunchKernelEx(&cfg, vlut::vlut_quantize_amax_kernel, x, amax, K, N, q, scale));
   return ok();
 }
 

@@ -249,6 +249,44 @@ __global__ void __launch_bounds__(256)
   asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
 }
 
+// ---------------------------------------------------------------- K3a: quantize with known amax (f1)
+// The per-token |x| maxima were produced by the producing GEMM's epilogue
+// (vlut_mpgemm_fused), so quantization is one elementwise pass:
+// s_n = amax_n / 127 (1 if 0), q = clamp(roundf(x / s_n), +-127).  4 tokens
+// per thread (float4 in, 4 codes out), grid-stride.
+__global__ void __launch_bounds__(256)
+    vlut_quantize_amax_kernel(const float* __restrict__ x, const unsigned* __restrict__ amax,
+                              int K, int N, int8_t* __restrict__ q, float* __restrict__ scale) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  const int n4 = (N + 3) / 4;
+  const long long total = (long long)K * n4;
+  const bool vec = ((N & 3) == 0) && ((((uintptr_t)x) & 15) == 0) && ((((uintptr_t)q) & 3) == 0);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(e / n4), n = 4 * (int)(e % n4);
+    float s[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float a = (n + i < N) ? __uint_as_float(__ldg(amax + n + i)) : 0.f;
+      s[i] = (a == 0.f) ? 1.f : __fdiv_rn(a, 127.f);
+    }
+    if (k == 0)
+      for (int i = 0; i < 4 && n + i < N; ++i) scale[n + i] = s[i];
+    const size_t o = (size_t)k * N + n;
+    if (vec) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(x + o));
+      const uint32_t packed = (uint32_t)(uint8_t)q_code(v.x, s[0]) |
+                              ((uint32_t)(uint8_t)q_code(v.y, s[1]) << 8) |
+                              ((uint32_t)(uint8_t)q_code(v.z, s[2]) << 16) |
+                              ((uint32_t)(uint8_t)q_code(v.w, s[3]) << 24);
+      *reinterpret_cast<uint32_t*>(q + o) = packed;
+    } else {
+      for (int i = 0; i < 4 && n + i < N; ++i) q[o + i] = q_code(__ldg(x + o + i), s[i]);
+    }
+  }
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
 // ---------------------------------------------------------------- device packer (a1)
 // One thread per payload byte [kt][m][j]: index = sum_r (w_r + 1) 3^r of
 // group kt*16 + j of row m; padding -> the zero index.

@@ -89,7 +89,8 @@ struct Layout {
   static constexpr int MISC_OFF = A_OFF + kStageBufs * Cfg<G>::A_BYTES;  // tmem address
   static constexpr int MBAR_OFF = MISC_OFF + 16;  // FULL[2], EMPTY[2], STAGE[3] (8 B each)
   static constexpr int SCALE_OFF = MBAR_OFF + 64;  // fl(a_scale[n] * w_scale), 64 floats
-  static constexpr int SMEM = SCALE_OFF + kNcta * 4;
+  static constexpr int AMAX_OFF = SCALE_OFF + kNcta * 4;  // per-token |out| max of the CTA
+  static constexpr int SMEM = AMAX_OFF + kNcta * 4;
   // epilogue: 16-byte output units per thread (upper bound, splits = 1)
   static constexpr int EPI_UNITS = (MCTA * 16 + THREADS - 1) / THREADS;
   static_assert(WARPS <= 16, "TMEM columns: at most 4 column blocks of 64");
@@ -271,6 +272,9 @@ struct alignas(64) Params {
   int a_vec;               // 16 (TMA), 4 or 1: activation staging width
   int out_vec4;            // 1 if out rows allow aligned 16-byte stores
   int out_t;               // 1: out is [N][M] (feature-major, fused output transposition)
+  const float* mul_in;     // optional fp32 [M][N]: out = fl(out * mul_in) (gate (.) up glue)
+  unsigned* amax_out;      // optional [N]: atomicMax of |out| (float bits) over rows < amax_rows
+  int amax_rows;
 };
 
 // ---------------------------------------------------------------- staging (a2)
@@ -794,6 +798,7 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
       if (S > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     }
     VLUT_STAMP(6);
+    float tok_max[4] = {0.f, 0.f, 0.f, 0.f};
     if (p.out_t) {
       // fused output transposition: out[n][m .. m+3], one token scale
 #pragma unroll
@@ -825,7 +830,7 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
     for (int i = 0; i < L::EPI_UNITS; ++i) {
       const int e = tid + i * L::THREADS;
       if (e >= units) continue;
-      const int u = e & 15;
+      const int u = e & 15;  // == tid & 15 (THREADS is a multiple of 16)
       const int m = m0 + r_begin + (e >> 4);
       const int n = n0 + 4 * u;
       if (m >= p.M || n >= p.N) continue;
@@ -855,11 +860,40 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
         float f[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) f[k] = __fmul_rn((float)vv[k], scale_s[4 * u + k]);
+        if (p.mul_in) {  // fused element-wise product (config 5: h = gate (.) up)
+          const float* mi = p.mul_in + (size_t)m * p.N + n;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (n + k < p.N) f[k] = __fmul_rn(f[k], __ldg(mi + k));
+        }
+        if (p.amax_out && m < p.amax_rows) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (n + k < p.N) tok_max[k] = fmaxf(tok_max[k], fabsf(f[k]));
+        }
         if (p.out_vec4 && n + 3 < p.N) {
           *reinterpret_cast<float4*>(o) = make_float4(f[0], f[1], f[2], f[3]);
         } else {
           for (int k = 0; k < 4 && n + k < p.N; ++k) o[k] = f[k];
         }
+      }
+    }
+    if constexpr (!ACC_ONLY) {
+      if (p.amax_out) {
+        // fused re-quantization (f1): per-token |out| max of this CTA ->
+        // global atomicMax on the float bits (non-negative floats order as
+        // unsigned integers).  Thread's token quad: 4 (tid & 15) .. +3.
+        unsigned* cta_max = reinterpret_cast<unsigned*>(smem + L::AMAX_OFF);
+        if (tid < kNcta) cta_max[tid] = 0u;
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          tok_max[k] = fmaxf(tok_max[k], __shfl_xor_sync(0xffffffffu, tok_max[k], 16));
+          if (lane < 16) atomicMax(cta_max + 4 * (tid & 15) + k, __float_as_uint(tok_max[k]));
+        }
+        __syncthreads();
+        if (tid < kNcta && n0 + tid < p.N && cta_max[tid] != 0u)
+          atomicMax(p.amax_out + n0 + tid, cta_max[tid]);
       }
     }
   }

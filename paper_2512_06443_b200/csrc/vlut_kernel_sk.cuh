@@ -112,6 +112,12 @@ __device__ __forceinline__ void sk_epilogue(const Params& p, const SkParams& sk,
   const bool producer = sg.kb < KT;
   const bool owner = !producer && sg.ka > 0;
   const long long head = (long long)sg.tile * KT;
+  unsigned* cta_max = reinterpret_cast<unsigned*>(const_cast<uint8_t*>(smem) + L::AMAX_OFF);
+  const bool want_max = !ACC_ONLY && p.amax_out != nullptr && !producer;
+  if (want_max) {
+    if (tid < kNcta) cta_max[tid] = 0u;
+    bar_sync(6, L::MCTA);
+  }
   if (owner) {
     // the owner segment is the CTA's last: every table read is done once
     // all lookup warps get here, so the table region holds the tile.
@@ -156,6 +162,7 @@ __device__ __forceinline__ void sk_epilogue(const Params& p, const SkParams& sk,
     // halves of 8 units per thread; all loads of a producer issued together
     constexpr int UPT = 4;
     const int4* red = reinterpret_cast<const int4*>(smem);
+    float tok_max[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 1
     for (int half = 0; half < 16 / UPT; ++half) {
       int4 acc4[UPT];
@@ -192,11 +199,33 @@ __device__ __forceinline__ void sk_epilogue(const Params& p, const SkParams& sk,
             const float sc = (n + k < p.N) ? __fmul_rn(__ldg(p.a_scale + n + k), p.w_scale) : 0.f;
             f[k] = __fmul_rn((float)x[k], sc);
           }
+          if (p.mul_in) {
+            const float* mi = p.mul_in + (size_t)mm * p.N + n;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (n + k < p.N) f[k] = __fmul_rn(f[k], __ldg(mi + k));
+          }
+          if (want_max && mm < p.amax_rows) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (n + k < p.N) tok_max[k] = fmaxf(tok_max[k], fabsf(f[k]));
+          }
           float* o = p.out + (size_t)mm * p.N + n;
           if (p.out_vec4 && n + 3 < p.N) *reinterpret_cast<float4*>(o) = make_float4(f[0], f[1], f[2], f[3]);
           else for (int k = 0; k < 4 && n + k < p.N; ++k) o[k] = f[k];
         }
       }
+    }
+    if (want_max) {
+      // thread's token quad 4 (tid & 15) .. +3 is fixed: lanes l, l+16 share it
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        tok_max[k] = fmaxf(tok_max[k], __shfl_xor_sync(0xffffffffu, tok_max[k], 16));
+        if (lane < 16) atomicMax(cta_max + 4 * (tid & 15) + k, __float_as_uint(tok_max[k]));
+      }
+      bar_sync(6, L::MCTA);
+      if (tid < kNcta && n0 + tid < p.N && cta_max[tid] != 0u)
+        atomicMax(p.amax_out + n0 + tid, cta_max[tid]);
     }
     return;
   }
@@ -244,12 +273,27 @@ __device__ __forceinline__ void sk_epilogue(const Params& p, const SkParams& sk,
             const float sc = (n + k < p.N) ? __fmul_rn(__ldg(p.a_scale + n + k), p.w_scale) : 0.f;
             f[k] = __fmul_rn((float)x[k], sc);
           }
+          if (p.mul_in) {
+            const float* mi = p.mul_in + (size_t)m * p.N + n;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (n + k < p.N) f[k] = __fmul_rn(f[k], __ldg(mi + k));
+          }
+          if (want_max && m < p.amax_rows) {
+            for (int k = 0; k < 4 && n + k < p.N; ++k)
+              atomicMax(cta_max + (n - n0) + k, __float_as_uint(fabsf(f[k])));
+          }
           float* o = p.out + (size_t)m * p.N + n;
           if (p.out_vec4 && n + 3 < p.N) *reinterpret_cast<float4*>(o) = make_float4(f[0], f[1], f[2], f[3]);
           else for (int k = 0; k < 4 && n + k < p.N; ++k) o[k] = f[k];
         }
       }
     }
+  }
+  if (want_max) {
+    bar_sync(6, L::MCTA);
+    if (tid < kNcta && n0 + tid < p.N && cta_max[tid] != 0u)
+      atomicMax(p.amax_out + n0 + tid, cta_max[tid]);
   }
   if (producer) {
     __threadfence();

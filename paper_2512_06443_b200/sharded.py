@@ -49,7 +49,8 @@ class RowShardedLinear:
 
     def __init__(self, W, g: int, w_scale: float, device=None,
                  compute: Optional[Callable] = None, pack: Optional[Callable] = None,
-                 device_pack: bool = False):
+                 device_pack: bool = False, fused: Optional[Callable] = None,
+                 quantize_amax: Optional[Callable] = None):
         dist = _dist()
         self.world = dist.get_world_size() if dist else 1
         self.rank = dist.get_rank() if dist else 0
@@ -76,6 +77,60 @@ class RowShardedLinear:
             import paper_2512_06443_b200 as v
             self.shard = v.pack_weights(np.ascontiguousarray(W_r), g, device=device)
         self._compute = compute or self._cuda_compute
+        self._fused = fused or self._cuda_fused
+        if quantize_amax is None:
+            def quantize_amax(x, amax, q, scale):
+                import paper_2512_06443_b200 as v
+                v.quantize_amax(x, amax, q=q, scale=scale)
+        self._quantize_amax = quantize_amax
+
+    def _cuda_fused(self, shard, A, a_scale, out, mul_in, amax, amax_rows):
+        import paper_2512_06443_b200 as v
+        v.mpgemm_fused(shard, A, a_scale, self.w_scale, out=out, mul_in=mul_in, amax=amax,
+                       amax_rows=amax_rows, ws=v.workspace(A.device))
+
+    def local(self, A, a_scale):
+        """This rank's fp32 rows [rows][N] (no gather)."""
+        import torch
+        out = torch.empty((self.rows, A.shape[1]), dtype=torch.float32, device=A.device)
+        if self.rows:
+            self._compute(self.shard, A, a_scale, out)
+        return out
+
+    def forward_quantized(self, A, a_scale, q_rows: Optional[int] = None, mul_in=None):
+        """Fused re-quantization (f1): the GEMM epilogue multiplies by mul_in
+        (this rank's rows, optional) and produces per-token |out| maxima over
+        the first q_rows global rows; the maxima are all-reduced (MAX) across
+        ranks, each rank quantizes its own rows, and the int8 shards (4x fewer
+        bytes than fp32) are all-gathered.  Returns (q [q_rows][N] int8,
+        scale [N] fp32) on every rank -- bit-identical to quantizing the
+        gathered fp32 output."""
+        import torch
+        N = A.shape[1]
+        dev = A.device
+        q_rows = self.M if q_rows is None else q_rows
+        amax = torch.zeros((N,), dtype=torch.int32, device=dev)
+        local = torch.empty((max(self.rows, 1), N), dtype=torch.float32, device=dev)[:self.rows]
+        arows = max(0, min(self.rows, q_rows - self.r0))
+        if self.rows:
+            self._fused(self.shard, A, a_scale, local, mul_in, amax, arows)
+        d = _dist()
+        if d is not None and self.world > 1:
+            d.all_reduce(amax, op=d.ReduceOp.MAX)
+        q_loc = torch.empty((self.Mp, N), dtype=torch.int8, device=dev)
+        scale = torch.empty((N,), dtype=torch.float32, device=dev)
+        if self.rows:
+            self._quantize_amax(local, amax, q_loc[:self.rows], scale)
+        else:
+            self._quantize_amax(torch.zeros((1, N), dtype=torch.float32, device=dev), amax,
+                                torch.empty((1, N), dtype=torch.int8, device=dev), scale)
+        if self.world == 1:
+            return q_loc[:q_rows], scale
+        if self.rows < self.Mp:
+            q_loc[self.rows:].zero_()
+        full = torch.empty((self.Mp * self.world, N), dtype=torch.int8, device=dev)
+        d.all_gather_into_tensor(full, q_loc)
+        return full[:q_rows], scale
 
     def _cuda_compute(self, shard, A, a_scale, out):
         # workspace path: the planner may pick the stream-K schedule
@@ -122,7 +177,8 @@ class LayerChain:
     """
 
     def __init__(self, layers: Sequence[Sequence[RowShardedLinear]], q_rows: int = CHAIN_Q_ROWS,
-                 quantize: Optional[Callable] = None):
+                 quantize: Optional[Callable] = None, fused: bool = False):
+        self.fused = fused
         self.layers = [tuple(l) for l in layers]
         self.q_rows = q_rows
         if quantize is None:
@@ -130,7 +186,20 @@ class LayerChain:
             quantize = v.quantize
         self.quantize = quantize
 
+    def layer_fused(self, l, xq, xs):
+        """Same layer with fused re-quantization (f1): no separate amax pass,
+        int8 gathers, and gate (.) up fused into the up-projection epilogue
+        (the gate rows never leave their rank)."""
+        L_qkv, L_o, L_gate, L_up, L_down = self.layers[l]
+        q1, s1 = L_qkv.forward_quantized(xq, xs, q_rows=self.q_rows)
+        u, su = L_o.forward_quantized(q1, s1)
+        gate = L_gate.local(u, su)
+        hq, hs = L_up.forward_quantized(u, su, mul_in=gate)
+        return L_down.forward_quantized(hq, hs)
+
     def layer(self, l, xq, xs):
+        if self.fused:
+            return self.layer_fused(l, xq, xs)
         L_qkv, L_o, L_gate, L_up, L_down = self.layers[l]
         qkv = L_qkv(xq, xs)
         q1, s1 = self.quantize(qkv[:self.q_rows])

@@ -333,3 +333,49 @@ def test_streamk_fp32_and_planner_identity(v, M, K, N, g):
     assert torch.equal(o_auto.view(torch.int32), o_cl.view(torch.int32))
     pick = np.unique(np.concatenate([[0, M - 1], synth.rng(2).integers(0, M, size=16)]))
     check_fp32(o_sk.cpu().numpy()[pick], oracle.gemm_i32(W[pick], q), s, synth.W_SCALE)
+
+
+# ------------------------------------------------------------------ fused re-quantization (f1)
+FUSED_PLANS = {"cluster": None, "auto_ws": "ws", "sk16": (16, 1, 1), "sk12": (12, 1, 1),
+               "sk8": (8, 1, 1), "cl12x3": (12, 3, 0)}
+
+
+@pytest.mark.parametrize("M,K,N,rows", [(6912, 2560, 256, 6912), (3840, 2560, 200, 2560),
+                                        (100, 512, 9, 37), (2560, 6912, 130, 2560)])
+@pytest.mark.parametrize("how", list(FUSED_PLANS))
+def test_mpgemm_fused_mul_and_amax(v, M, K, N, rows, how):
+    W = synth.ternary_weights(M, K, seed=M + 5)
+    x = synth.activations_f32(K, N, seed=N + 5)
+    q, s = oracle.quantize(x)
+    g = synth.rng(3).standard_normal((M, N), dtype=np.float32)
+    pw = v.pack_weights(W, 4, device=dev())
+    amax = torch.zeros((N,), dtype=torch.int32, device=dev())
+    h = FUSED_PLANS[how]
+    plan = v.LaunchPlan(h[0], h[1], streamk=h[2]) if isinstance(h, tuple) else None
+    ws = v.workspace(dev()) if h is not None else None
+    out = v.mpgemm_fused(pw, to_dev(q), to_dev(s), synth.W_SCALE, mul_in=to_dev(g), amax=amax,
+                         amax_rows=rows, plan=plan, ws=ws)
+    torch.cuda.synchronize()
+    ref = (oracle.dequant_f32(oracle.gemm_i32(W, q), s, synth.W_SCALE) * g).astype(np.float32)
+    assert np.array_equal(out.cpu().numpy().view(np.int32), ref.view(np.int32))
+    ref_amax = np.abs(ref[:rows]).max(0).astype(np.float32)
+    assert np.array_equal(amax.cpu().numpy().view(np.float32), ref_amax)
+    # quantize with the fused maxima == the oracle quantizer on those rows
+    qq, ss = v.quantize_amax(out[:rows].contiguous(), amax)
+    qr, sr = oracle.quantize(np.ascontiguousarray(ref[:rows]))
+    torch.cuda.synchronize()
+    assert np.array_equal(ss.cpu().numpy(), sr) and np.array_equal(qq.cpu().numpy(), qr)
+
+
+def test_config5_chain_fused_equals_unfused(v):
+    from paper_2512_06443_b200.sharded import LayerChain, RowShardedLinear
+    cfg = synth.CONFIGS[5]
+    N, n_layers = 2048, 2
+    layers = [[RowShardedLinear(w, 4, synth.W_SCALE, device=dev(), device_pack=True)
+               for _, w in synth.config_weights(cfg, l)] for l in range(n_layers)]
+    x = synth.activations_f32(2560, N, synth.act_seed(cfg, N))
+    xq, xs = v.quantize(to_dev(x))
+    a_q, a_s = LayerChain(layers)(xq, xs)
+    b_q, b_s = LayerChain(layers, fused=True)(xq, xs)
+    torch.cuda.synchronize()
+    assert torch.equal(a_q, b_q) and torch.equal(a_s.view(torch.int32), b_s.view(torch.int32))

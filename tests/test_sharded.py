@@ -31,6 +31,29 @@ def oracle_compute(w_scale):
     return f
 
 
+def oracle_fused(w_scale):
+    def f(shard, A, a_scale, out, mul_in, amax, amax_rows):
+        o = oracle.dequant_f32(oracle.gemm_i32(shard, A.numpy()), a_scale.numpy(), w_scale)
+        if mul_in is not None:
+            o = (o * mul_in.numpy()).astype(np.float32)
+        out.copy_(torch.from_numpy(o))
+        if amax_rows > 0:
+            m = np.abs(o[:amax_rows]).max(0).astype(np.float32).view(np.int32)
+            amax.copy_(torch.maximum(amax, torch.from_numpy(m)))
+    return f
+
+
+def oracle_quantize_amax(x, amax, q, scale):
+    s = amax.numpy().view(np.float32)
+    s = np.where(s == 0, np.float32(1), (s / np.float32(127)).astype(np.float32)).astype(np.float32)
+    t = (x.numpy() / s[None, :]).astype(np.float32)
+    # roundf = round half away from zero, via the oracle's own quantizer on a
+    # column-scaled copy would re-derive the scale; do it directly here
+    r = np.where(t >= 0, np.floor(t + np.float32(0.5)), -np.floor(-t + np.float32(0.5)))
+    q.copy_(torch.from_numpy(np.clip(r, -127, 127).astype(np.int8)))
+    scale.copy_(torch.from_numpy(s))
+
+
 def oracle_quantize(x, y=None):
     xx = x.numpy() if y is None else (x.numpy() * y.numpy()).astype(np.float32)
     q, s = oracle.quantize(np.ascontiguousarray(xx))
@@ -65,12 +88,18 @@ def _worker(rank, world, port, M, K, N, g, result_path):
               synth.ternary_weights(80, Kc, 3), synth.ternary_weights(80, Kc, 4),
               synth.ternary_weights(Kc, 80, 5)]
         layer = [RowShardedLinear(w, 4, synth.W_SCALE, compute=oracle_compute(synth.W_SCALE),
-                                  pack=lambda w_, gg: w_) for w in Ws]
+                                  pack=lambda w_, gg: w_, fused=oracle_fused(synth.W_SCALE),
+                                  quantize_amax=oracle_quantize_amax) for w in Ws]
         chain = LayerChain([layer, layer], q_rows=Kc, quantize=oracle_quantize)
         xq, xs = oracle.quantize(synth.activations_f32(Kc, 6, seed=7))
         cq, cs = chain(torch.from_numpy(xq), torch.from_numpy(xs))
+        # f1: fused re-quantization, MAX all-reduce of the per-rank maxima,
+        # int8 all-gather, gate (.) up fused into the up projection
+        fchain = LayerChain([layer, layer], q_rows=Kc, quantize=oracle_quantize, fused=True)
+        fq, fs = fchain(torch.from_numpy(xq), torch.from_numpy(xs))
         if rank == 0:
-            np.savez(result_path, out=out.numpy(), cq=cq.numpy(), cs=cs.numpy())
+            np.savez(result_path, out=out.numpy(), cq=cq.numpy(), cs=cs.numpy(),
+                     fq=fq.numpy(), fs=fs.numpy())
     finally:
         dist.destroy_process_group()
 
@@ -94,3 +123,4 @@ def test_gloo_row_sharded_equals_single(tmp_path, world, M):
     for _ in range(2):
         xq, xs = oracle.config5_layer(Ws, synth.W_SCALE, xq, xs, q_rows=Kc)
     assert np.array_equal(res["cq"], xq) and np.array_equal(res["cs"], xs)
+    assert np.array_equal(res["fq"], xq) and np.array_equal(res["fs"], xs)
