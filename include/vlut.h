@@ -97,6 +97,12 @@ typedef struct {
   int32_t grid_ctas;    /* total CTAs launched                              */
   int32_t smem_bytes;   /* dynamic shared memory per CTA                    */
   int32_t streamk;      /* 1: stream-K persistent schedule (needs a workspace) */
+  int32_t slot;         /* 1: K2 lane-slot kernel (small N / decode / scalar-LUT comparator):
+                           m_cta = 1024 (g=4) or 2048 (g=5), n_cta = nw * tpw, `splits`
+                           CTAs along K (> 1 needs a workspace)                       */
+  int32_t tpw;          /* K2 tokens per 4-byte table word: 1 = scalar LUT (1->1 lookups,
+                           one table per token), 2 = vector LUT (1->2)       */
+  int32_t nw;           /* K2 table words per lookup: 1, 2, 4 or 8 (g=5: 1 or 2)      */
 } vlut_launch_plan;
 
 /* Payload bytes for an M x K ternary matrix packed with group size g
@@ -172,8 +178,9 @@ vlut_status vlut_mpgemm_ex(const vlut_packed_weights* W, const int8_t* A,
  * Stream-K persistent schedule (one CTA per SM; every SM gets the same number
  * of K-tile work units whatever the tile count; split tiles are combined
  * through int32 partials in a caller-provided workspace).  Same results as
- * vlut_mpgemm.  The planner picks stream-K or the cluster split-K schedule by
- * its cost model (plan == NULL) unless plan->streamk forces it.
+ * vlut_mpgemm.  The planner picks stream-K, the cluster split-K schedule or,
+ * for small N, the K2 lane-slot kernel (split-K through the workspace) by its
+ * cost model (plan == NULL) unless plan->streamk / plan->slot forces one.
  *   workspace : device, >= vlut_workspace_bytes() bytes, 16-B aligned, ZEROED
  *               ONCE before its first use (flags are per-launch epochs), and
  *               used by one stream at a time.
@@ -189,6 +196,21 @@ vlut_status vlut_mpgemm_acc_ws(const vlut_packed_weights* W, const int8_t* A, in
                                void* workspace, size_t ws_bytes, void* stream);
 /* The plan vlut_mpgemm_ws would choose (stream-K or cluster split-K). */
 vlut_status vlut_plan_ws(int M, int K, int N, int g, vlut_launch_plan* plan);
+
+/*
+ * Scalar-LUT comparator and decode path (f4):
+ * the K2 kernel with one table PER TOKEN and one 1->1 lookup per (row, group,
+ * token) -- the T-MAC paradigm the paper contrasts with Vec-LUT -- laid out
+ * so every lookup is a conflict-free 4-byte shared-memory read.  At N = 1 it
+ * is also the Vec-LUT (one token: the two paradigms coincide) and the planner
+ * uses it for decode.  Same results and contract as vlut_mpgemm_ws
+ * (workspace may be NULL: then no split-K).  plan may be NULL (heuristic
+ * nw); plan->slot/tpw are forced to 1/1.
+ */
+vlut_status vlut_mpgemm_scalar_lut(const vlut_packed_weights* W, const int8_t* A,
+                                   const float* a_scale, float w_scale, float* out, int M, int K,
+                                   int N, const vlut_launch_plan* plan, void* workspace,
+                                   size_t ws_bytes, void* stream);
 
 /* Raw int32 accumulators, no scales (bit-exact test hook):
  *   acc_out : device int32 [M][N].  Other arguments as vlut_mpgemm_ex. */

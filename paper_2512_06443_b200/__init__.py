@@ -26,7 +26,7 @@ __all__ = [
     "mpgemm_ex", "mpgemm_acc", "quantize", "last_error", "EXPORTS", "group_schedule",
     "MixedPackedWeights", "pack_weights_mixed", "mpgemm_mixed", "mpgemm_layout", "quantize_t",
     "linear", "workspace", "plan_ws", "mpgemm_ws", "mpgemm_acc_ws", "mpgemm_fused",
-    "quantize_amax",
+    "quantize_amax", "mpgemm_scalar_lut", "slot_plan",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -63,7 +63,8 @@ class _Plan(ctypes.Structure):
     _fields_ = [("warps", ctypes.c_int32), ("splits", ctypes.c_int32),
                 ("m_cta", ctypes.c_int32), ("n_cta", ctypes.c_int32),
                 ("grid_ctas", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
-                ("streamk", ctypes.c_int32)]
+                ("streamk", ctypes.c_int32), ("slot", ctypes.c_int32),
+                ("tpw", ctypes.c_int32), ("nw", ctypes.c_int32)]
 
 
 # Every symbol include/vlut.h declares (tests check the .so exports them all).
@@ -124,6 +125,10 @@ EXPORTS = {
                            ctypes.c_void_p], ctypes.c_int),
     "vlut_quantize_amax": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "vlut_mpgemm_scalar_lut": ([ctypes.POINTER(_Desc), ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_float, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                ctypes.c_int, ctypes.POINTER(_Plan), ctypes.c_void_p,
+                                ctypes.c_size_t, ctypes.c_void_p], ctypes.c_int),
     "vlut_launches_per_mpgemm": ([], ctypes.c_int),
     "vlut_active_clusters": ([ctypes.c_int, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "vlut_last_error": ([], ctypes.c_char_p),
@@ -185,10 +190,23 @@ class LaunchPlan:
     grid_ctas: int = 0
     smem_bytes: int = 0
     streamk: int = 0
+    slot: int = 0   # 1: K2 lane-slot kernel (small N / decode / scalar-LUT comparator)
+    tpw: int = 0    # K2 tokens per table word: 1 = scalar LUT (1->1), 2 = vector (1->2)
+    nw: int = 0     # K2 table words per lookup (0 = heuristic)
 
     def _c(self) -> _Plan:
         return _Plan(self.warps, self.splits, self.m_cta, self.n_cta, self.grid_ctas,
-                     self.smem_bytes, self.streamk)
+                     self.smem_bytes, self.streamk, self.slot, self.tpw, self.nw)
+
+    @staticmethod
+    def _from_c(p: "_Plan") -> "LaunchPlan":
+        return LaunchPlan(p.warps, p.splits, p.m_cta, p.n_cta, p.grid_ctas, p.smem_bytes,
+                          p.streamk, p.slot, p.tpw, p.nw)
+
+
+def slot_plan(tpw: int = 2, nw: int = 0, splits: int = 0) -> LaunchPlan:
+    """A K2 plan: tpw 1 (scalar LUT) or 2 (vector); nw / splits 0 = heuristic."""
+    return LaunchPlan(warps=16, splits=splits, n_cta=0, slot=1, tpw=tpw, nw=nw)
 
 
 class PackedWeights:
@@ -263,7 +281,7 @@ def unpack_weights_host(pw: PackedWeights) -> np.ndarray:
 def plan(M: int, K: int, N: int, g: int) -> LaunchPlan:
     p = _Plan()
     _check(lib().vlut_plan(M, K, N, g, ctypes.byref(p)))
-    return LaunchPlan(p.warps, p.splits, p.m_cta, p.n_cta, p.grid_ctas, p.smem_bytes, p.streamk)
+    return LaunchPlan._from_c(p)
 
 
 def _plan_ptr(p: Optional[LaunchPlan]):
@@ -444,7 +462,7 @@ def workspace(device=None):
 def plan_ws(M: int, K: int, N: int, g: int) -> LaunchPlan:
     p = _Plan()
     _check(lib().vlut_plan_ws(M, K, N, g, ctypes.byref(p)))
-    return LaunchPlan(p.warps, p.splits, p.m_cta, p.n_cta, p.grid_ctas, p.smem_bytes, p.streamk)
+    return LaunchPlan._from_c(p)
 
 
 def mpgemm_ws(W: PackedWeights, A, a_scale, w_scale: float, out=None,
@@ -511,3 +529,24 @@ def quantize_amax(x, amax, q=None, scale=None, stream=None):
     _check(lib().vlut_quantize_amax(_dev_ptr(x), _dev_ptr(amax), K, N, _dev_ptr(q),
                                     _dev_ptr(scale), _stream_ptr(stream)))
     return q, scale
+
+
+# ---------------------------------------------------------------- scalar-LUT comparator (f4)
+def mpgemm_scalar_lut(W: PackedWeights, A, a_scale, w_scale: float, out=None,
+                      plan: Optional[LaunchPlan] = None, ws=None, use_ws: bool = True,
+                      stream=None):
+    """The scalar-LUT (1->1, one table per token) mpGeMM on the K2 kernel
+    (P:84-85); with use_ws the K range is split across CTAs."""
+    import torch
+    K, N = A.shape
+    M = W.M
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    if ws is None and use_ws:
+        ws = workspace(A.device)
+    wsp, wsn = (_dev_ptr(ws), ws.numel()) if ws is not None else (ctypes.c_void_p(0), 0)
+    keep, pp = _plan_ptr(plan)
+    _check(lib().vlut_mpgemm_scalar_lut(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(a_scale),
+                                        float(w_scale), _dev_ptr(out), M, K, N, pp, wsp, wsn,
+                                        _stream_ptr(stream)))
+    return out

@@ -12,6 +12,7 @@
 #include "vlut_aux_kernels.cuh"
 #include "vlut_kernel.cuh"
 #include "vlut_kernel_sk.cuh"
+#include "vlut_kernel_slot.cuh"
 #include <atomic>
 
 namespace {
@@ -207,8 +208,16 @@ int active_clusters_for(int g, int warps, int S) {
 
 inline bool valid_split(int warps, int S) { return warps > 0 && S >= 1 && S <= 8; }
 
-// Stream-K workspace: int32 partials [sms][512 x 64] + flags.
-size_t sk_workspace_bytes(int sms) { return (size_t)sms * 512 * 64 * 4 + 4096; }
+// Workspace layout (caller-provided, zeroed once):
+//   [0, SK)             stream-K int32 partials [sms][512 x 64]
+//   [SK, SK + 4096)     stream-K epoch flags
+//   [.., + 64 KB)       K2 split-K arrival counters (kept zero between launches)
+//   [.., + 16 MB)       K2 split-K int32 accumulators [M][N] (kept zero)
+size_t sk_part_bytes(int sms) { return (size_t)sms * 512 * 64 * 4; }
+size_t slot_cnt_off(int sms) { return sk_part_bytes(sms) + 4096; }
+size_t slot_acc_off(int sms) { return slot_cnt_off(sms) + (size_t)vlut::slot::kMaxCounters * 4; }
+constexpr size_t kSlotAccBytes = (size_t)16 << 20;
+size_t sk_workspace_bytes(int sms) { return slot_acc_off(sms) + kSlotAccBytes; }
 
 // Best stream-K plan (persistent, grid = #SMs): every CTA gets ceil(U / sms)
 // K-tile units; cost in the same SMEM-cycle units as plan_for.
@@ -292,7 +301,121 @@ double plan_for(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
   return best_cost;
 }
 
+// ------------------------------------------------------------ K2 (lane-slot) planner
+// K2 variants: (nw, tpw) with n_cta = nw * tpw tokens per CTA.
+inline bool slot_variant_ok(int g, int nw, int tpw) {
+  if (!(tpw == 1 || tpw == 2)) return false;
+  if (!(nw == 1 || nw == 2 || nw == 4 || nw == 8)) return false;
+  return g == 4 || nw <= 2;
+}
+inline int slot_mcta(int g) { return g == 4 ? 1024 : 2048; }
+int slot_smem(int g, int nw, int tpw);
+
+// The narrowest variant covering N tokens in one N-tile (capped at the widest).
+int slot_default_nw(int g, int N, int tpw) {
+  const int maxnw = g == 4 ? 8 : 2;
+  int nw = 1;
+  while (nw < maxnw && nw * tpw < N) nw *= 2;
+  return nw;
+}
+
+// Cost in shared-memory cycles of one SM (the K1 planner's unit): per K-tile
+// lookups (m_cta * 16 groups * nw words / 32 lanes per wavefront) + the table
+// build (nw * 3^g wavefronts) + the index reads (m_cta / 8); an index tile of
+// m_cta * 16 B must also arrive from HBM (~22 B/clk/SM when all SMs stream);
+// split-K adds the red.global traffic of the partial tile.
+double plan_slot(int M, int K, int N, int g, int sms, int tpw, int nw_force, int S_force,
+                 bool have_ws, vlut_launch_plan* out) {
+  const int KG = K / g;
+  const int kgt = (KG + VLUT_KG_TILE - 1) / VLUT_KG_TILE;
+  const int nw = nw_force > 0 ? nw_force : slot_default_nw(g, N, tpw);
+  if (!slot_variant_ok(g, nw, tpw)) return 1e300;
+  const int ntok = nw * tpw, mcta = slot_mcta(g);
+  const long long NTt = (N + ntok - 1) / ntok, MT = (M + mcta - 1) / mcta;
+  const long long tiles = NTt * MT;
+  int S = 1;
+  if (S_force > 0) {
+    S = S_force;
+  } else if (have_ws && tiles <= vlut::slot::kMaxCounters &&
+             (size_t)M * (size_t)N * 4 <= kSlotAccBytes) {
+    S = (int)(sms / tiles);
+    if (S < 1) S = 1;
+    if (S > kgt) S = kgt;
+  }
+  if (S > kgt) S = kgt;
+  if (S < 1) S = 1;
+  const long long ctas = tiles * S;
+  const long long waves = (ctas + sms - 1) / sms;
+  const double kt_per = (double)((kgt + S - 1) / S);
+  const double smem_tile = mcta * 16.0 * nw / 32.0 + (double)nw * pow3i(g) + mcta / 8.0;
+  const double hbm_tile = mcta * 16.0 / 22.0;
+  double per_cta = kt_per * (smem_tile > hbm_tile ? smem_tile : hbm_tile) + 3000.0;
+  if (S > 1) per_cta += mcta * (double)ntok / 32.0 * 8.0;
+  const double cost = (double)waves * per_cta;
+  if (out) {
+    memset(out, 0, sizeof(*out));
+    out->warps = vlut::slot::kLW;
+    out->splits = S;
+    out->m_cta = mcta;
+    out->n_cta = ntok;
+    out->grid_ctas = (int)(ctas > 0x7fffffff ? 0x7fffffff : ctas);
+    out->smem_bytes = slot_smem(g, nw, tpw);
+    out->streamk = 0;
+    out->slot = 1;
+    out->tpw = tpw;
+    out->nw = nw;
+  }
+  return cost;
+}
+
 // ------------------------------------------------------------ launches
+template <int G, int NW, int TPW>
+vlut_status launch_slot(const vlut::slot::SlotParams& p, int S, int NTt, int MT, cudaStream_t st) {
+  using L = vlut::slot::SL<G, NW, TPW>;
+  auto kern = vlut::slot::vlut_slot_kernel<G, NW, TPW>;
+  static std::once_flag flags[64];
+  static cudaError_t errs[64];
+  int dev = 0;
+  VLUT_CUDA_TRY(cudaGetDevice(&dev));
+  std::call_once(flags[dev & 63], [&] {
+    errs[dev & 63] = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+  });
+  VLUT_CUDA_TRY(errs[dev & 63]);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)S, (unsigned)NTt, (unsigned)MT);
+  cfg.blockDim = dim3(vlut::slot::kThreads, 1, 1);
+  cfg.dynamicSmemBytes = L::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  VLUT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
+  return VLUT_OK;
+}
+
+#define VLUT_SLOT_VARIANTS(X) \
+  X(4, 1, 1) X(4, 2, 1) X(4, 4, 1) X(4, 8, 1) X(4, 1, 2) X(4, 2, 2) X(4, 4, 2) X(4, 8, 2) \
+  X(5, 1, 1) X(5, 2, 1) X(5, 1, 2) X(5, 2, 2)
+
+int slot_smem(int g, int nw, int tpw) {
+#define X(G_, NW_, TPW_) \
+  if (g == G_ && nw == NW_ && tpw == TPW_) return vlut::slot::SL<G_, NW_, TPW_>::SMEM;
+  VLUT_SLOT_VARIANTS(X)
+#undef X
+  return 0;
+}
+
+vlut_status dispatch_slot(int g, int nw, int tpw, const vlut::slot::SlotParams& p, int S, int NTt,
+                          int MT, cudaStream_t st) {
+#define X(G_, NW_, TPW_) \
+  if (g == G_ && nw == NW_ && tpw == TPW_) return launch_slot<G_, NW_, TPW_>(p, S, NTt, MT, st);
+  VLUT_SLOT_VARIANTS(X)
+#undef X
+  return fail(VLUT_ERR_UNSUPPORTED, "no K2 variant for g=%d nw=%d tpw=%d", g, nw, tpw);
+}
+
 template <int G, int WARPS, bool ACC>
 vlut_status launch_k1(const vlut::Params& p, int S, int NT, int MT, cudaStream_t st) {
   using L = vlut::Layout<G, WARPS>;
@@ -374,6 +497,62 @@ vlut_status dispatch(int g, int warps, const vlut::Params& p, int S, int NT, int
   return fail(VLUT_ERR_UNSUPPORTED, "no kernel variant for g=%d warps=%d", g, warps);
 }
 
+// K2 launch for a validated call (sizes, descriptor, pointers checked by the
+// caller).  plan.slot must be 1; nw/tpw/splits 0 = heuristic.
+constexpr int kSlotAutoMaxN = 128;
+
+vlut_status run_slot(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,
+                     float w_scale, void* out, int M, int K, int N, vlut_launch_plan plan,
+                     void* ws, size_t ws_bytes, void* stream, bool acc_only, const DeviceInfo& d) {
+  const int g = W->g;
+  const int tpw = plan.tpw ? plan.tpw : 2;
+  const bool have_ws = ws != nullptr;
+  if (have_ws) {
+    if (ws_bytes < sk_workspace_bytes(d.sms))
+      return fail(VLUT_ERR_BUFFER_TOO_SMALL, "workspace needs %zu bytes", sk_workspace_bytes(d.sms));
+    if (((uintptr_t)ws) & 15) return fail(VLUT_ERR_MISALIGNED, "workspace not 16-B aligned");
+  }
+  if (plan.nw && !slot_variant_ok(g, plan.nw, tpw))
+    return fail(VLUT_ERR_UNSUPPORTED, "no K2 variant for g=%d nw=%d tpw=%d", g, plan.nw, tpw);
+  if (!(tpw == 1 || tpw == 2)) return fail(VLUT_ERR_INVALID_ARGUMENT, "tpw must be 1 or 2");
+  vlut_launch_plan pl = {};
+  plan_slot(M, K, N, g, d.sms, tpw, plan.nw, plan.splits, have_ws, &pl);
+  const int S = pl.splits;
+  const long long NTt = (N + pl.n_cta - 1) / pl.n_cta;
+  const long long MT = (M + pl.m_cta - 1) / pl.m_cta;
+  if (NTt > 65535 || MT > 65535 || S > 65535) return fail(VLUT_ERR_SHAPE, "grid too large");
+  if (S > 1) {
+    if (!have_ws) return fail(VLUT_ERR_INVALID_ARGUMENT, "K2 split-K (splits=%d) needs a workspace", S);
+    if (NTt * MT > vlut::slot::kMaxCounters || (size_t)M * (size_t)N * 4 > kSlotAccBytes)
+      return fail(VLUT_ERR_SHAPE, "M*N too large for K2 split-K workspace");
+  }
+  if (pl.smem_bytes > d.smem_optin)
+    return fail(VLUT_ERR_UNSUPPORTED, "needs %d B shared memory, device allows %d", pl.smem_bytes,
+                d.smem_optin);
+  vlut::slot::SlotParams p;
+  memset(&p, 0, sizeof(p));
+  p.payload = static_cast<const uint8_t*>(W->payload);
+  p.A = A;
+  p.a_scale = a_scale;
+  p.w_scale = w_scale;
+  p.out = out;
+  p.M = M;
+  p.K = K;
+  p.N = N;
+  p.m_pad = W->m_pad;
+  p.kg_tiles = W->kg_tiles;
+  p.splits = S;
+  p.acc_only = acc_only ? 1 : 0;
+  if (have_ws) {
+    p.ws_cnt = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + slot_cnt_off(d.sms));
+    p.ws_acc = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + slot_acc_off(d.sms));
+  }
+  vlut_status st = dispatch_slot(g, pl.nw, tpw, p, S, (int)NTt, (int)MT,
+                                 static_cast<cudaStream_t>(stream));
+  if (st != VLUT_OK) return st;
+  return ok();
+}
+
 vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,
                        float w_scale, void* out, int M, int K, int N,
                        const vlut_launch_plan* plan_in, void* stream, bool acc_only,
@@ -394,8 +573,15 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
   st = device_info(&d);
   if (st != VLUT_OK) return st;
   vlut_launch_plan plan = {};
+  const bool plain_epilogue = !acc_in && !out_t && !mul_in && !amax_out;
   if (plan_in) {
     plan = *plan_in;
+    if (plan.slot) {
+      if (!plain_epilogue)
+        return fail(VLUT_ERR_UNSUPPORTED, "K2 plan: no acc_in / transposed / fused epilogue");
+      return run_slot(W, A, a_scale, w_scale, out, M, K, N, plan, ws, ws_bytes, stream, acc_only,
+                      d);
+    }
     if (!(plan.warps == 8 || plan.warps == 12 || plan.warps == 16) ||
         !valid_split(plan.warps, plan.splits))
       return fail(VLUT_ERR_INVALID_ARGUMENT, "invalid plan warps=%d splits=%d", plan.warps,
@@ -403,11 +589,22 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
     if (plan.streamk && (!ws || acc_in || out_t))
       return fail(VLUT_ERR_INVALID_ARGUMENT, "stream-K plan needs a workspace and [M][N] output");
   } else {
-    const double c_cl = plan_for(M, K, N, W->g, d.sms, &plan);
+    double c_best = plan_for(M, K, N, W->g, d.sms, &plan);
     if (ws && !acc_in && !out_t) {
       vlut_launch_plan sk_plan = {};
       const double c_sk = plan_sk(M, K, N, W->g, d.sms, &sk_plan);
-      if (c_sk < c_cl) plan = sk_plan;
+      if (c_sk < c_best) {
+        plan = sk_plan;
+        c_best = c_sk;
+      }
+    }
+    if (plain_epilogue && N <= kSlotAutoMaxN) {
+      vlut_launch_plan sl = {};
+      const bool have_ws = ws && ws_bytes >= sk_workspace_bytes(d.sms) && ((uintptr_t)ws & 15) == 0;
+      const double c_sl = plan_slot(M, K, N, W->g, d.sms, 2, 0, 0, have_ws, &sl);
+      if (c_sl < c_best)
+        return run_slot(W, A, a_scale, w_scale, out, M, K, N, sl, have_ws ? ws : nullptr,
+                        ws_bytes, stream, acc_only, d);
     }
   }
   if (plan.streamk && ws_bytes < sk_workspace_bytes(d.sms))
@@ -456,7 +653,7 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
     sk.MT = (int)MT;
     sk.U = MT * NT * (long long)W->kg_tiles;
     sk.ws = static_cast<int32_t*>(ws);
-    sk.flags = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + (size_t)d.sms * 512 * 64 * 4);
+    sk.flags = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + sk_part_bytes(d.sms));
     unsigned e = ++epoch;
     if (e == 0) e = ++epoch;
     sk.epoch = e;
@@ -651,6 +848,18 @@ vlut_status vlut_mpgemm_acc_ws(const vlut_packed_weights* W, const int8_t* A, in
                     workspace, ws_bytes);
 }
 
+vlut_status vlut_mpgemm_scalar_lut(const vlut_packed_weights* W, const int8_t* A,
+                                   const float* a_scale, float w_scale, float* out, int M, int K,
+                                   int N, const vlut_launch_plan* plan, void* workspace,
+                                   size_t ws_bytes, void* stream) {
+  vlut_launch_plan pl = {};
+  if (plan) pl = *plan;
+  pl.slot = 1;
+  pl.tpw = 1;
+  return run_mpgemm(W, A, a_scale, w_scale, out, M, K, N, &pl, stream, false, nullptr, 0,
+                    workspace, ws_bytes);
+}
+
 vlut_status vlut_plan_ws(int M, int K, int N, int g, vlut_launch_plan* plan) {
   if (!plan) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL plan");
   if (M <= 0 || K <= 0 || N <= 0 || !valid_g(g)) return fail(VLUT_ERR_INVALID_ARGUMENT, "bad sizes");
@@ -659,9 +868,14 @@ vlut_status vlut_plan_ws(int M, int K, int N, int g, vlut_launch_plan* plan) {
   vlut_status st = device_info(&d);
   if (st != VLUT_OK) return st;
   memset(plan, 0, sizeof(*plan));
-  vlut_launch_plan skp = {};
-  const double c_cl = plan_for(M, K, N, g, d.sms, plan);
-  if (plan_sk(M, K, N, g, d.sms, &skp) < c_cl) *plan = skp;
+  vlut_launch_plan skp = {}, slp = {};
+  double c = plan_for(M, K, N, g, d.sms, plan);
+  const double c_sk = plan_sk(M, K, N, g, d.sms, &skp);
+  if (c_sk < c) {
+    *plan = skp;
+    c = c_sk;
+  }
+  if (N <= kSlotAutoMaxN && plan_slot(M, K, N, g, d.sms, 2, 0, 0, true, &slp) < c) *plan = slp;
   return ok();
 }
 
