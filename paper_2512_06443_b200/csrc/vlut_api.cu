@@ -215,7 +215,7 @@ inline bool valid_split(int warps, int S) { return warps > 0 && S >= 1 && S <= 8
 //   [.., + 16 MB)       K2 split-K int32 accumulators [M][N] (kept zero)
 size_t sk_part_bytes(int sms) { return (size_t)sms * 512 * 64 * 4; }
 size_t slot_cnt_off(int sms) { return sk_part_bytes(sms) + 4096; }
-size_t slot_acc_off(int sms) { return slot_cnt_off(sms) + (size_t)vlut::slot::kMaxCounters * 4; }
+size_t slot_acc_off(int sms) { return slot_cnt_off(sms) + (size_t)vlut::slot::kMaxCounters * 8; }
 constexpr size_t kSlotAccBytes = (size_t)16 << 20;
 size_t sk_workspace_bytes(int sms) { return slot_acc_off(sms) + kSlotAccBytes; }
 
@@ -338,7 +338,7 @@ double plan_slot(int M, int K, int N, int g, int sms, int tpw, int nw_force, int
     S = S_force;
   } else if (have_ws && tiles <= vlut::slot::kMaxCounters &&
              (size_t)M * (size_t)N * 4 <= kSlotAccBytes) {
-    S = (int)(sms / tiles);
+    S = (int)(sms / tiles);  // one wave: split-K CTAs must be co-resident
     if (S < 1) S = 1;
     if (S > kgt) S = kgt;
   }
@@ -386,11 +386,14 @@ vlut_status launch_slot(const vlut::slot::SlotParams& p, int S, int NTt, int MT,
   cfg.blockDim = dim3(vlut::slot::kThreads, 1, 1);
   cfg.dynamicSmemBytes = L::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  // split-K CTAs of a tile wait for each other: all CTAs must be co-resident
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = S > 1 ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   VLUT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
   return VLUT_OK;
 }
@@ -499,7 +502,7 @@ vlut_status dispatch(int g, int warps, const vlut::Params& p, int S, int NT, int
 
 // K2 launch for a validated call (sizes, descriptor, pointers checked by the
 // caller).  plan.slot must be 1; nw/tpw/splits 0 = heuristic.
-constexpr int kSlotAutoMaxN = 128;
+constexpr int kSlotAutoMaxN = 64;
 
 vlut_status run_slot(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,
                      float w_scale, void* out, int M, int K, int N, vlut_launch_plan plan,
@@ -523,6 +526,9 @@ vlut_status run_slot(const vlut_packed_weights* W, const int8_t* A, const float*
   if (NTt > 65535 || MT > 65535 || S > 65535) return fail(VLUT_ERR_SHAPE, "grid too large");
   if (S > 1) {
     if (!have_ws) return fail(VLUT_ERR_INVALID_ARGUMENT, "K2 split-K (splits=%d) needs a workspace", S);
+    if (NTt * MT * S > d.sms)
+      return fail(VLUT_ERR_UNSUPPORTED, "K2 split-K needs all %lld CTAs co-resident (%d SMs)",
+                  NTt * MT * S, d.sms);
     if (NTt * MT > vlut::slot::kMaxCounters || (size_t)M * (size_t)N * 4 > kSlotAccBytes)
       return fail(VLUT_ERR_SHAPE, "M*N too large for K2 split-K workspace");
   }
@@ -543,6 +549,7 @@ vlut_status run_slot(const vlut_packed_weights* W, const int8_t* A, const float*
   p.kg_tiles = W->kg_tiles;
   p.splits = S;
   p.acc_only = acc_only ? 1 : 0;
+  p.act_tma = (N <= vlut::slot::kActNMax && (((uintptr_t)A) & 15) == 0) ? 1 : 0;
   if (have_ws) {
     p.ws_cnt = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + slot_cnt_off(d.sms));
     p.ws_acc = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + slot_acc_off(d.sms));
@@ -601,7 +608,9 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
     if (plain_epilogue && N <= kSlotAutoMaxN) {
       vlut_launch_plan sl = {};
       const bool have_ws = ws && ws_bytes >= sk_workspace_bytes(d.sms) && ((uintptr_t)ws & 15) == 0;
-      const double c_sl = plan_slot(M, K, N, W->g, d.sms, 2, 0, 0, have_ws, &sl);
+      // N = 1: one token, the scalar and the vector LUT coincide; a 1-token
+      // word (tpw = 1) wastes no half-words
+      const double c_sl = plan_slot(M, K, N, W->g, d.sms, N == 1 ? 1 : 2, 0, 0, have_ws, &sl);
       if (c_sl < c_best)
         return run_slot(W, A, a_scale, w_scale, out, M, K, N, sl, have_ws ? ws : nullptr,
                         ws_bytes, stream, acc_only, d);
@@ -875,7 +884,8 @@ vlut_status vlut_plan_ws(int M, int K, int N, int g, vlut_launch_plan* plan) {
     *plan = skp;
     c = c_sk;
   }
-  if (N <= kSlotAutoMaxN && plan_slot(M, K, N, g, d.sms, 2, 0, 0, true, &slp) < c) *plan = slp;
+  if (N <= kSlotAutoMaxN && plan_slot(M, K, N, g, d.sms, N == 1 ? 1 : 2, 0, 0, true, &slp) < c)
+    *plan = slp;
   return ok();
 }
 

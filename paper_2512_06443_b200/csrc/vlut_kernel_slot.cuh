@@ -1,5 +1,5 @@
 // vlut_kernel_slot.cuh -- K2: lane-slot LUT mpGeMM for small token counts
-// (decode, N = 1 .. ~64) and the scalar-LUT (1->1) comparator (f4).
+// (decode, N = 1 .. 64) and the scalar-LUT (1->1) comparator (f4).
 //
 // K1 (vlut_kernel.cuh) reads a 128-byte table row (64 tokens) per lookup and
 // needs N >= 64 to fill it.  K2 keeps every lookup conflict-free for ANY
@@ -13,30 +13,37 @@
 //                 XOR order j = step ^ x; at every step the 16 lanes of each
 //                 half-warp read 16 different slots and the two halves the
 //                 two copies: 32 lanes -> 32 banks, whatever indices they
-//                 hold.  One LDS.32 per lookup and word.
+//                 hold.  One PRMT forms the address (index byte -> bits 8..15,
+//                 slot -> bits 0..7); one LDS.32 per lookup and word.
 //   words         TPW = 1: a word is ONE token's int32 entry -> the scalar LUT
 //                 of T-MAC (each token its own table, N lookups per index,
 //                 P:84-85).  TPW = 2: a word packs two tokens as
 //                 biased 16-bit fields (field = T + 128 g, as K1) -> a 1->2
 //                 vector lookup (the Vec-LUT paradigm) at 2 B of
 //                 shared memory per lookup-add, K1's roofline.
+//   staging (a2)  a producer warp streams each K-tile's 16-byte index rows of
+//                 the CTA (one contiguous block of the packed payload) and its
+//                 activation rows A[16g][N] (contiguous: token axis innermost)
+//                 into a 2-4 stage ring with cp.async.bulk + one mbarrier per
+//                 stage, so HBM stays busy at N = 1 (bandwidth-bound) and the
+//                 builders never wait on global-memory latency.
 //   build (a3)    builder lanes own a slot: lane l computes ALL 3^g entries of
-//                 group l & 15 along the base-3 reflected Gray code (one add
-//                 per entry, the topological order of P:503-513) and stores
-//                 one 128-byte wavefront per entry and word.  Full tables (no
-//                 sign decode on the lookup path).
-//   index tiles   a producer warp streams each K-tile's 16-byte index rows of
-//                 the CTA (one contiguous block of the packed payload) into a
-//                 3-4 stage ring with cp.async.bulk + mbarriers, so HBM stays
-//                 busy at N = 1 where the kernel is bandwidth-bound.
+//                 group l & 15 in the topological order of P:503-513 (one add
+//                 per entry), as 9 independent base-3 reflected Gray-code
+//                 chains (one per value of the two top trits) for ILP, and
+//                 stores one 128-byte wavefront per entry and word.  Full
+//                 tables: no sign decode on the lookup path.
 //   accumulate    TPW = 1: int32 registers.  TPW = 2: SWAR fields widened into
 //                 int32 registers every 48 groups (INT16 -> INT32).
-//   split-K (a5)  CTAs of one (M-block, N-tile) split its K-tiles; with S > 1
-//                 their int32 partials meet in a zero-kept workspace through
-//                 red.global.add, and the last CTA to arrive (acq_rel counter)
-//                 applies the epilogue, then re-zeroes the workspace and the
-//                 counter.  Integer addition is associative: bit-exact for
-//                 every split.
+//   split-K (a5)  CTAs of one (M-block, N-tile) split its K-tiles.  The CTA's
+//                 int32 tile goes through shared memory; with S > 1 it is
+//                 added into a zero-kept workspace by bulk reduce-add copies
+//                 (cp.reduce.async.bulk .add.s32: one per CTA when its rows
+//                 are contiguous there), the CTAs of the tile meet at an
+//                 acq_rel arrival counter (co-resident: cooperative launch),
+//                 and each finishes 1/S of the tile's elements (epilogue +
+//                 re-zeroing), so no single CTA serialises the epilogue.
+//                 Integer addition is associative: bit-exact for every split.
 //   epilogue (a6) out = fl((float)acc * fl(a_scale[n] * w_scale)), or raw int32.
 //
 // Citations: P:n = /root/reference/PAPER.md line n.  DESIGN.md §4 (K2) gives
@@ -46,17 +53,21 @@
 #include <type_traits>
 
 #include "vlut_kernel.cuh"
+#include "vlut_kernel_sk.cuh"
 
 namespace vlut {
 namespace slot {
 
 constexpr int kLW = 16;                           // lookup warps
 constexpr int kBW = 2;                            // builder warps
+constexpr int kLookupThreads = kLW * 32;
 constexpr int kThreads = (kLW + kBW + 1) * 32;    // + 1 producer warp = 608
 constexpr int kRowStride = 256;                   // bytes per table index row
 constexpr int kSmemMax = 232448;                  // 227 KB opt-in per CTA
 constexpr int kFlushTiles = 3;                    // TPW = 2: widen every 48 groups
-constexpr int kMaxCounters = 16384;               // split-K tile counters in the workspace
+constexpr int kMaxCounters = 8192;                // split-K tiles (2 counters each) in the workspace
+constexpr int kActNMax = 64;                      // activations staged by TMA when N <= 64
+constexpr int kMaxStages = 8;                     // staging ring depth (bytes in flight at N = 1)
 
 template <int G, int NW, int TPW>
 struct SL {
@@ -68,18 +79,20 @@ struct SL {
   static constexpr int NWP = (NW + 1) / 2;        // 256-B row blocks (word pairs)
   static constexpr int TAB_BYTES = NWP * R * kRowStride;
   static constexpr int IDX_BYTES = MCTA * 16;
-  static constexpr int FIXED = 2 * TAB_BYTES + 1024;
-  static constexpr int ST_FIT = (kSmemMax - FIXED) / IDX_BYTES;
-  static constexpr int STAGES = ST_FIT < 4 ? ST_FIT : 4;
+  static constexpr int ACT_BYTES = kKgTile * G * kActNMax;  // one K-tile of A, N <= 64
+  static constexpr int FIXED = 2 * TAB_BYTES + 32 + 16 * kMaxStages + 16;
+  static constexpr int ST_FIT = (kSmemMax - FIXED) / (IDX_BYTES + ACT_BYTES);
+  static constexpr int STAGES = ST_FIT < kMaxStages ? ST_FIT : kMaxStages;
   static constexpr int IDX_OFF = 2 * TAB_BYTES;
-  static constexpr int MBAR_OFF = IDX_OFF + STAGES * IDX_BYTES;  // FULL[2] EMPTY[2] STG[4] IFREE[4]
-  static constexpr int MISC_OFF = MBAR_OFF + 96;
+  static constexpr int ACT_OFF = IDX_OFF + STAGES * IDX_BYTES;
+  static constexpr int MBAR_OFF = ACT_OFF + STAGES * ACT_BYTES;  // FULL[2] EMPTY[2] STG[S] IFREE[S]
+  static constexpr int MISC_OFF = MBAR_OFF + 32 + 16 * kMaxStages;
   static constexpr int SMEM = MISC_OFF + 16;
   static constexpr int BIAS = (TPW == 2) ? 128 * G : 0;
-  static constexpr int WPB = (NW + kBW - 1) / kBW;  // words per builder warp
   static_assert(TPW == 1 || TPW == 2, "1 or 2 tokens per table word");
-  static_assert(STAGES >= 2, "index ring needs two stages");
+  static_assert(STAGES >= 2, "staging ring needs two stages");
   static_assert(SMEM <= kSmemMax, "shared memory budget");
+  static_assert(MCTA * NTOK * 4 <= 2 * TAB_BYTES, "int32 tile must fit the table region");
   static_assert(TPW == 1 || kFlushTiles * kKgTile * 2 * BIAS <= 65535, "SWAR field overflow");
 };
 
@@ -93,8 +106,9 @@ struct SlotParams {
   int m_pad, kg_tiles;
   int splits;              // CTAs per (M-block, N-tile) along K (grid.x)
   int acc_only;
+  int act_tma;             // 1: A is staged by bulk copies (N <= 64, 16-B aligned A)
   int32_t* ws_acc;         // splits > 1: int32 [M][N], all zero between launches
-  unsigned* ws_cnt;        // splits > 1: per-tile arrival counters, zero between launches
+  unsigned* ws_cnt;        // splits > 1: per-tile (arrived, done) counters, zero between launches
 };
 
 __device__ __forceinline__ void red_add_s32(int32_t* p, int32_t v) {
@@ -105,51 +119,95 @@ __device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
 }
+__device__ __forceinline__ void bulk_red_add_s32(int32_t* dst, uint32_t src_s, uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.s32 [%0], [%1], %2;\n" ::"l"(dst),
+               "r"(src_s), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_wait_all() {
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];\n" : "=r"(v) : "r"(addr));
+  return v;
+}
 
-// Gray walk over all 3^G entries from entry 0 (all trits -1) with packed
-// deltas P[r] (+a_r) / Mn[r] (-a_r); entry i stored at row_addr + i * 256.
-template <int G>
-__device__ __forceinline__ void walk_full(uint32_t row_addr, uint32_t T, const uint32_t (&P)[8],
-                                          const uint32_t (&Mn)[8]) {
-  constexpr GrayWalk<G> gw{};
+// Activation bytes of K-tile kt that the producer stages (rows [k0, k0+16g)
+// of A, full N-wide rows, clipped to K and rounded down to 16 B; the rest of
+// a ragged last tile is read from global memory by the builders).
+__device__ __forceinline__ int act_tile_bytes(const SlotParams& p, int kt, int G) {
+  const int k0 = kt * kKgTile * G;
+  const int rows = min(kKgTile * G, p.K - k0);
+  return (rows * p.N) & ~15;
+}
+
+// Builder chain: all entries whose two top trits are fixed by prefix PF
+// (d_{G-2} = PF % 3, d_{G-1} = PF / 3), the lower G-2 trits walked along the
+// base-3 reflected Gray code from all -1.  T enters as the entry with the
+// lower digits at 0.
+// Plain C++ stores (not volatile asm) so the compiler interleaves the nine
+// independent chains; the mbarrier arrive (asm volatile, memory clobber)
+// orders them before the lookups.
+template <int G, int PF>
+__device__ __forceinline__ void build_chain(uint8_t* row, uint32_t T, const uint32_t (&P)[8],
+                                            const uint32_t (&Mn)[8]) {
+  constexpr int D = G - 2;
+  constexpr int STRIDE = pow3(D);
+  constexpr GrayWalk<D> gw{};
+  *reinterpret_cast<uint32_t*>(row + (PF * STRIDE) * kRowStride) = T;
 #pragma unroll
-  for (int s = 1; s < pow3(G); ++s) {
+  for (int s = 1; s < pow3(D); ++s) {
     T += (gw.dir[s] > 0) ? P[gw.digit[s]] : Mn[gw.digit[s]];
-    sts32(row_addr + gw.idx[s] * kRowStride, T);
+    *reinterpret_cast<uint32_t*>(row + (gw.idx[s] + PF * STRIDE) * kRowStride) = T;
   }
 }
 
-// Activation values a builder lane needs for one K-tile: group j of the tile,
-// rows r < G, tokens of its words.  Packed per (word, row): TPW = 1 -> the
-// int8 value as int32; TPW = 2 -> (a0 + 128) | (a1 + 128) << 16.
+// Packed per-row activation deltas of one word: TPW = 1 -> (a, -a) as int32;
+// TPW = 2 -> two tokens as arithmetic 16-bit fields (a0 + 65536 a1) and its
+// negation.  base = BIAS (packed) minus the sum of the lower G-2 rows.
 template <int G, int NW, int TPW>
-__device__ __forceinline__ void load_act(const SlotParams& p, int kt, int j, int n0, int bw,
-                                         uint32_t (&U)[SL<G, NW, TPW>::WPB][G]) {
+__device__ __forceinline__ void build_word(uint8_t* row_addr, const uint32_t (&U)[G], int bw,
+                                           bool split_chains) {
   using L = SL<G, NW, TPW>;
+  uint32_t P[8], Mn[8];
+  uint32_t base = (uint32_t)L::BIAS * (TPW == 2 ? 0x00010001u : 1u);
 #pragma unroll
-  for (int wi = 0; wi < L::WPB; ++wi) {
-    const int w = bw + wi * kBW;
-#pragma unroll
-    for (int r = 0; r < G; ++r) {
-      const int k = (kt * kKgTile + j) * G + r;
-      uint32_t u = 0;
-      if (w < NW && k < p.K) {
-        const int8_t* row = p.A + (size_t)k * p.N;
-        if constexpr (TPW == 1) {
-          const int n = n0 + w;
-          u = (n < p.N) ? (uint32_t)(int32_t)__ldg(row + n) : 0u;
-        } else {
-          const int n = n0 + 2 * w;
-          const uint32_t a0 = (n < p.N) ? (uint32_t)((int)__ldg(row + n) + 128) : 128u;
-          const uint32_t a1 = (n + 1 < p.N) ? (uint32_t)((int)__ldg(row + n + 1) + 128) : 128u;
-          u = a0 | (a1 << 16);
-        }
-      } else if constexpr (TPW == 2) {
-        u = 128u | (128u << 16);
-      }
-      U[wi][r] = u;
+  for (int r = 0; r < G; ++r) {
+    if constexpr (TPW == 1) {
+      P[r] = U[r];
+      Mn[r] = 0u - U[r];
+    } else {
+      P[r] = U[r] - 0x00800080u;   // +a as a packed arithmetic delta
+      Mn[r] = 0x00800080u - U[r];  // -a
     }
+    if (r < G - 2) base += Mn[r];  // lower trits all -1
   }
+  const uint32_t c2[3] = {Mn[G - 2], 0u, P[G - 2]};
+  const uint32_t c1[3] = {Mn[G - 1], 0u, P[G - 1]};
+#define VLUT_CHAIN(PF)                                                  \
+  if (!split_chains || ((PF) % kBW) == bw)                              \
+    build_chain<G, PF>(row_addr, base + c2[(PF) % 3] + c1[(PF) / 3], P, Mn);
+  VLUT_CHAIN(0) VLUT_CHAIN(1) VLUT_CHAIN(2) VLUT_CHAIN(3) VLUT_CHAIN(4)
+  VLUT_CHAIN(5) VLUT_CHAIN(6) VLUT_CHAIN(7) VLUT_CHAIN(8)
+#undef VLUT_CHAIN
+}
+
+// One activation value (token n of feature row k) for the builders: staged
+// copy when it landed there, else global memory; 0 outside [K) x [N).
+__device__ __forceinline__ int act_value(const SlotParams& p, uint32_t act_s, int act_bytes,
+                                         int k0, int k, int n) {
+  if (k >= p.K || n >= p.N) return 0;
+  const int e = (k - k0) * p.N + n;
+  if (e < act_bytes) return (int)(int8_t)lds_u8(act_s + e);
+  return (int)__ldg(p.A + (size_t)k * p.N + n);
 }
 
 template <int G, int NW, int TPW>
@@ -166,12 +224,15 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
   const int kt0 = (int)(((long long)rank * p.kg_tiles) / S);
   const int kt1 = (int)(((long long)(rank + 1) * p.kg_tiles) / S);
   const int ntiles = kt1 - kt0;
+  VLUT_STAMP(0);
 
   const uint32_t tab_s = smem_u32(smem);
   const uint32_t idx_s = tab_s + L::IDX_OFF;
+  const uint32_t act_s = tab_s + L::ACT_OFF;
   const uint32_t mbar = tab_s + L::MBAR_OFF;
-  // FULL[b] = mbar + 8b, EMPTY[b] = mbar + 16 + 8b, STG[s] = mbar + 32 + 8s, IFREE[s] = mbar + 64 + 8s
-  volatile unsigned* last_flag = reinterpret_cast<volatile unsigned*>(smem + L::MISC_OFF);
+  constexpr uint32_t IFREE0 = 32 + 8 * kMaxStages;
+  // FULL[b] = mbar + 8b, EMPTY[b] = mbar + 16 + 8b, STG[s] = mbar + 32 + 8s,
+  // IFREE[s] = mbar + 32 + 8 kMaxStages + 8s
 
   if (tid == 0) {
     mbar_init(mbar + 0, kBW);
@@ -180,83 +241,88 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
     mbar_init(mbar + 24, kLW);
     for (int s = 0; s < L::STAGES; ++s) {
       mbar_init(mbar + 32 + 8 * s, 1);
-      mbar_init(mbar + 64 + 8 * s, kLW);
+      mbar_init(mbar + IFREE0 + 8 * s, kLW + kBW);  // ring slot read by lookups and builders
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
-  // per-(row, word, token-in-word) int32 results of the lookup lanes
-  int32_t acc[L::RPL][NW][TPW];
-#pragma unroll
-  for (int q = 0; q < L::RPL; ++q)
-#pragma unroll
-    for (int w = 0; w < NW; ++w)
-#pragma unroll
-      for (int e = 0; e < TPW; ++e) acc[q][w][e] = 0;
-
   if (warp == kLW + kBW) {
-    // =========================== producer: index tiles -> ring (a2)
+    // =========================== producer: index + activation tiles -> ring (a2)
     if (lane == 0 && ntiles > 0) {
       const int rows = min(L::MCTA, p.m_pad - m0);
 #pragma unroll 1
       for (int t = 0; t < ntiles; ++t) {
         const int st = t % L::STAGES, use = t / L::STAGES;
-        if (use > 0) mbar_wait(mbar + 64 + 8 * st, (use - 1) & 1);
-        mbar_expect_tx(mbar + 32 + 8 * st, (uint32_t)(rows * 16));
-        bulk_g2s(idx_s + (uint32_t)(st * L::IDX_BYTES),
-                 p.payload + ((size_t)(kt0 + t) * p.m_pad + m0) * 16, (uint32_t)(rows * 16),
-                 mbar + 32 + 8 * st);
+        const int kt = kt0 + t;
+        if (use > 0) mbar_wait(mbar + IFREE0 + 8 * st, (use - 1) & 1);
+        const int ab = p.act_tma ? act_tile_bytes(p, kt, G) : 0;
+        const uint32_t stg = mbar + 32 + 8 * st;
+        mbar_expect_tx(stg, (uint32_t)(rows * 16 + ab));
+        bulk_g2s(idx_s + (uint32_t)(st * L::IDX_BYTES), p.payload + ((size_t)kt * p.m_pad + m0) * 16,
+                 (uint32_t)(rows * 16), stg);
+        if (t == 0) pdl_wait();  // A is produced by the previous kernel (quantizer)
+        if (ab > 0)
+          bulk_g2s(act_s + (uint32_t)(st * L::ACT_BYTES), p.A + (size_t)kt * kKgTile * G * p.N,
+                   (uint32_t)ab, stg);
       }
     }
   } else if (warp >= kLW) {
     // =========================== builders: full tables (a3)
     const int bw = warp - kLW;
     const int j = lane & 15;
-    pdl_wait();  // A is produced by the previous kernel (quantizer)
-    uint32_t U[L::WPB][G];
-    if (ntiles > 0) load_act<G, NW, TPW>(p, kt0, j, n0, bw, U);
+    pdl_wait();  // the global-memory tail of A comes from the previous kernel
 #pragma unroll 1
     for (int t = 0; t < ntiles; ++t) {
-      const int b = t & 1;
-      uint32_t Un[L::WPB][G];
-      if (t + 1 < ntiles) load_act<G, NW, TPW>(p, kt0 + t + 1, j, n0, bw, Un);
+      const int b = t & 1, st = t % L::STAGES;
+      const int kt = kt0 + t;
+      const int k0 = kt * kKgTile * G;
       if (t >= 2) mbar_wait(mbar + 16 + 8 * b, ((t >> 1) - 1) & 1);  // lookups of t-2 done
+      mbar_wait(mbar + 32 + 8 * st, (t / L::STAGES) & 1);             // tile t staged
+      const int ab = p.act_tma ? act_tile_bytes(p, kt, G) : 0;
+      const uint32_t as = act_s + (uint32_t)(st * L::ACT_BYTES);
+      // activations of this lane's group j for every word it builds
+      constexpr int WPB = (NW + kBW - 1) / kBW;
+      uint32_t U[WPB][G];
 #pragma unroll
-      for (int wi = 0; wi < L::WPB; ++wi) {
-        const int w = bw + wi * kBW;
-        if (w < NW) {
-          uint32_t P[8], Mn[8];
-          uint32_t T = (uint32_t)L::BIAS * (TPW == 2 ? 0x00010001u : 1u);
+      for (int wi = 0; wi < WPB; ++wi) {
+        const int w = (NW == 1) ? 0 : bw + wi * kBW;
 #pragma unroll
-          for (int r = 0; r < G; ++r) {
-            if constexpr (TPW == 1) {
-              P[r] = U[wi][r];
-              Mn[r] = 0u - U[wi][r];
-            } else {
-              P[r] = U[wi][r] - 0x00800080u;   // +a as a packed arithmetic delta
-              Mn[r] = 0x00800080u - U[wi][r];  // -a
-            }
-            T += Mn[r];  // entry 0: every trit -1
+        for (int r = 0; r < G; ++r) {
+          const int k = k0 + j * G + r;
+          if constexpr (TPW == 1) {
+            U[wi][r] = (uint32_t)act_value(p, as, ab, k0, k, n0 + w);
+          } else {
+            const int nn = n0 + 2 * w;
+            U[wi][r] = (uint32_t)(act_value(p, as, ab, k0, k, nn) + 128) |
+                       ((uint32_t)(act_value(p, as, ab, k0, k, nn + 1) + 128) << 16);
           }
-          const uint32_t row = tab_s + (uint32_t)(b * L::TAB_BYTES) +
-                               (uint32_t)((w >> 1) * L::R * kRowStride) + (uint32_t)((w & 1) * 128) +
-                               (uint32_t)(4 * lane);
-          sts32(row, T);
-          walk_full<G>(row, T, P, Mn);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(mbar + IFREE0 + 8 * st);  // done with the ring slot's A rows
+#pragma unroll
+      for (int wi = 0; wi < WPB; ++wi) {
+        const int w = (NW == 1) ? 0 : bw + wi * kBW;
+        if (w < NW) {
+          uint8_t* row = smem + b * L::TAB_BYTES + (w >> 1) * L::R * kRowStride + (w & 1) * 128 +
+                         4 * lane;
+          build_word<G, NW, TPW>(row, U[wi], bw, NW == 1);
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(mbar + 8 * b);  // table t ready
-      if (t + 1 < ntiles) {
-#pragma unroll
-        for (int wi = 0; wi < L::WPB; ++wi)
-#pragma unroll
-          for (int r = 0; r < G; ++r) U[wi][r] = Un[wi][r];
-      }
     }
   } else {
     // =========================== lookup warps (a4)
+    // per-(row, word, token-in-word) int32 results
+    int32_t acc[L::RPL][NW][TPW];
+#pragma unroll
+    for (int q = 0; q < L::RPL; ++q)
+#pragma unroll
+      for (int w = 0; w < NW; ++w)
+#pragma unroll
+        for (int e = 0; e < TPW; ++e) acc[q][w][e] = 0;
     const int x = lane & 15;
     const int qk = x >> 2;
     uint32_t selv[4];
@@ -274,20 +340,22 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
       constexpr int B = decltype(Bc)::value;
       const int st = t % L::STAGES;
       mbar_wait(mbar + 32 + 8 * st, (t / L::STAGES) & 1);  // index rows landed
+      if (t == 0) VLUT_STAMP(1);
       uint4 v[L::RPL];
 #pragma unroll
       for (int q = 0; q < L::RPL; ++q) {
-        const int r = q * (kLW * 32) + warp * 32 + lane;
-        v[q] = (m0 + q * (kLW * 32) + warp * 32 < p.m_pad)
+        const int r = q * kLookupThreads + warp * 32 + lane;
+        v[q] = (m0 + q * kLookupThreads + warp * 32 < p.m_pad)
                    ? *reinterpret_cast<const uint4*>(smem + L::IDX_OFF + st * L::IDX_BYTES + r * 16)
                    : make_uint4(0, 0, 0, 0);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(mbar + 64 + 8 * st);  // ring slot free
+      if (lane == 0) mbar_arrive(mbar + IFREE0 + 8 * st);  // ring slot's index rows consumed
       mbar_wait(mbar + 8 * B, (t >> 1) & 1);           // table t built
+      if (t == 0) VLUT_STAMP(2);
 #pragma unroll
       for (int q = 0; q < L::RPL; ++q) {
-        if (m0 + q * (kLW * 32) + warp * 32 >= p.m_pad) continue;  // warp-uniform
+        if (m0 + q * kLookupThreads + warp * 32 >= p.m_pad) continue;  // warp-uniform
         // Wp[c] = v[c ^ qk]: the word holding group (4c + k) ^ x
         const uint32_t t0 = (qk & 1) ? v[q].y : v[q].x;
         const uint32_t t1 = (qk & 1) ? v[q].x : v[q].y;
@@ -340,64 +408,128 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
           acc[q][w][1] -= bias_total;
         }
     }
+    VLUT_STAMP(3);
+    // int32 tile -> shared memory [row][token] (the table region: every
+    // lookup warp is past its last table read after this barrier)
+    bar_sync(1, kLookupThreads);
+    // dense [row][ld] with ld = min(N, NTOK): for N <= NTOK the CTA's rows are
+    // one contiguous block of the [M][N] output / workspace
+    int32_t* tile_s = reinterpret_cast<int32_t*>(smem);
+    const int ld = min(p.N, L::NTOK);
+#pragma unroll
+    for (int q = 0; q < L::RPL; ++q) {
+      const int r = q * kLookupThreads + warp * 32 + lane;
+      if constexpr (L::NTOK >= 4) {
+        if (ld == L::NTOK) {  // 16-byte vector stores
+#pragma unroll
+          for (int c = 0; c < L::NTOK / 4; ++c) {
+            const int t0 = 4 * c;
+            *reinterpret_cast<int4*>(tile_s + r * L::NTOK + t0) =
+                make_int4(acc[q][t0 / TPW][t0 % TPW], acc[q][(t0 + 1) / TPW][(t0 + 1) % TPW],
+                          acc[q][(t0 + 2) / TPW][(t0 + 2) % TPW],
+                          acc[q][(t0 + 3) / TPW][(t0 + 3) % TPW]);
+          }
+          continue;
+        }
+      }
+#pragma unroll
+      for (int w = 0; w < NW; ++w)
+#pragma unroll
+        for (int e = 0; e < TPW; ++e)
+          if (w * TPW + e < ld) tile_s[r * ld + w * TPW + e] = acc[q][w][e];
+    }
+    fence_proxy_async_smem();  // the tile is read by bulk-reduce copies
     pdl_wait();  // epilogue reads a_scale / the workspace of the previous kernel
   }
   pdl_launch_dependents();
+  __syncthreads();  // int32 tile complete
+  VLUT_STAMP(4);
 
   // =========================== split-K reduction + epilogue (a5, a6)
+  const int rows_valid = min(L::MCTA, p.M - m0);
+  const int ntok_valid = min(L::NTOK, p.N - n0);
+  const int ld = min(p.N, L::NTOK);
+  const int elems = rows_valid * ntok_valid;
+  const int32_t* tile_c = reinterpret_cast<const int32_t*>(smem);
+  int e_begin = 0, e_end = elems;  // the slice of (row, token) elements this CTA finishes
   if (S > 1) {
-    if (warp < kLW) {
-#pragma unroll
-      for (int q = 0; q < L::RPL; ++q) {
-        const int m = m0 + q * (kLW * 32) + warp * 32 + lane;
-        if (m >= p.M) continue;
-#pragma unroll
-        for (int w = 0; w < NW; ++w)
-#pragma unroll
-          for (int e = 0; e < TPW; ++e) {
-            const int n = n0 + w * TPW + e;
-            if (n < p.N) red_add_s32(p.ws_acc + (size_t)m * p.N + n, acc[q][w][e]);
-          }
+    // (1) partial -> zero-kept workspace: one bulk reduce-add when the CTA's
+    // rows are contiguous there (N <= NTOK), one per row when rows are >= 64 B
+    const bool contig = (p.N <= L::NTOK) && ((elems & 3) == 0);
+    const bool rowwise = !contig && (p.N > L::NTOK) && (ntok_valid >= 16) &&
+                         ((ntok_valid & 3) == 0) && ((p.N & 3) == 0);
+    if (contig) {
+      if (tid == 0) {
+        bulk_red_add_s32(p.ws_acc + (size_t)m0 * p.N, tab_s, (uint32_t)(elems * 4));
+        bulk_commit_wait_all();
+      }
+    } else if (rowwise) {
+      if (warp < kLW) {
+        for (int r = tid; r < rows_valid; r += kLookupThreads)
+          bulk_red_add_s32(p.ws_acc + (size_t)(m0 + r) * p.N + n0, tab_s + (uint32_t)(r * ld * 4),
+                           (uint32_t)(ntok_valid * 4));
+        bulk_commit_wait_all();
+      }
+    } else if (warp < kLW) {
+#pragma unroll 4
+      for (int e = tid; e < elems; e += kLookupThreads) {
+        const int r = e / ntok_valid, c = e - r * ntok_valid;
+        red_add_s32(p.ws_acc + (size_t)(m0 + r) * p.N + n0 + c, tile_c[r * ld + c]);
       }
     }
-    __threadfence();
+    fence_proxy_async_global();
+    __syncthreads();
+    // (2) arrive, then wait for the tile's S CTAs (co-resident: cooperative
+    // launch).  Bounded spin: a schedule bug must fail loudly, never hang.
+    unsigned* cnt = p.ws_cnt + 2 * (blockIdx.z * gridDim.y + blockIdx.y);
+    if (tid == 0) {
+      __threadfence();  // cumulative: every reduction of this CTA precedes the arrival
+      atom_add_acq_rel(cnt, 1u);
+      unsigned spins = 0;
+      while (ld_acquire_gpu(cnt) < (unsigned)S) {
+        __nanosleep(32);
+        if (++spins > (1u << 26)) __trap();
+      }
+    }
+    __syncthreads();
+    VLUT_STAMP(5);
+    // (3) this CTA finishes elements [e_begin, e_end) of the tile
+    e_begin = (int)(((long long)elems * rank) / S);
+    e_end = (int)(((long long)elems * (rank + 1)) / S);
+  }
+  if (warp < kLW) {
+#pragma unroll 4
+    for (int e = e_begin + tid; e < e_end; e += kLookupThreads) {
+      const int r = e / ntok_valid, c = e - r * ntok_valid;
+      const size_t o = (size_t)(m0 + r) * p.N + n0 + c;
+      int32_t a;
+      if (S > 1) {
+        a = __ldcg(p.ws_acc + o);
+        __stcg(p.ws_acc + o, 0);  // keep the workspace zero for the next launch
+      } else {
+        a = tile_c[r * ld + c];
+      }
+      if (p.acc_only) {
+        reinterpret_cast<int32_t*>(p.out)[o] = a;
+      } else {
+        const float sc = __fmul_rn(__ldg(p.a_scale + n0 + c), p.w_scale);
+        reinterpret_cast<float*>(p.out)[o] = __fmul_rn((float)a, sc);
+      }
+    }
+  }
+  if (S > 1) {
+    // (4) the last CTA through re-arms both counters for the next launch
+    // (every CTA of the tile has passed its wait by then)
     __syncthreads();
     if (tid == 0) {
-      unsigned* cnt = p.ws_cnt + (blockIdx.z * gridDim.y + blockIdx.y);
-      const unsigned prev = atom_add_acq_rel(cnt, 1u);
-      const bool last = (prev == (unsigned)(S - 1));
-      if (last) *cnt = 0u;  // every CTA of the tile has arrived: re-arm for the next launch
-      *last_flag = last ? 1u : 0u;
-    }
-    __syncthreads();
-    if (*last_flag == 0u) return;
-    __threadfence();
-  }
-  if (warp >= kLW) return;
-#pragma unroll
-  for (int q = 0; q < L::RPL; ++q) {
-    const int m = m0 + q * (kLW * 32) + warp * 32 + lane;
-    if (m >= p.M) continue;
-#pragma unroll
-    for (int w = 0; w < NW; ++w)
-#pragma unroll
-      for (int e = 0; e < TPW; ++e) {
-        const int n = n0 + w * TPW + e;
-        if (n >= p.N) continue;
-        int32_t a = acc[q][w][e];
-        if (S > 1) {
-          int32_t* src = p.ws_acc + (size_t)m * p.N + n;
-          a = __ldcg(src);
-          __stcg(src, 0);  // keep the workspace zero for the next launch
-        }
-        if (p.acc_only) {
-          reinterpret_cast<int32_t*>(p.out)[(size_t)m * p.N + n] = a;
-        } else {
-          const float sc = __fmul_rn(__ldg(p.a_scale + n), p.w_scale);
-          reinterpret_cast<float*>(p.out)[(size_t)m * p.N + n] = __fmul_rn((float)a, sc);
-        }
+      unsigned* cnt = p.ws_cnt + 2 * (blockIdx.z * gridDim.y + blockIdx.y);
+      if (atom_add_acq_rel(cnt + 1, 1u) == (unsigned)(S - 1)) {
+        cnt[0] = 0u;
+        cnt[1] = 0u;
       }
+    }
   }
+  VLUT_STAMP(6);
 }
 
 }  // namespace slot
