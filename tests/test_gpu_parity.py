@@ -379,3 +379,25 @@ def test_config5_chain_fused_equals_unfused(v):
     b_q, b_s = LayerChain(layers, fused=True)(xq, xs)
     torch.cuda.synchronize()
     assert torch.equal(a_q, b_q) and torch.equal(a_s.view(torch.int32), b_s.view(torch.int32))
+
+
+# ------------------------------------------------------------------ host pipeline (e2e path)
+def test_host_pipeline_matches_oracle(v):
+    """bench.py's e2e path: pinned fp32 inputs -> HostPipeline (H2D, quantize,
+    mpGeMM, D2H on three streams, 2 slots) -> pinned outputs; every step's
+    download equals the oracle (different inputs per step catch slot races)."""
+    from paper_2512_06443_b200.pipeline import HostPipeline
+    M, K, N, g = 700, 1280, 96, 4
+    W = synth.ternary_weights(M, K, seed=71)
+    pw = v.pack_weights(W, g, device=dev())
+    steps = 6
+    xs = [synth.activations_f32(K, N, seed=80 + i) for i in range(steps)]
+    x_pins = [torch.from_numpy(x).pin_memory() for x in xs]
+    o_pins = [torch.empty((M, N), dtype=torch.float32).pin_memory() for _ in range(steps)]
+    pipe = HostPipeline(pw, synth.W_SCALE, K, N, dev(), depth=2)
+    for i in range(steps):
+        pipe.submit(x_pins[i], o_pins[i])
+    pipe.synchronize()
+    for i in range(steps):
+        q, s = oracle.quantize(xs[i])
+        check_fp32(o_pins[i].numpy(), oracle.gemm_i32(W, q), s, synth.W_SCALE)
