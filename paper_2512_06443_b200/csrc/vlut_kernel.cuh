@@ -447,12 +447,43 @@ __device__ __forceinline__ void build_tables(uint32_t tab_s, uint32_t a_s, int g
 }
 
 // ---------------------------------------------------------------- lookups (a4)
+template <int WARPS>
+constexpr int kLookupGP = (WARPS >= 16) ? 1 : 2;
+
 // Groups [SUB*GS, SUB*GS+GS) of the K-tile whose index vector is iwa.
-template <int G>
+// GP = groups per load batch: 2 (16 LDS.128 in flight, half the negations on
+// the ALU pipe as XOR, half on the FMA pipe as multiply) or 1 (8 in flight,
+// every negation a multiply: 32 fewer live registers, for the 16-warp
+// variants whose 102-register budget would otherwise spill).
+template <int G, int GP = 2>
 __device__ __forceinline__ void lookup_sub(const int SUB, uint32_t tab, const uint32_t (&iwa)[4],
                                            const uint32_t (&rot)[8], uint32_t (&sw)[8][4],
                                            int32_t& nneg) {
   using C = Cfg<G>;
+  if constexpr (GP == 1) {
+#pragma unroll
+    for (int j = 0; j < C::GS; ++j) {
+      const int b = SUB * C::GS + j;
+      const int i = (int)((iwa[b >> 2] >> (8 * (b & 3))) & C::IDX_MASK);
+      const int d = i - C::ZERO;
+      const uint32_t m = (uint32_t)(d >> 31);
+      const uint32_t pos = (uint32_t)((d ^ (int)m) - (int)m);
+      nneg += (int)m;
+      const uint32_t sg = m | 1u;
+      const uint32_t r = tab + (uint32_t)(j * C::HR * kRowBytes) + pos * kRowBytes;
+      uint4 v[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) v[s] = lds128(r + rot[s]);
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        sw[s][0] += v[s].x * sg;
+        sw[s][1] += v[s].y * sg;
+        sw[s][2] += v[s].z * sg;
+        sw[s][3] += v[s].w * sg;
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int jp = 0; jp < C::GS / 2; ++jp) {
     const int b0 = SUB * C::GS + 2 * jp, b1 = b0 + 1;  // index bytes in the K-tile
@@ -494,7 +525,7 @@ __device__ __forceinline__ void lookup_sub(const int SUB, uint32_t tab, const ui
 // instead of the packed 2*BIAS - field; add the difference back per negation
 // before splitting the fields.  TMEM column 8*s + t of this thread's lane
 // holds token slot (s, t); `first` initialises instead of accumulating.
-template <int G>
+template <int G, bool ALL_MUL = false>
 __device__ __forceinline__ void flush_tmem(uint32_t (&sw)[8][4], int32_t& nneg, uint32_t taddr,
                                            bool first) {
   constexpr uint32_t K1 = 0x00010001u;
@@ -516,7 +547,7 @@ __device__ __forceinline__ void flush_tmem(uint32_t (&sw)[8][4], int32_t& nneg, 
       const int s = 2 * h + e;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const uint32_t w = sw[s][q] + (s < 4 ? corr_xor : corr_mul);
+        const uint32_t w = sw[s][q] + ((s < 4 && !ALL_MUL) ? corr_xor : corr_mul);
         v[8 * e + 2 * q] += w & 0xFFFFu;
         v[8 * e + 2 * q + 1] += w >> 16;
         sw[s][q] = 0;
@@ -671,13 +702,14 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
           const uint4 iw = lds128(idx_s + (t % kStageBufs) * L::IDX_BYTES + tid * 16);
           iwa[0] = iw.x; iwa[1] = iw.y; iwa[2] = iw.z; iwa[3] = iw.w;
         }
-        lookup_sub<G>(sub, tab_s + (uint32_t)((u & 1) * C::TAB_BYTES), iwa, rot, sw, nneg);
+        lookup_sub<G, kLookupGP<WARPS>>(sub, tab_s + (uint32_t)((u & 1) * C::TAB_BYTES), iwa, rot, sw,
+                                        nneg);
         __syncwarp();
         if (lane == 0) mbar_arrive(mbar + 16 + 8 * (u & 1));  // table buffer u & 1 free
       }
       if (++since_flush >= kFlushTiles || t + 1 == ntiles) {
         since_flush = 0;
-        flush_tmem<G>(sw, nneg, taddr, first);
+        flush_tmem<G, kLookupGP<WARPS> == 1>(sw, nneg, taddr, first);
         first = false;
       }
     }

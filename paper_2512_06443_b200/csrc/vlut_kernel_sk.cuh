@@ -430,14 +430,15 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
           const uint4 iw = lds128(idx_s + (t % kStageBufs) * L::IDX_BYTES + tid * 16);
           iwa[0] = iw.x; iwa[1] = iw.y; iwa[2] = iw.z; iwa[3] = iw.w;
         }
-        lookup_sub<G>(sub, tab_s + (uint32_t)((u & 1) * C::TAB_BYTES), iwa, rot, sw, nneg);
+        lookup_sub<G, kLookupGP<WARPS>>(sub, tab_s + (uint32_t)((u & 1) * C::TAB_BYTES), iwa, rot, sw,
+                                        nneg);
         __syncwarp();
         if (lane == 0) mbar_arrive(mbar + 16 + 8 * (u & 1));
       }
       const bool seg_end = (cur.kt + 1 == cur.seg.kb);
       if (++since_flush >= kFlushTiles || seg_end) {
         since_flush = 0;
-        flush_tmem<G>(sw, nneg, taddr, first);
+        flush_tmem<G, kLookupGP<WARPS> == 1>(sw, nneg, taddr, first);
         first = false;
       }
       if (seg_end) {

@@ -60,3 +60,4 @@ for name, fn in (("k3_only", lambda: v.quantize(x, q=q, scale=s, stream=st)),
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     print(name, "us mean %.2f med %.2f" % (np.mean(ts) * 1e3, np.median(ts) * 1e3))
+
