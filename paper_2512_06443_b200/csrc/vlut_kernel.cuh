@@ -803,113 +803,119 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
       const int r = r_begin + (e >> 4);
       return r * 16 + ((e & 15) ^ ((r >> 2) & 1));
     };
-    int4 acc4[L::EPI_UNITS];
+    // chunks of CH units per thread (all loads of a chunk first): the
+    // 16-warp variants' 13 units x 2 int4 arrays would not fit 102 registers
+    constexpr int CH = (WARPS >= 16) ? 4 : L::EPI_UNITS;
+    float tok_max[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+    for (int c0 = 0; c0 < L::EPI_UNITS; c0 += CH) {
+      int4 acc4[CH];
 #pragma unroll
-    for (int i = 0; i < L::EPI_UNITS; ++i) {
-      const int e = tid + i * L::THREADS;
-      acc4[i] = make_int4(0, 0, 0, 0);
-      if (e < units) acc4[i] = red_local[tile_off(e)];
-    }
-    {
-      for (int q = 1; q < S; ++q) {
-        const int4* rem = cluster.map_shared_rank(red_local, (rank + q) % S);
-        int4 w4[L::EPI_UNITS];
+      for (int i = 0; i < CH; ++i) {
+        const int e = tid + (c0 + i) * L::THREADS;
+        acc4[i] = make_int4(0, 0, 0, 0);
+        if (e < units) acc4[i] = red_local[tile_off(e)];
+      }
+      {
+        for (int q = 1; q < S; ++q) {
+          const int4* rem = cluster.map_shared_rank(red_local, (rank + q) % S);
+          int4 w4[CH];
 #pragma unroll
-        for (int i = 0; i < L::EPI_UNITS; ++i) {
-          const int e = tid + i * L::THREADS;
-          w4[i] = make_int4(0, 0, 0, 0);
-          if (e < units) w4[i] = rem[tile_off(e)];
-        }
+          for (int i = 0; i < CH; ++i) {
+            const int e = tid + (c0 + i) * L::THREADS;
+            w4[i] = make_int4(0, 0, 0, 0);
+            if (e < units) w4[i] = rem[tile_off(e)];
+          }
 #pragma unroll
-        for (int i = 0; i < L::EPI_UNITS; ++i) {
-          acc4[i].x += w4[i].x; acc4[i].y += w4[i].y; acc4[i].z += w4[i].z; acc4[i].w += w4[i].w;
+          for (int i = 0; i < CH; ++i) {
+            acc4[i].x += w4[i].x; acc4[i].y += w4[i].y; acc4[i].z += w4[i].z; acc4[i].w += w4[i].w;
+          }
         }
       }
-      // remote reads done: arrive now, wait only before exit (the peers keep
-      // their shared memory until every CTA of the cluster has read it)
-      if (S > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
-    }
-    VLUT_STAMP(6);
-    float tok_max[4] = {0.f, 0.f, 0.f, 0.f};
-    if (p.out_t) {
-      // fused output transposition: out[n][m .. m+3], one token scale
+      if (p.out_t) {
+        // fused output transposition: out[n][m .. m+3], one token scale
 #pragma unroll
-      for (int i = 0; i < L::EPI_UNITS; ++i) {
-        const int e = tid + i * L::THREADS;
+        for (int i = 0; i < CH; ++i) {
+          const int e = tid + (c0 + i) * L::THREADS;
+          if (e >= units) continue;
+          const int nl = e / rq;
+          const int n = n0 + nl;
+          const int m = m0 + r_begin + 4 * (e % rq);
+          if (n >= p.N || m >= p.M) continue;
+          const int4 vv4 = acc4[i];
+          const int vv[4] = {vv4.x, vv4.y, vv4.z, vv4.w};
+          if constexpr (ACC_ONLY) {
+            int32_t* o = reinterpret_cast<int32_t*>(p.out) + (size_t)n * p.M + m;
+            if (p.out_vec4 && m + 3 < p.M) *reinterpret_cast<int4*>(o) = vv4;
+            else for (int k = 0; k < 4 && m + k < p.M; ++k) o[k] = vv[k];
+          } else {
+            float* o = p.out + (size_t)n * p.M + m;
+            const float sc = scale_s[nl];
+            float f[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) f[k] = __fmul_rn((float)vv[k], sc);
+            if (p.out_vec4 && m + 3 < p.M) *reinterpret_cast<float4*>(o) = make_float4(f[0], f[1], f[2], f[3]);
+            else for (int k = 0; k < 4 && m + k < p.M; ++k) o[k] = f[k];
+          }
+        }
+      } else
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {
+        const int e = tid + (c0 + i) * L::THREADS;
         if (e >= units) continue;
-        const int nl = e / rq;
-        const int n = n0 + nl;
-        const int m = m0 + r_begin + 4 * (e % rq);
-        if (n >= p.N || m >= p.M) continue;
-        const int4 vv4 = acc4[i];
-        const int vv[4] = {vv4.x, vv4.y, vv4.z, vv4.w};
+        const int u = e & 15;  // == tid & 15 (THREADS is a multiple of 16)
+        const int m = m0 + r_begin + (e >> 4);
+        const int n = n0 + 4 * u;
+        if (m >= p.M || n >= p.N) continue;
+        int4 vv4 = acc4[i];
+        if (p.acc_in) {  // chained K ranges (mixed g=5/g=4 schedule): add the prior partial
+          const int32_t* src = p.acc_in + (size_t)m * p.N + n;
+          if (p.out_vec4 && n + 3 < p.N) {
+            const int4 w = __ldcg(reinterpret_cast<const int4*>(src));
+            vv4.x += w.x; vv4.y += w.y; vv4.z += w.z; vv4.w += w.w;
+          } else {
+            int t4[4] = {0, 0, 0, 0};
+            for (int k = 0; k < 4 && n + k < p.N; ++k) t4[k] = __ldcg(src + k);
+            vv4.x += t4[0]; vv4.y += t4[1]; vv4.z += t4[2]; vv4.w += t4[3];
+          }
+        }
         if constexpr (ACC_ONLY) {
-          int32_t* o = reinterpret_cast<int32_t*>(p.out) + (size_t)n * p.M + m;
-          if (p.out_vec4 && m + 3 < p.M) *reinterpret_cast<int4*>(o) = vv4;
-          else for (int k = 0; k < 4 && m + k < p.M; ++k) o[k] = vv[k];
+          int32_t* o = reinterpret_cast<int32_t*>(p.out) + (size_t)m * p.N + n;
+          if (p.out_vec4 && n + 3 < p.N) {
+            *reinterpret_cast<int4*>(o) = vv4;
+          } else {
+            const int vv[4] = {vv4.x, vv4.y, vv4.z, vv4.w};
+            for (int k = 0; k < 4 && n + k < p.N; ++k) o[k] = vv[k];
+          }
         } else {
-          float* o = p.out + (size_t)n * p.M + m;
-          const float sc = scale_s[nl];
+          float* o = p.out + (size_t)m * p.N + n;
+          const int vv[4] = {vv4.x, vv4.y, vv4.z, vv4.w};
           float f[4];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) f[k] = __fmul_rn((float)vv[k], sc);
-          if (p.out_vec4 && m + 3 < p.M) *reinterpret_cast<float4*>(o) = make_float4(f[0], f[1], f[2], f[3]);
-          else for (int k = 0; k < 4 && m + k < p.M; ++k) o[k] = f[k];
-        }
-      }
-    } else
+          for (int k = 0; k < 4; ++k) f[k] = __fmul_rn((float)vv[k], scale_s[4 * u + k]);
+          if (p.mul_in) {  // fused element-wise product (config 5: h = gate (.) up)
+            const float* mi = p.mul_in + (size_t)m * p.N + n;
 #pragma unroll
-    for (int i = 0; i < L::EPI_UNITS; ++i) {
-      const int e = tid + i * L::THREADS;
-      if (e >= units) continue;
-      const int u = e & 15;  // == tid & 15 (THREADS is a multiple of 16)
-      const int m = m0 + r_begin + (e >> 4);
-      const int n = n0 + 4 * u;
-      if (m >= p.M || n >= p.N) continue;
-      int4 vv4 = acc4[i];
-      if (p.acc_in) {  // chained K ranges (mixed g=5/g=4 schedule): add the prior partial
-        const int32_t* src = p.acc_in + (size_t)m * p.N + n;
-        if (p.out_vec4 && n + 3 < p.N) {
-          const int4 w = __ldcg(reinterpret_cast<const int4*>(src));
-          vv4.x += w.x; vv4.y += w.y; vv4.z += w.z; vv4.w += w.w;
-        } else {
-          int t4[4] = {0, 0, 0, 0};
-          for (int k = 0; k < 4 && n + k < p.N; ++k) t4[k] = __ldcg(src + k);
-          vv4.x += t4[0]; vv4.y += t4[1]; vv4.z += t4[2]; vv4.w += t4[3];
-        }
-      }
-      if constexpr (ACC_ONLY) {
-        int32_t* o = reinterpret_cast<int32_t*>(p.out) + (size_t)m * p.N + n;
-        if (p.out_vec4 && n + 3 < p.N) {
-          *reinterpret_cast<int4*>(o) = vv4;
-        } else {
-          const int vv[4] = {vv4.x, vv4.y, vv4.z, vv4.w};
-          for (int k = 0; k < 4 && n + k < p.N; ++k) o[k] = vv[k];
-        }
-      } else {
-        float* o = p.out + (size_t)m * p.N + n;
-        const int vv[4] = {vv4.x, vv4.y, vv4.z, vv4.w};
-        float f[4];
+            for (int k = 0; k < 4; ++k)
+              if (n + k < p.N) f[k] = __fmul_rn(f[k], __ldg(mi + k));
+          }
+          if (p.amax_out && m < p.amax_rows) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) f[k] = __fmul_rn((float)vv[k], scale_s[4 * u + k]);
-        if (p.mul_in) {  // fused element-wise product (config 5: h = gate (.) up)
-          const float* mi = p.mul_in + (size_t)m * p.N + n;
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (n + k < p.N) f[k] = __fmul_rn(f[k], __ldg(mi + k));
-        }
-        if (p.amax_out && m < p.amax_rows) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (n + k < p.N) tok_max[k] = fmaxf(tok_max[k], fabsf(f[k]));
-        }
-        if (p.out_vec4 && n + 3 < p.N) {
-          *reinterpret_cast<float4*>(o) = make_float4(f[0], f[1], f[2], f[3]);
-        } else {
-          for (int k = 0; k < 4 && n + k < p.N; ++k) o[k] = f[k];
+            for (int k = 0; k < 4; ++k)
+              if (n + k < p.N) tok_max[k] = fmaxf(tok_max[k], fabsf(f[k]));
+          }
+          if (p.out_vec4 && n + 3 < p.N) {
+            *reinterpret_cast<float4*>(o) = make_float4(f[0], f[1], f[2], f[3]);
+          } else {
+            for (int k = 0; k < 4 && n + k < p.N; ++k) o[k] = f[k];
+          }
         }
       }
     }
+    // remote reads done: arrive now, wait only before exit (the peers keep
+    // their shared memory until every CTA of the cluster has read it)
+    if (S > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+    VLUT_STAMP(6);
     if constexpr (!ACC_ONLY) {
       if (p.amax_out) {
         // fused re-quantization (f1): per-token |out| max of this CTA ->
