@@ -341,6 +341,10 @@ double plan_slot(int M, int K, int N, int g, int sms, int tpw, int nw_force, int
     S = (int)(sms / tiles);  // one wave: split-K CTAs must be co-resident
     if (S < 1) S = 1;
     if (S > kgt) S = kgt;
+    // the makespan is ceil(kgt / S) K-tiles: use the fewest CTAs that reach
+    // it (fewer partial tiles to reduce, no idle tail on the others)
+    const int per = (kgt + S - 1) / S;
+    S = (kgt + per - 1) / per;
   }
   if (S > kgt) S = kgt;
   if (S < 1) S = 1;

@@ -68,6 +68,7 @@ constexpr int kFlushTiles = 3;                    // TPW = 2: widen every 48 gro
 constexpr int kMaxCounters = 8192;                // split-K tiles (2 counters each) in the workspace
 constexpr int kActNMax = 64;                      // activations staged by TMA when N <= 64
 constexpr int kMaxStages = 8;                     // staging ring depth (bytes in flight at N = 1)
+constexpr int kRampStages = 2;                    // stages issued before the first tile lands
 
 template <int G, int NW, int TPW>
 struct SL {
@@ -256,6 +257,9 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
         const int st = t % L::STAGES, use = t / L::STAGES;
         const int kt = kt0 + t;
         if (use > 0) mbar_wait(mbar + IFREE0 + 8 * st, (use - 1) & 1);
+        // ramp: all CTAs start their streams together, so the first tile
+        // lands sooner when only two stages per CTA are in flight until it does
+        if (t == kRampStages) mbar_wait(mbar + 32, 0);
         const int ab = p.act_tma ? act_tile_bytes(p, kt, G) : 0;
         const uint32_t stg = mbar + 32 + 8 * st;
         mbar_expect_tx(stg, (uint32_t)(rows * 16 + ab));
@@ -284,18 +288,55 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
       // activations of this lane's group j for every word it builds
       constexpr int WPB = (NW + kBW - 1) / kBW;
       uint32_t U[WPB][G];
-#pragma unroll
-      for (int wi = 0; wi < WPB; ++wi) {
-        const int w = (NW == 1) ? 0 : bw + wi * kBW;
+      if (ab == kKgTile * G * p.N && p.N % L::NTOK == 0) {
+        // fast path: the whole tile is staged and the CTA's NTOK tokens of a
+        // row are one aligned NTOK-byte vector -> one shared load per row
 #pragma unroll
         for (int r = 0; r < G; ++r) {
-          const int k = k0 + j * G + r;
-          if constexpr (TPW == 1) {
-            U[wi][r] = (uint32_t)act_value(p, as, ab, k0, k, n0 + w);
+          const uint32_t addr = as + (uint32_t)((j * G + r) * p.N + n0);
+          uint32_t by[4] = {0u, 0u, 0u, 0u};
+          if constexpr (L::NTOK == 16) {
+            const uint4 q4 = *reinterpret_cast<const uint4*>(smem + (addr - tab_s));
+            by[0] = q4.x; by[1] = q4.y; by[2] = q4.z; by[3] = q4.w;
+          } else if constexpr (L::NTOK == 8) {
+            const uint2 q2 = *reinterpret_cast<const uint2*>(smem + (addr - tab_s));
+            by[0] = q2.x; by[1] = q2.y;
+          } else if constexpr (L::NTOK == 4) {
+            by[0] = *reinterpret_cast<const uint32_t*>(smem + (addr - tab_s));
+          } else if constexpr (L::NTOK == 2) {
+            by[0] = *reinterpret_cast<const uint16_t*>(smem + (addr - tab_s));
           } else {
-            const int nn = n0 + 2 * w;
-            U[wi][r] = (uint32_t)(act_value(p, as, ab, k0, k, nn) + 128) |
-                       ((uint32_t)(act_value(p, as, ab, k0, k, nn + 1) + 128) << 16);
+            by[0] = *(smem + (addr - tab_s));
+          }
+#pragma unroll
+          for (int wi = 0; wi < WPB; ++wi) {
+            const int w = (NW == 1) ? 0 : bw + wi * kBW;
+            const int t0 = (w * TPW) & 15;  // token of the word's first field (w < NW)
+            const uint32_t src = by[(t0 >> 2) & 3];
+            if constexpr (TPW == 1) {
+              U[wi][r] = (uint32_t)(int32_t)(int8_t)(src >> (8 * (t0 & 3)));
+            } else {
+              // bytes t0, t0+1 (same word: t0 even) -> (a + 128) in 16-bit fields
+              // selector nibbles (b, zero, b+1, zero), b = t0 & 3
+              const uint32_t sel = 0x4140u + ((uint32_t)(t0 & 3) * 0x0101u);
+              U[wi][r] = __byte_perm(src ^ 0x80808080u, 0u, sel);
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int wi = 0; wi < WPB; ++wi) {
+          const int w = (NW == 1) ? 0 : bw + wi * kBW;
+#pragma unroll
+          for (int r = 0; r < G; ++r) {
+            const int k = k0 + j * G + r;
+            if constexpr (TPW == 1) {
+              U[wi][r] = (uint32_t)act_value(p, as, ab, k0, k, n0 + w);
+            } else {
+              const int nn = n0 + 2 * w;
+              U[wi][r] = (uint32_t)(act_value(p, as, ab, k0, k, nn) + 128) |
+                         ((uint32_t)(act_value(p, as, ab, k0, k, nn + 1) + 128) << 16);
+            }
           }
         }
       }
