@@ -96,7 +96,7 @@ class ClockSampler:
                 self.reasons |= int(r)
             except Exception:
                 pass
-            time.sleep(0.0005)
+            time.sleep(0.002)  # sparse: the sampler competes with the launch thread for the GIL
 
     def __enter__(self):
         if self.ok:
@@ -220,7 +220,7 @@ def vlut_launches_per_step(v, plan):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="vlut", choices=["vlut", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
@@ -307,23 +307,28 @@ def main():
             step()
             e[1].record(stream)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        for i in range(args.steps):  # per-kernel pass: each kernel alone
-            # the L2 flush runs on the GPU while the host enqueues the event
-            # and the kernel, so no host submission latency enters a window
-            e = kev[i]
-            flush.zero_()
-            e[0].record(stream)
-            v.quantize(x, q=q, scale=s, stream=stream)
-            e[1].record(stream)
-            flush.zero_()
-            e[2].record(stream)
-            v.mpgemm_ws(pw, q, s, synth.W_SCALE, out=out_r, ws=ws, stream=stream)
-            e[3].record(stream)
-            if world > 1:
-                dist.all_gather_into_tensor(out_full, out_r)
-            torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    # per-kernel passes (outside the clock sampler: no GIL contention), one
+    # loop per kernel: each launch right after its own L2 flush, which runs on
+    # the GPU while the host enqueues the event and the kernel (no host
+    # submission latency in the window).  Separate loops because a preceding
+    # K3 + synchronize measurably slows the next K1 launch (+6 us, idle-gap
+    # effect, scripts/k1_timing_variants.py) -- inside the step, K1 follows
+    # K3 back to back and takes ~step - K3.
+    for i in range(args.steps):
+        e = kev[i]
+        flush.zero_()
+        e[0].record(stream)
+        v.quantize(x, q=q, scale=s, stream=stream)
+        e[1].record(stream)
+        torch.cuda.synchronize()
+    for i in range(args.steps):
+        e = kev[i]
+        flush.zero_()
+        e[2].record(stream)
+        v.mpgemm_ws(pw, q, s, synth.W_SCALE, out=out_r, ws=ws, stream=stream)
+        e[3].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -416,8 +421,8 @@ def main():
         "peak_source": f"derived: {SM_COUNT} SMs x {SMEM_BYTES_PER_CLK_SM} B/clk x "
                        f"{sm_max:.0f} MHz (sm_max_mhz, {peaks_src})",
         "k1_ms_mean": k1_mean, "k3_quantize_ms_mean": float(np.mean(k3_ms)),
-        "kernel_timing": "second pass of the K steps: each kernel alone right after its "
-                         "own L2 flush (events around the kernel only; synchronize per step)",
+        "kernel_timing": "per-kernel passes of K launches each: every launch right after its "
+                         "own L2 flush, CUDA events around the kernel only, synchronize per launch",
         "hbm_achieved_gbs": a_shard["hbm_bytes"] / (k1_mean * 1e-3) / 1e9,
         "hbm_peak_gbs": float(peaks.get("hbm_gbs", HBM_FALLBACK_GBS)),
         "lookups_per_s": a_shard["lookups"] / (k1_mean * 1e-3),
