@@ -223,6 +223,9 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="vlut", choices=["vlut", "reference"])
+    ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1: fused all-gather in the K1 epilogue (NVLink peer stores into "
+                         "symmetric buffers) or mpGeMM + NCCL all_gather_into_tensor")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-sweep", action="store_true", help="skip the config 3/4 sweep")
     ap.add_argument("--no-e2e", action="store_true")
@@ -272,8 +275,37 @@ def main():
     ws = v.workspace(dev)
     plan = v.plan_ws(Ms, K, N, g)
 
+    # N > 1: the all-gather fused into the K1 epilogue (peer stores into
+    # symmetric buffers + one cross-GPU barrier), validated once against the
+    # NCCL path; any failure falls back to NCCL and says why
+    gather = "none" if world == 1 else args.gather
+    peer = None
+    if world > 1 and gather == "p2p":
+        try:
+            from paper_2512_06443_b200.sharded import PeerOutputs
+            peer = PeerOutputs()
+            v.quantize(x, q=q, scale=s, stream=stream)
+            v.mpgemm_ws(pw, q, s, synth.W_SCALE, out=out_r, ws=ws, stream=stream)
+            dist.all_gather_into_tensor(out_full, out_r)
+            for _ in range(2):  # both alternating buffers
+                buf, peers, barrier = peer.get(M, N, dev)
+                v.mpgemm_allgather(pw, q, s, synth.W_SCALE, buf, rank * Ms, peers, stream=stream)
+                barrier()
+                okt = torch.tensor([1 if torch.equal(buf, out_full) else 0], device=dev)
+                dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+                if int(okt.item()) != 1:
+                    raise RuntimeError("fused all-gather result differs from NCCL all-gather")
+        except Exception as ex:  # keep measuring, on the NCCL path
+            gather = f"nccl (p2p unavailable: {str(ex)[:120]})"
+            peer = None
+
     def step():
         v.quantize(x, q=q, scale=s, stream=stream)
+        if peer is not None:
+            buf, peers, barrier = peer.get(M, N, dev)
+            v.mpgemm_allgather(pw, q, s, synth.W_SCALE, buf, rank * Ms, peers, stream=stream)
+            barrier()
+            return
         v.mpgemm_ws(pw, q, s, synth.W_SCALE, out=out_r, ws=ws, stream=stream)
         if world > 1:
             dist.all_gather_into_tensor(out_full, out_r)
@@ -394,7 +426,7 @@ def main():
 
     if rank != 0:
         if not args.no_chain:
-            chain_bench(v, dev, world, rank, args)
+            chain_bench(v, dev, world, rank, args, peer=peer)
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
@@ -440,7 +472,10 @@ def main():
                    "N": N, "g": g, "weights": "iid ternary P(0)=0.4 P(+-1)=0.3, seeded",
                    "activations": "N(0,1) fp32, per-token int8 absmax quantized on GPU",
                    "step": "quantize (K3) + fused Vec-LUT mpGeMM + fp32 dequant (K1)"
-                           + (" + NCCL all-gather of row shards" if world > 1 else ""),
+                           + ((" with the all-gather of row shards fused into the epilogue "
+                               "(NVLink peer stores + cross-GPU barrier)" if peer is not None
+                               else " + NCCL all-gather of row shards") if world > 1 else ""),
+                   "gather": gather,
                    "parallelism": f"row-shard M over {world} GPU(s)" if world > 1 else "single GPU",
                    "plan": plan.__dict__,
                    "l2": "flushed between steps (256 MiB memset outside each step's event window)"},
@@ -459,7 +494,7 @@ def main():
         line["sweep"] = sweep(v, dev, stream, flush)
 
     if not args.no_chain:
-        line["config5"] = chain_bench(v, dev, world, rank, args)
+        line["config5"] = chain_bench(v, dev, world, rank, args, peer=peer)
 
     if world > 1:
         dist.barrier()
@@ -468,7 +503,7 @@ def main():
     return 0
 
 
-def chain_bench(v, dev, world, rank, args, reps=3):
+def chain_bench(v, dev, world, rank, args, reps=3, peer=None):
     """BASELINE.json configs[4]: 30 BitNet-2B-shaped layers of ternary linears
     (QKV, O, gate, up, down), N = 2048 tokens, every linear row-sharded over
     the N GPUs with an NCCL all-gather (north star), int8 re-quantization
@@ -515,10 +550,31 @@ def chain_bench(v, dev, world, rank, args, reps=3):
         torch.cuda.synchronize()
         tf.append(a.elapsed_time(b))
     t_f = float(np.median(tf))
+    # N > 1: every linear's all-gather fused into its K1 epilogue (peer stores)
+    t_p = float("nan")
+    if world > 1 and peer is not None:
+        for lay in layers:
+            for lin in lay:
+                lin.peers = peer
+        chain(xq, xs)
+        torch.cuda.synchronize()
+        dist.barrier()
+        tp = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            chain(xq, xs)
+            b.record()
+            torch.cuda.synchronize()
+            tp.append(a.elapsed_time(b))
+        t_p = float(np.median(tp))
+        for lay in layers:
+            for lin in lay:
+                lin.peers = None
     if world > 1:
-        tt = torch.tensor([t, t_f], device=dev)
+        tt = torch.tensor([t, t_f, t_p], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t, t_f = float(tt[0]), float(tt[1])
+        t, t_f, t_p = float(tt[0]), float(tt[1]), float(tt[2])
     lookups = L * N * sum(lin.M * lin.K // 4 for lin in cfg.linears)
     R_LU = SM_COUNT * 64 * SM_MAX_MHZ_FALLBACK * 1e6
     return {"config": 5, "layers": L, "N": N, "n_gpus": world, "ms_per_forward": t,
@@ -526,6 +582,9 @@ def chain_bench(v, dev, world, rank, args, reps=3):
             "frac_smem_roofline": lookups / (R_LU * world) / (t * 1e-3),
             "fused_requant": {"ms_per_forward": t_f, "tokens_s": N / (t_f * 1e-3),
                               "frac_smem_roofline": lookups / (R_LU * world) / (t_f * 1e-3)},
+            "fused_allgather": ({"ms_per_forward": t_p, "tokens_s": N / (t_p * 1e-3),
+                                 "frac_smem_roofline": lookups / (R_LU * world) / (t_p * 1e-3)}
+                                if t_p == t_p else None),
             "step": "per layer: 5 row-sharded Vec-LUT linears (+ all-gather when n_gpus > 1) "
                     "and 4 int8 re-quantizations; weights packed once before timing; "
                     "fused_requant = f1 (epilogue maxima, int8 all-gathers)"}

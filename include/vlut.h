@@ -284,6 +284,24 @@ vlut_status vlut_quantize_amax(const float* x, const unsigned* amax, int K, int 
                                float* scale, void* stream);
 
 /*
+ * Row-sharded mpGeMM with the all-gather fused into the epilogue (a8, §8e):
+ * this rank computes rows [row0, row0 + M) of an [M_total][N] output (W holds
+ * those M rows) and its K1 epilogue stores every 16-byte output unit to
+ *   out_full + row0*N (local, device)  and  peer_full[i] + row0*N, i < n_peers
+ * -- the other ranks' full output buffers, mapped into this process (CUDA IPC
+ * / symmetric memory; NVLink P2P stores), so the gather overlaps the other
+ * CTAs' compute instead of following the kernel.  The caller orders the
+ * peers' reads after every rank's launch (a cross-GPU barrier on the stream).
+ *   peer_full : host array of n_peers device pointers (each 16-B aligned,
+ *               >= (row0 + M) * N floats); n_peers <= 7 (8 GPUs).
+ * Cluster split-K schedule; plain fp32 epilogue.  Same values as vlut_mpgemm.
+ */
+vlut_status vlut_mpgemm_allgather(const vlut_packed_weights* W, const int8_t* A,
+                                  const float* a_scale, float w_scale, float* out_full, int M,
+                                  int K, int N, int row0, void* const* peer_full, int n_peers,
+                                  void* stream);
+
+/*
  * Per-token absmax int8 quantizer (a7; w1.6A8 named at P:102; formula
  * S:339-347, reading c8), IEEE single precision throughout:
  *   x'[k][n] = x[k][n] * (y ? y[k][n] : 1)      (fp32 multiply, config 5's

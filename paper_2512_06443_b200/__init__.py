@@ -26,7 +26,7 @@ __all__ = [
     "mpgemm_ex", "mpgemm_acc", "quantize", "last_error", "EXPORTS", "group_schedule",
     "MixedPackedWeights", "pack_weights_mixed", "mpgemm_mixed", "mpgemm_layout", "quantize_t",
     "linear", "workspace", "plan_ws", "mpgemm_ws", "mpgemm_acc_ws", "mpgemm_fused",
-    "quantize_amax", "mpgemm_scalar_lut", "slot_plan",
+    "quantize_amax", "mpgemm_scalar_lut", "slot_plan", "mpgemm_allgather",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -129,6 +129,10 @@ EXPORTS = {
                                 ctypes.c_float, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                 ctypes.c_int, ctypes.POINTER(_Plan), ctypes.c_void_p,
                                 ctypes.c_size_t, ctypes.c_void_p], ctypes.c_int),
+    "vlut_mpgemm_allgather": ([ctypes.POINTER(_Desc), ctypes.c_void_p, ctypes.c_void_p,
+                               ctypes.c_float, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                               ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
+                               ctypes.c_int, ctypes.c_void_p], ctypes.c_int),
     "vlut_launches_per_mpgemm": ([], ctypes.c_int),
     "vlut_active_clusters": ([ctypes.c_int, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "vlut_last_error": ([], ctypes.c_char_p),
@@ -550,3 +554,18 @@ def mpgemm_scalar_lut(W: PackedWeights, A, a_scale, w_scale: float, out=None,
                                         float(w_scale), _dev_ptr(out), M, K, N, pp, wsp, wsn,
                                         _stream_ptr(stream)))
     return out
+
+
+# ---------------------------------------------------------------- fused all-gather (a8)
+def mpgemm_allgather(W: PackedWeights, A, a_scale, w_scale: float, out_full, row0: int,
+                     peer_ptrs=(), stream=None):
+    """Shard rows [row0, row0 + W.M) of out_full [M_total][N], stored locally
+    and to every peer buffer in ``peer_ptrs`` (device pointers mapped into
+    this process) by the K1 epilogue.  Returns out_full."""
+    K, N = A.shape
+    arr = (ctypes.c_void_p * max(1, len(peer_ptrs)))(*[ctypes.c_void_p(int(x)) for x in peer_ptrs])
+    _check(lib().vlut_mpgemm_allgather(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(a_scale),
+                                       float(w_scale), _dev_ptr(out_full), W.M, K, N, int(row0),
+                                       ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p)),
+                                       len(peer_ptrs), _stream_ptr(stream)))
+    return out_full

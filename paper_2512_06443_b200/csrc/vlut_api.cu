@@ -19,6 +19,14 @@ namespace {
 
 thread_local std::string g_err;
 
+// Peer destinations of the next launch (vlut_mpgemm_allgather -> run_mpgemm),
+// thread-local so concurrent callers on other threads are unaffected.
+struct PeerTls {
+  int n = 0;
+  float* ptr[vlut::kMaxPeers] = {};
+};
+thread_local PeerTls g_peer_tls;
+
 vlut_status fail(vlut_status st, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -650,6 +658,10 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
     if (st != VLUT_OK) return st;
   }
   p.out_t = out_t;
+  p.n_peers = g_peer_tls.n;
+  for (int i = 0; i < g_peer_tls.n; ++i) p.peer_out[i] = g_peer_tls.ptr[i];
+  if (p.n_peers && (plan.streamk || acc_only || out_t || acc_in))
+    return fail(VLUT_ERR_UNSUPPORTED, "fused all-gather: cluster schedule, fp32 [M][N] output only");
   p.mul_in = mul_in;
   p.amax_out = amax_out;
   p.amax_rows = amax_rows;
@@ -871,6 +883,34 @@ vlut_status vlut_mpgemm_scalar_lut(const vlut_packed_weights* W, const int8_t* A
   pl.tpw = 1;
   return run_mpgemm(W, A, a_scale, w_scale, out, M, K, N, &pl, stream, false, nullptr, 0,
                     workspace, ws_bytes);
+}
+
+vlut_status vlut_mpgemm_allgather(const vlut_packed_weights* W, const int8_t* A,
+                                  const float* a_scale, float w_scale, float* out_full, int M,
+                                  int K, int N, int row0, void* const* peer_full, int n_peers,
+                                  void* stream) {
+  if (n_peers < 0 || n_peers > vlut::kMaxPeers)
+    return fail(VLUT_ERR_INVALID_ARGUMENT, "n_peers must be in [0, %d]", vlut::kMaxPeers);
+  if (!out_full || row0 < 0) return fail(VLUT_ERR_INVALID_ARGUMENT, "bad output / row0");
+  if (n_peers > 0 && !peer_full) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL peer pointer table");
+  for (int i = 0; i < n_peers; ++i)
+    if (!peer_full[i] || (((uintptr_t)peer_full[i]) & 15))
+      return fail(VLUT_ERR_MISALIGNED, "peer buffer %d NULL or not 16-B aligned", i);
+  if (M == 0 || N == 0) return ok();
+  g_peer_tls.n = n_peers;
+  for (int i = 0; i < n_peers; ++i)
+    g_peer_tls.ptr[i] = static_cast<float*>(peer_full[i]) + (size_t)row0 * N;
+  // cluster schedule (its epilogue carries the peer stores)
+  vlut_launch_plan pl = {};
+  DeviceInfo d;
+  vlut_status st = device_info(&d);
+  if (st == VLUT_OK) {
+    plan_for(M, K, N, W ? W->g : 4, d.sms, &pl);
+    st = run_mpgemm(W, A, a_scale, w_scale, out_full + (size_t)row0 * N, M, K, N, &pl, stream,
+                    false);
+  }
+  g_peer_tls.n = 0;
+  return st;
 }
 
 vlut_status vlut_plan_ws(int M, int K, int N, int g, vlut_launch_plan* plan) {

@@ -258,6 +258,8 @@ __device__ __forceinline__ void tmem_fence_after() {
 }
 
 // ---------------------------------------------------------------- params
+constexpr int kMaxPeers = 7;  // 8 GPUs of one NVSwitch box: 7 remote copies
+
 struct alignas(64) Params {
   CUtensorMap a_map;       // 2D TMA map of A [K][N] int8, box 64 x 16g (a_vec == 16)
   const uint8_t* payload;  // packed indices [kt][m_pad][16]
@@ -275,6 +277,11 @@ struct alignas(64) Params {
   const float* mul_in;     // optional fp32 [M][N]: out = fl(out * mul_in) (gate (.) up glue)
   unsigned* amax_out;      // optional [N]: atomicMax of |out| (float bits) over rows < amax_rows
   int amax_rows;
+  // fused all-gather (a8): the fp32 tile is also stored to n_peers remote
+  // copies of the output (peer device pointers, NVLink P2P), each already
+  // offset to this shard's first row, same [M][N] indexing as `out`
+  float* peer_out[kMaxPeers];
+  int n_peers;
 };
 
 // ---------------------------------------------------------------- staging (a2)
@@ -905,9 +912,16 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
               if (n + k < p.N) tok_max[k] = fmaxf(tok_max[k], fabsf(f[k]));
           }
           if (p.out_vec4 && n + 3 < p.N) {
-            *reinterpret_cast<float4*>(o) = make_float4(f[0], f[1], f[2], f[3]);
+            const float4 f4 = make_float4(f[0], f[1], f[2], f[3]);
+            *reinterpret_cast<float4*>(o) = f4;
+            // fused all-gather: the same 16 bytes to every peer's copy (P2P
+            // stores over NVLink, overlapping the other CTAs' compute)
+            for (int pi = 0; pi < p.n_peers; ++pi)
+              *reinterpret_cast<float4*>(p.peer_out[pi] + (size_t)m * p.N + n) = f4;
           } else {
             for (int k = 0; k < 4 && n + k < p.N; ++k) o[k] = f[k];
+            for (int pi = 0; pi < p.n_peers; ++pi)
+              for (int k = 0; k < 4 && n + k < p.N; ++k) p.peer_out[pi][(size_t)m * p.N + n + k] = f[k];
           }
         }
       }

@@ -19,7 +19,7 @@ from typing import Callable, List, Optional, Sequence, Tuple
 
 import numpy as np
 
-__all__ = ["shard_rows", "RowShardedLinear", "LayerChain", "CHAIN_Q_ROWS"]
+__all__ = ["shard_rows", "RowShardedLinear", "LayerChain", "CHAIN_Q_ROWS", "PeerOutputs"]
 
 
 def shard_rows(M: int, world: int, rank: int) -> Tuple[int, int, int]:
@@ -39,6 +39,45 @@ def _dist():
     return None
 
 
+class PeerOutputs:
+    """Symmetric fp32 [M][N] output buffers on every rank for the fused
+    all-gather (``vlut_mpgemm_allgather``): allocated with torch symmetric
+    memory (CUDA IPC mappings; NVLink P2P on one NVSwitch box), so each rank
+    holds device pointers to every peer's buffer and its K1 epilogue stores
+    its row shard into all of them.  Two buffers per N alternate between
+    calls: a rank can only be one call ahead of a peer (every call ends with a
+    cross-GPU barrier on the stream), so it never overwrites a buffer a peer
+    is still reading.  Plumbing only -- the stores are the kernel's."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        self.symm = symm_mem
+        self.group = group or dist.group.WORLD
+        self.rank = dist.get_rank(self.group)
+        self.world = dist.get_world_size(self.group)
+        self._bufs = {}
+        self._turn = {}
+
+    def get(self, M: int, N: int, device):
+        """(buffer [M][N] fp32, [peer device pointers], barrier) for this call."""
+        key = (M, N)
+        if key not in self._bufs:
+            import torch
+            pair = []
+            for _ in range(2):
+                t = self.symm.empty((M, N), dtype=torch.float32, device=device)
+                h = self.symm.rendezvous(t, self.group)
+                peers = [int(h.buffer_ptrs[r]) for r in range(self.world) if r != self.rank]
+                pair.append((t, peers, h))
+            self._bufs[key] = pair
+            self._turn[key] = 0
+        i = self._turn[key]
+        self._turn[key] = 1 - i
+        t, peers, h = self._bufs[key][i]
+        return t, peers, (lambda: h.barrier(channel=0))
+
+
 class RowShardedLinear:
     """One ternary linear, row-sharded over the default process group.
 
@@ -50,7 +89,7 @@ class RowShardedLinear:
     def __init__(self, W, g: int, w_scale: float, device=None,
                  compute: Optional[Callable] = None, pack: Optional[Callable] = None,
                  device_pack: bool = False, fused: Optional[Callable] = None,
-                 quantize_amax: Optional[Callable] = None):
+                 quantize_amax: Optional[Callable] = None, peers: Optional[PeerOutputs] = None):
         dist = _dist()
         self.world = dist.get_world_size() if dist else 1
         self.rank = dist.get_rank() if dist else 0
@@ -76,6 +115,7 @@ class RowShardedLinear:
         else:
             import paper_2512_06443_b200 as v
             self.shard = v.pack_weights(np.ascontiguousarray(W_r), g, device=device)
+        self.peers = peers  # fused all-gather buffers (None: NCCL all_gather_into_tensor)
         self._compute = compute or self._cuda_compute
         self._fused = fused or self._cuda_fused
         if quantize_amax is None:
@@ -149,6 +189,18 @@ class RowShardedLinear:
             if self.rows:
                 self._compute(self.shard, A, a_scale, out)
             return out
+        if self.peers is not None:
+            # fused all-gather: the K1 epilogue stores this rank's rows into
+            # every rank's copy over NVLink; one cross-GPU barrier completes it
+            import paper_2512_06443_b200 as v
+            buf, peer_ptrs, barrier = self.peers.get(self.M, N, dev)
+            if self.rows:
+                v.mpgemm_allgather(self.shard, A, a_scale, self.w_scale, buf, self.r0, peer_ptrs)
+            barrier()
+            if out is not None:
+                out.copy_(buf)
+                return out
+            return buf
         local = torch.empty((self.Mp, N), dtype=torch.float32, device=dev)
         if self.rows:
             self._compute(self.shard, A, a_scale, local[:self.rows])

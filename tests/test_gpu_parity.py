@@ -401,3 +401,73 @@ def test_host_pipeline_matches_oracle(v):
     for i in range(steps):
         q, s = oracle.quantize(xs[i])
         check_fp32(o_pins[i].numpy(), oracle.gemm_i32(W, q), s, synth.W_SCALE)
+
+
+# ------------------------------------------------------------------ fused all-gather epilogue (a8)
+@pytest.mark.parametrize("M,K,N,G", [(6912, 2560, 256, 2), (1000, 1280, 100, 3), (700, 260, 64, 8)])
+def test_mpgemm_allgather_emulated_ranks(v, M, K, N, G):
+    """Single-process emulation of G ranks (no rank waits on another): rank r
+    computes rows [r0, r1) with vlut_mpgemm_allgather into its own buffer and
+    the G-1 'peer' buffers; afterwards every buffer holds the full output,
+    bit-identical to the oracle, and nothing outside the shards was touched."""
+    from paper_2512_06443_b200.sharded import shard_rows
+    W = synth.ternary_weights(M, K, seed=M + G)
+    x = synth.activations_f32(K, N, seed=N + G)
+    q, s = oracle.quantize(x)
+    qd, sd = to_dev(q), to_dev(s)
+    bufs = [torch.full((M + 4, N), float("nan"), device=dev()) for _ in range(G)]
+    for r in range(G):
+        r0, r1, _ = shard_rows(M, G, r)
+        if r1 <= r0:
+            continue
+        pw = v.pack_weights(np.ascontiguousarray(W[r0:r1]), 4, device=dev())
+        peers = [bufs[p].data_ptr() for p in range(G) if p != r]
+        v.mpgemm_allgather(pw, qd, sd, synth.W_SCALE, bufs[r], r0, peers)
+    torch.cuda.synchronize()
+    ref = oracle.gemm_i32(W, q)
+    for b in bufs:
+        got = b.cpu().numpy()
+        check_fp32(got[:M], ref, s, synth.W_SCALE)
+        assert np.isnan(got[M:]).all()
+
+
+def test_mpgemm_allgather_rejects_bad_peers(v):
+    W = synth.ternary_weights(64, 64, seed=1)
+    pw = v.pack_weights(W, 4, device=dev())
+    A = to_dev(synth.int8_activations(64, 8, seed=2))
+    s = to_dev(synth.token_scales(8, seed=3))
+    out = torch.empty((64, 8), device=dev())
+    with pytest.raises(v.VlutError):
+        v.mpgemm_allgather(pw, A, s, 0.02, out, 0, [out.data_ptr() + 4])  # misaligned peer
+    with pytest.raises(v.VlutError):
+        v.mpgemm_allgather(pw, A, s, 0.02, out, 0, [out.data_ptr()] * 8)  # > 7 peers
+
+
+def test_peer_outputs_symmetric_memory_world1(v):
+    """The symmetric-memory plumbing of the fused all-gather on a 1-rank
+    NCCL group: allocation, rendezvous, alternating buffers, barrier."""
+    import os
+    import torch.distributed as dist
+    from paper_2512_06443_b200.sharded import PeerOutputs
+    if dist.is_initialized():
+        pytest.skip("process group already initialised")
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev())
+    try:
+        po = PeerOutputs()
+        b0, peers0, bar0 = po.get(128, 64, dev())
+        b1, peers1, bar1 = po.get(128, 64, dev())
+        b2, _, _ = po.get(128, 64, dev())
+        assert peers0 == [] and peers1 == []
+        assert b0.data_ptr() != b1.data_ptr() and b2.data_ptr() == b0.data_ptr()
+        W = synth.ternary_weights(128, 256, seed=5)
+        x = synth.activations_f32(256, 64, seed=6)
+        q, s = oracle.quantize(x)
+        pw = v.pack_weights(W, 4, device=dev())
+        v.mpgemm_allgather(pw, to_dev(q), to_dev(s), synth.W_SCALE, b0, 0, peers0)
+        bar0()
+        torch.cuda.synchronize()
+        check_fp32(b0.cpu().numpy(), oracle.gemm_i32(W, q), s, synth.W_SCALE)
+    finally:
+        dist.destroy_process_group()
