@@ -8,17 +8,96 @@
 //   mode 3: + TMEM flush every 3 K-tiles
 //   mode 4: + builders stage A and index tiles from HBM with cp.async (Params)
 //   mode 5: + lookup warps take their indices from the staged tiles
+// Ablations of single design choices:
+//   mode 10: mode 0 with the naive chunk order (no lane rotation): the 8
+//            lanes of an LDS.128 phase hit the same bank group
+//   mode 11: mode 0 with plain int32 accumulation (every 16-bit field
+//            widened on every lookup) instead of SWAR fields
+//   mode 12: mode 2 with the vanilla table build (every row summed from its
+//            g activations) instead of the topological walk
 //   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o k1_ablate k1_ablate.cu
 #include <cstdio>
 #include "../paper_2512_06443_b200/csrc/vlut_kernel.cuh"
 
 using namespace vlut;
+
+// vanilla build: every half-table row of a group summed from
+// scratch over its g trits (g-1 packed adds per row) instead of one add along
+// the Gray walk; same rows, same stores
+template <int G>
+__device__ __forceinline__ void build_tables_vanilla(uint32_t tab_s, uint32_t a_s, int grp0, int bw,
+                                                     int lane) {
+  using CC = Cfg<G>;
+  constexpr uint32_t K1 = 0x00010001u;
+  constexpr uint32_t C128 = 128u * K1;
+  for (int j = bw; j < CC::GS; j += kBuilderWarps) {
+    uint32_t P[8], Mn[8];
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+      const uint32_t x = lds_u16(a_s + ((grp0 + j) * G + r) * kNcta + 2 * lane);
+      const uint32_t U = __byte_perm(x ^ 0x8080u, 0u, 0x4140);
+      P[r] = U - C128;
+      Mn[r] = C128 - U;
+    }
+    const uint32_t row0 = tab_s + (uint32_t)(j * CC::HR * kRowBytes) + 4 * lane;
+#pragma unroll
+    for (int pos = 0; pos < CC::HR; ++pos) {
+      int idx = CC::ZERO + pos;  // upper half: idx >= zero
+      uint32_t T = (uint32_t)CC::BIAS * K1;
+#pragma unroll
+      for (int r = 0; r < G; ++r) {
+        const int d = idx % 3;
+        idx /= 3;
+        T += (d == 2) ? P[r] : ((d == 0) ? Mn[r] : 0u);
+      }
+      sts32(row0 + pos * kRowBytes, T);
+    }
+  }
+}
+
+// plain int32 accumulation: both 16-bit fields of every looked-up word are
+// widened and added on every lookup (2 extra ops per word, 64 accumulators)
+template <int G>
+__device__ __forceinline__ void lookup_int32(uint32_t tab, const uint32_t (&iwa)[4],
+                                             const uint32_t (&rot)[8], int32_t (&acc)[64]) {
+  using CC = Cfg<G>;
+#pragma unroll
+  for (int b = 0; b < CC::GS; ++b) {
+    const int i = (int)((iwa[b >> 2] >> (8 * (b & 3))) & CC::IDX_MASK);
+    const int d = i - CC::ZERO;
+    const int m = d >> 31;
+    const uint32_t pos = (uint32_t)((d ^ m) - m);
+    const uint32_t r = tab + (uint32_t)(b * CC::HR * kRowBytes) + pos * kRowBytes;
+    uint4 v[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) v[s] = lds128(r + rot[s]);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const uint32_t w[4] = {v[s].x, v[s].y, v[s].z, v[s].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int lo = (int)(w[q] & 0xFFFFu) - CC::BIAS, hi = (int)(w[q] >> 16) - CC::BIAS;
+        acc[8 * s + 2 * q] += m ? -lo : lo;
+        acc[8 * s + 2 * q + 1] += m ? -hi : hi;
+      }
+    }
+  }
+}
 constexpr int G = 4, W = 12;
 using C = Cfg<G>;
 constexpr int THREADS = (W + kBuilderWarps) * 32;
 // staging buffers live after the tables (the kernel layout's IDX/A offsets,
 // rebased so that they start at STAGE_BASE + IDX_OFF)
 constexpr int STAGE_BASE = 2 * Cfg<G>::TAB_BYTES + Cfg<G>::A_BYTES + 64 - Layout<G, W>::IDX_OFF;
+
+template <int MODE>
+struct Mode {
+  static constexpr bool HANDSHAKE = (MODE >= 1 && MODE <= 7) || MODE == 12;
+  static constexpr bool BUILD = (MODE >= 2 && MODE <= 7);
+  static constexpr bool VANILLA = MODE == 12;
+  static constexpr bool FLUSH = MODE >= 3 && MODE <= 7;
+  static constexpr bool STAGE = MODE >= 4 && MODE <= 7;
+};
 
 template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1) ablate(int ntiles, unsigned long long* cyc, uint32_t* sink,
@@ -49,9 +128,9 @@ __global__ void __launch_bounds__(THREADS, 1) ablate(int ntiles, unsigned long l
   if (warp >= W) {
     const int bw = warp - W;
     for (int u = 0; u < ntiles + 2; ++u) {
-      if (MODE >= 1 && u >= 2) mbar_wait(mbar + 16 + 8 * (u & 1), ((u >> 1) - 1) & 1);
+      if (Mode<MODE>::HANDSHAKE && u >= 2) mbar_wait(mbar + 16 + 8 * (u & 1), ((u >> 1) - 1) & 1);
       if (u >= ntiles) continue;
-      if (MODE >= 4) {
+      if (Mode<MODE>::STAGE) {
         if (u + 1 < ntiles) {
           if (MODE != 6) stage_tile<G, W>(p, u + 1, (u + 1) % kStageBufs, 0, 0, smem + STAGE_BASE, tid - W * 32, 3);
           if (MODE != 7) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
@@ -60,15 +139,19 @@ __global__ void __launch_bounds__(THREADS, 1) ablate(int ntiles, unsigned long l
         }
         if (MODE != 7) bar_sync(5, kBuilderWarps * 32);
       }
-      if (MODE >= 2) build_tables<G>(tab_s + (u & 1) * C::TAB_BYTES,
+      if (Mode<MODE>::VANILLA) build_tables_vanilla<G>(tab_s + (u & 1) * C::TAB_BYTES, a_s, 0, bw, lane);
+      else if (Mode<MODE>::BUILD) build_tables<G>(tab_s + (u & 1) * C::TAB_BYTES,
                                      MODE >= 4 ? smem_u32(smem + STAGE_BASE + Layout<G, W>::A_OFF + (u % kStageBufs) * C::A_BYTES) : a_s,
                                      0, bw, lane);
-      if (MODE >= 1) { __syncwarp(); if (lane == 0) mbar_arrive(mbar + 8 * (u & 1)); }
+      if (Mode<MODE>::HANDSHAKE) { __syncwarp(); if (lane == 0) mbar_arrive(mbar + 8 * (u & 1)); }
     }
   } else {
     uint32_t rot[8];
 #pragma unroll
-    for (int s = 0; s < 8; ++s) rot[s] = (uint32_t)(((lane + s) & 7) * 16);
+    for (int s = 0; s < 8; ++s) rot[s] = (uint32_t)((MODE == 10 ? s : ((lane + s) & 7)) * 16);
+    int32_t acc32[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) acc32[i] = 0;
     const uint32_t taddr = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
     uint32_t sw[8][4];
 #pragma unroll
@@ -80,7 +163,7 @@ __global__ void __launch_bounds__(THREADS, 1) ablate(int ntiles, unsigned long l
     int since = 0;
     bool first = true;
     for (int t = 0; t < ntiles; ++t) {
-      if (MODE >= 1) mbar_wait(mbar + 8 * (t & 1), (t >> 1) & 1);
+      if (Mode<MODE>::HANDSHAKE) mbar_wait(mbar + 8 * (t & 1), (t >> 1) & 1);
       uint32_t iwa[4];
       if (MODE == 5) {
         const uint4 iw = lds128(smem_u32(smem + STAGE_BASE + Layout<G, W>::IDX_OFF) + (t % kStageBufs) * Layout<G, W>::IDX_BYTES + tid * 16);
@@ -95,9 +178,10 @@ __global__ void __launch_bounds__(THREADS, 1) ablate(int ntiles, unsigned long l
         for (int b = 0; b < 4; ++b) w |= (((x >> (7 * b)) & 127u) % 81u) << (8 * b);
         iwa[i] = w;
       }
-      lookup_sub<G>(0, tab_s + (t & 1) * C::TAB_BYTES, iwa, rot, sw, nneg);
-      if (MODE >= 1) { __syncwarp(); if (lane == 0) mbar_arrive(mbar + 16 + 8 * (t & 1)); }
-      if (MODE >= 3 && (++since == 3 || t + 1 == ntiles)) {
+      if (MODE == 11) lookup_int32<G>(tab_s + (t & 1) * C::TAB_BYTES, iwa, rot, acc32);
+      else lookup_sub<G>(0, tab_s + (t & 1) * C::TAB_BYTES, iwa, rot, sw, nneg);
+      if (Mode<MODE>::HANDSHAKE) { __syncwarp(); if (lane == 0) mbar_arrive(mbar + 16 + 8 * (t & 1)); }
+      if (Mode<MODE>::FLUSH && (++since == 3 || t + 1 == ntiles)) {
         since = 0;
         flush_tmem<G>(sw, nneg, taddr, first);
         first = false;
@@ -107,6 +191,8 @@ __global__ void __launch_bounds__(THREADS, 1) ablate(int ntiles, unsigned long l
     for (int s = 0; s < 8; ++s)
 #pragma unroll
       for (int q = 0; q < 4; ++q) out += sw[s][q];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) out += (uint32_t)acc32[i];
   }
   const long long t1 = clock64();
   tmem_fence_before();
@@ -153,7 +239,7 @@ void run(int sms, int ntiles) {
   for (int i = 0; i < sms; ++i) mc += h[i];
   mc /= sms;
   const double lookup_bytes = (double)W * 32 * ntiles * 16 * 128;  // rows x groups x 128 B
-  const double build_bytes = (MODE >= 2) ? (double)ntiles * 16 * C::HR * 128 : 0;
+  const double build_bytes = (Mode<MODE>::BUILD || Mode<MODE>::VANILLA) ? (double)ntiles * 16 * C::HR * 128 : 0;
   printf("mode=%d: lookups %.1f B/clk/SM, lookups+build %.1f B/clk/SM  (%.3f ms, %.0f MHz) err=%s\n",
          MODE, lookup_bytes / mc, (lookup_bytes + build_bytes) / mc, ms, mc / (ms * 1e-3) / 1e6,
          cudaGetErrorString(cudaGetLastError()));
@@ -170,5 +256,8 @@ int main() {
   run<5>(sms, 400);
   run<6>(sms, 400);
   run<7>(sms, 400);
+  run<10>(sms, 400);
+  run<11>(sms, 400);
+  run<12>(sms, 400);
   return 0;
 }
