@@ -14,9 +14,12 @@
  *   - Plain C types only.  "dev" pointers are CUDA device pointers, "host"
  *     pointers are ordinary host memory.  `stream` is a cudaStream_t passed
  *     as void* (0 = legacy default stream).
- *   - The caller owns every buffer.  The library never allocates or frees
- *     device memory; it keeps no global mutable state except a thread-local
- *     error string and a per-device property/attribute cache.
+ *   - The caller owns every buffer.  The library allocates device memory in
+ *     one place only: vlut_mpgemm (the north-star signature, which has no
+ *     workspace argument) keeps one workspace per (device, stream), allocated
+ *     and zeroed on first use and kept for the life of the process.  Other
+ *     global state: a thread-local error string and per-device
+ *     property/attribute caches.
  *   - Arguments are validated on the host before anything is launched.  On
  *     failure nothing is launched, a status != VLUT_OK is returned and
  *     vlut_last_error() describes it.  Nothing aborts or throws across the ABI.
@@ -162,6 +165,8 @@ vlut_status vlut_plan(int M, int K, int N, int g, vlut_launch_plan* plan);
  *   out     : device fp32 [M][N], token axis contiguous.
  * M == 0 or N == 0 is a no-op returning VLUT_OK.  A, out need 4-byte
  * alignment; 16-byte alignment and N % 16 == 0 take the vectorised path.
+ * The planner may choose any schedule (cluster split-K, stream-K, K2 for small
+ * N) using the library's workspace for `stream` (see Conventions).
  */
 vlut_status vlut_mpgemm(const vlut_packed_weights* W, const int8_t* A,
                         const float* a_scale, float w_scale, float* out,

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/vlut.h"
@@ -696,6 +697,40 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
 
 }  // namespace
 
+// Library-owned workspaces of vlut_mpgemm, one per (device, stream): calls on
+// one stream are ordered, so they may share it; allocated with cudaMalloc and
+// zeroed (stream-ordered) on first use, kept for the life of the process.
+bool internal_workspace(void* stream, void** ws, size_t* bytes) {
+  static std::mutex mu;
+  static std::vector<std::tuple<int, void*, void*, size_t>> cache;  // (device, stream, ptr, bytes)
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  DeviceInfo d;
+  if (device_info(&d) != VLUT_OK) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& e : cache)
+    if (std::get<0>(e) == dev && std::get<1>(e) == stream) {
+      *ws = std::get<2>(e);
+      *bytes = std::get<3>(e);
+      return true;
+    }
+  const size_t need = sk_workspace_bytes(d.sms);
+  void* p = nullptr;
+  if (cudaMalloc(&p, need) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (cudaMemsetAsync(p, 0, need, static_cast<cudaStream_t>(stream)) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(p);
+    return false;
+  }
+  cache.emplace_back(dev, stream, p, need);
+  *ws = p;
+  *bytes = need;
+  return true;
+}
+
 // ================================================================ C ABI
 extern "C" {
 
@@ -838,7 +873,14 @@ vlut_status vlut_plan(int M, int K, int N, int g, vlut_launch_plan* plan) {
 
 vlut_status vlut_mpgemm(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,
                         float w_scale, float* out, int M, int K, int N, void* stream) {
-  return run_mpgemm(W, A, a_scale, w_scale, out, M, K, N, nullptr, stream, false);
+  // the north-star signature has no workspace argument: use the library's
+  // per-(device, stream) workspace so every schedule (stream-K, K2 split-K)
+  // is available; without one, only the cluster schedules
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  if (M > 0 && N > 0) internal_workspace(stream, &ws, &ws_bytes);
+  return run_mpgemm(W, A, a_scale, w_scale, out, M, K, N, nullptr, stream, false, nullptr, 0, ws,
+                    ws_bytes);
 }
 
 vlut_status vlut_mpgemm_ex(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,

@@ -149,3 +149,28 @@ def test_config4_full_size_slot_sampled(v, N, g):
     acc_ref = oracle.gemm_i32(W[pick], qr)
     check_fp32(out.cpu().numpy()[pick], acc_ref, sr, synth.W_SCALE)
     check_fp32(o_sc.cpu().numpy()[pick], acc_ref, sr, synth.W_SCALE)
+
+
+def test_north_star_mpgemm_uses_library_workspace(v):
+    """vlut_mpgemm (no workspace argument) reaches the K2 decode path through
+    the library's per-stream workspace: config 4 shape at N = 1 and 16, two
+    streams, repeated calls -- all equal to the oracle."""
+    M, K = 3072, 23040
+    W = synth.ternary_weights(M, K, seed=9)
+    pw = v.pack_weights(W, 4, device=dev())
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for N in (1, 16):
+        x = synth.activations_f32(K, N, seed=N)
+        q, s = oracle.quantize(x)
+        qd, sd = to_dev(q), to_dev(s)
+        outs = []
+        for st in streams:
+            with torch.cuda.stream(st):
+                for _ in range(2):
+                    o = v.mpgemm(pw, qd, sd, synth.W_SCALE, stream=st)
+                outs.append(o)
+        torch.cuda.synchronize()
+        pick = np.unique(np.concatenate([[0, M - 1], synth.rng(N).integers(0, M, size=40)]))
+        ref = oracle.gemm_i32(W[pick], q)
+        for o in outs:
+            check_fp32(o.cpu().numpy()[pick], ref, s, synth.W_SCALE)
