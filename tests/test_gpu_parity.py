@@ -404,7 +404,8 @@ def test_host_pipeline_matches_oracle(v):
 
 
 # ------------------------------------------------------------------ fused all-gather epilogue (a8)
-@pytest.mark.parametrize("M,K,N,G", [(6912, 2560, 256, 2), (1000, 1280, 100, 3), (700, 260, 64, 8)])
+@pytest.mark.parametrize("M,K,N,G", [(6912, 2560, 256, 2), (1000, 1280, 100, 3), (700, 260, 64, 8),
+                                     (333, 512, 63, 4)])
 def test_mpgemm_allgather_emulated_ranks(v, M, K, N, G):
     """Single-process emulation of G ranks (no rank waits on another): rank r
     computes rows [r0, r1) with vlut_mpgemm_allgather into its own buffer and

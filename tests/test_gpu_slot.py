@@ -70,6 +70,21 @@ def test_slot_acc_every_variant_and_split(v, g, nw, tpw, splits):
         assert np.array_equal(acc.cpu().numpy(), oracle.gemm_i32(W, A)), (M, K, N)
 
 
+@pytest.mark.parametrize("g,nw,tpw,N", [(4, 8, 2, 100), (4, 4, 1, 67), (5, 2, 2, 129), (4, 8, 2, 65)])
+def test_slot_wide_n_global_activation_path(v, g, nw, tpw, N):
+    """N > 64: activations are not staged by TMA (the builders read them from
+    global memory), several N-tiles, ragged last N-tile; forced K2 plans."""
+    M, K = 1100, 1280 if g == 4 else 1285
+    W = synth.ternary_weights(M, K, seed=N)
+    A = synth.int8_activations(K, N, seed=N + 1)
+    pw = v.pack_weights(W, g, device=dev())
+    ref = oracle.gemm_i32(W, A)
+    for splits in (1, 0):
+        acc = v.mpgemm_acc_ws(pw, to_dev(A), plan=v.slot_plan(tpw=tpw, nw=nw, splits=splits))
+        torch.cuda.synchronize()
+        assert np.array_equal(acc.cpu().numpy(), ref)
+
+
 @pytest.mark.parametrize("g,tpw", [(4, 1), (4, 2), (5, 1), (5, 2)])
 def test_slot_adversarial_extremes(v, g, tpw):
     # every field at its bound: all-+1 / all--1 rows against -128 / +127,
