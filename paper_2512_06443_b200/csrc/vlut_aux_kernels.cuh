@@ -19,6 +19,22 @@ constexpr int kQThreads = 256;   // 64 rows x 4 float4 columns per pass
 constexpr int kQTok = 16;        // tokens per cluster
 constexpr int kQCache = 12;      // float4 register cache per thread
 
+// One operand's float4 (4 tokens of row k), zeros outside N.
+template <bool ALIGNED>
+__device__ __forceinline__ float4 q_load1(const float* x, int k, int N, int n) {
+  const size_t o = (size_t)k * N + n;
+  if (ALIGNED && n + 3 < N) return __ldg(reinterpret_cast<const float4*>(x + o));
+  float t[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) t[i] = (n + i < N) ? __ldg(x + o + i) : 0.f;
+  return make_float4(t[0], t[1], t[2], t[3]);
+}
+
+__device__ __forceinline__ float4 fmul4(float4 a, float4 b) {
+  return make_float4(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y), __fmul_rn(a.z, b.z),
+                     __fmul_rn(a.w, b.w));
+}
+
 template <bool ALIGNED>
 __device__ __forceinline__ float4 q_load(const float* x, const float* y, int k, int N, int n) {
   const size_t o = (size_t)k * N + n;
@@ -72,11 +88,24 @@ __global__ void __launch_bounds__(kQThreads)
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   float4 cache[kQCache];
   float m[4] = {0.f, 0.f, 0.f, 0.f};
+  // every load of the register cache is issued before any use (a multiply
+  // right behind each load would serialise the DRAM round trips)
 #pragma unroll
   for (int i = 0; i < kQCache; ++i) {
     const int k = k_begin + rsub + 64 * i;
     cache[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (k < k_end && n < N) cache[i] = q_load<ALIGNED>(x, y, k, N, n);
+    if (k < k_end && n < N) cache[i] = q_load1<ALIGNED>(x, k, N, n);
+  }
+  if (y) {
+    float4 yc[kQCache];
+#pragma unroll
+    for (int i = 0; i < kQCache; ++i) {
+      const int k = k_begin + rsub + 64 * i;
+      yc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (k < k_end && n < N) yc[i] = q_load1<ALIGNED>(y, k, N, n);
+    }
+#pragma unroll
+    for (int i = 0; i < kQCache; ++i) cache[i] = fmul4(cache[i], yc[i]);
   }
 #pragma unroll
   for (int i = 0; i < kQCache; ++i) {
@@ -261,27 +290,43 @@ __global__ void __launch_bounds__(256)
   const int n4 = (N + 3) / 4;
   const long long total = (long long)K * n4;
   const bool vec = ((N & 3) == 0) && ((((uintptr_t)x) & 15) == 0) && ((((uintptr_t)q) & 3) == 0);
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int k = (int)(e / n4), n = 4 * (int)(e % n4);
-    float s[4];
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  constexpr int U = 4;  // units per thread and round: all loads issued before any use
+  for (long long e0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; e0 < total;
+       e0 += U * stride) {
+    float4 v[U];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float a = (n + i < N) ? __uint_as_float(__ldg(amax + n + i)) : 0.f;
-      s[i] = (a == 0.f) ? 1.f : __fdiv_rn(a, 127.f);
+    for (int u = 0; u < U; ++u) {
+      const long long e = e0 + u * stride;
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (vec && e < total) {
+        const int k = (int)(e / n4), n = 4 * (int)(e % n4);
+        v[u] = __ldg(reinterpret_cast<const float4*>(x + (size_t)k * N + n));
+      }
     }
-    if (k == 0)
-      for (int i = 0; i < 4 && n + i < N; ++i) scale[n + i] = s[i];
-    const size_t o = (size_t)k * N + n;
-    if (vec) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(x + o));
-      const uint32_t packed = (uint32_t)(uint8_t)q_code(v.x, s[0]) |
-                              ((uint32_t)(uint8_t)q_code(v.y, s[1]) << 8) |
-                              ((uint32_t)(uint8_t)q_code(v.z, s[2]) << 16) |
-                              ((uint32_t)(uint8_t)q_code(v.w, s[3]) << 24);
-      *reinterpret_cast<uint32_t*>(q + o) = packed;
-    } else {
-      for (int i = 0; i < 4 && n + i < N; ++i) q[o + i] = q_code(__ldg(x + o + i), s[i]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long e = e0 + u * stride;
+      if (e >= total) break;
+      const int k = (int)(e / n4), n = 4 * (int)(e % n4);
+      float s[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float a = (n + i < N) ? __uint_as_float(__ldg(amax + n + i)) : 0.f;
+        s[i] = (a == 0.f) ? 1.f : __fdiv_rn(a, 127.f);
+      }
+      if (k == 0)
+        for (int i = 0; i < 4 && n + i < N; ++i) scale[n + i] = s[i];
+      const size_t o = (size_t)k * N + n;
+      if (vec) {
+        const uint32_t packed = (uint32_t)(uint8_t)q_code(v[u].x, s[0]) |
+                                ((uint32_t)(uint8_t)q_code(v[u].y, s[1]) << 8) |
+                                ((uint32_t)(uint8_t)q_code(v[u].z, s[2]) << 16) |
+                                ((uint32_t)(uint8_t)q_code(v[u].w, s[3]) << 24);
+        *reinterpret_cast<uint32_t*>(q + o) = packed;
+      } else {
+        for (int i = 0; i < 4 && n + i < N; ++i) q[o + i] = q_code(__ldg(x + o + i), s[i]);
+      }
     }
   }
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
