@@ -39,6 +39,14 @@ def run(mode, n=200):
             v.mpgemm_ex(pw, q, s, 0.02, out=out, plan=v.LaunchPlan(12, 4), stream=st); torch.cuda.synchronize(); flush.zero_(); e[2].record(st); v.mpgemm_ws(pw, q, s, 0.02, out=out, ws=ws, stream=st); e[3].record(st)
         elif mode == "k1c1_then_flush":
             v.mpgemm_ex(pw, q, s, 0.02, out=out, plan=v.LaunchPlan(12, 1), stream=st); torch.cuda.synchronize(); flush.zero_(); e[2].record(st); v.mpgemm_ws(pw, q, s, 0.02, out=out, ws=ws, stream=st); e[3].record(st)
+        elif mode == "small_then_flush":
+            small.add_(1.0); torch.cuda.synchronize(); flush.zero_(); e[2].record(st); v.mpgemm_ws(pw, q, s, 0.02, out=out, ws=ws, stream=st); e[3].record(st)
+        elif mode == "k1_sleep_flush":
+            v.mpgemm_ws(pw, q, s, 0.02, out=out, ws=ws, stream=st); torch.cuda.synchronize(); time.sleep(0.0002); flush.zero_(); e[2].record(st); v.mpgemm_ws(pw, q, s, 0.02, out=out, ws=ws, stream=st); e[3].record(st)
+        elif mode == "k3_noflush_k1":
+            v.quantize(x, q=q, scale=s, stream=st); e[2].record(st); v.mpgemm_ws(pw, q, s, 0.02, out=out, ws=ws, stream=st); e[3].record(st)
+        elif mode == "k3_pdl_step":
+            flush.zero_(); e[2].record(st); v.quantize(x, q=q, scale=s, stream=st); v.mpgemm_ws(pw, q, s, 0.02, out=out, ws=ws, stream=st); e[3].record(st)
         elif mode == "double_flush":
             flush.zero_(); flush.zero_(); e[2].record(st); v.mpgemm_ws(pw, q, s, 0.02, out=out, ws=ws, stream=st); e[3].record(st)
         torch.cuda.synchronize()
@@ -46,5 +54,7 @@ def run(mode, n=200):
     ts = np.array(ts)
     print(mode, "mean %.2f med %.2f min %.2f max %.2f" % (ts.mean(), np.median(ts), ts.min(), ts.max()))
 q2 = torch.empty_like(q); s2 = torch.empty_like(s); q3 = q.clone(); s3 = s.clone()
-for m in ("sync_first", "k3_then_flush_sync", "k1c8_then_flush", "k1c4_then_flush", "k1c1_then_flush", "k1_then_flush"):
+import time
+small = torch.zeros(1024, device=dev)
+for m in ("sync_first", "k3_then_flush_sync", "small_then_flush", "k1_sleep_flush", "k1_then_flush", "k3_noflush_k1", "k3_pdl_step"):
     run(m)
