@@ -839,6 +839,9 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
           }
         }
       }
+#ifdef VLUT_TIMING_EPI
+      if (c0 == 0) VLUT_STAMP(6);
+#endif
       if (p.out_t) {
         // fused output transposition: out[n][m .. m+3], one token scale
 #pragma unroll
@@ -929,7 +932,9 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
     // remote reads done: arrive now, wait only before exit (the peers keep
     // their shared memory until every CTA of the cluster has read it)
     if (S > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+#ifndef VLUT_TIMING_EPI
     VLUT_STAMP(6);
+#endif
     if constexpr (!ACC_ONLY) {
       if (p.amax_out) {
         // fused re-quantization (f1): per-token |out| max of this CTA ->

@@ -5,6 +5,8 @@ import os, sys
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2512_06443_b200 as v
+if len(sys.argv) > 1:
+    v.lib_path = sys.argv[1]
 from paper_2512_06443_b200 import synth
 dev = torch.device("cuda")
 M, K, N = 6912, 2560, 256
@@ -21,6 +23,7 @@ modes = {
     "fill_0x5a": lambda: flush.fill_(0x5A),
     "copy_random": lambda: flush.copy_(src),
     "none": lambda: None,
+    "read_x_then_flush": lambda: (x.sum(), flush.zero_()),
 }
 for name, fl in list(modes.items()) * 2:
     ts = []

@@ -8,7 +8,7 @@ sys.path.insert(0, ROOT)
 from paper_2512_06443_b200 import build as B
 lib = "/tmp/libvlut_timing.so"
 subprocess.check_call([B.nvcc()] + [f for f in B.NVCC_FLAGS if f not in ("-v", "-Xptxas")] +
-                      ["-DVLUT_TIMING", "-o", lib] + B.SOURCES)
+                      ["-DVLUT_TIMING", "-DVLUT_TIMING_EPI", "-o", lib] + B.SOURCES)
 import paper_2512_06443_b200 as v
 v.lib_path = lib
 from paper_2512_06443_b200 import synth
@@ -23,9 +23,9 @@ out = torch.empty((M, N), device=dev)
 buf = torch.zeros(65536 * 8, dtype=torch.int64, device=dev)
 v.lib().vlut_debug_set_timing(ctypes.c_void_p(buf.data_ptr()))
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-names = ["entry", "tmem", "table0", "loop_end", "red_written", "sync1", "reduced", "stored"]
+names = ["entry", "tmem", "table0", "loop_end", "red_written", "sync1", "dsmem_loaded", "stored"]
 xs = x.clone()
-for mode in ("plain", "after_k3", "after_sum_x", "after_q_write", "after_k3_other_x", "after_quantize_t"):
+for mode in ("plain", "after_sum_x", "plain", "after_sum_x"):
     acc = []
     for it in range(6):
         if mode == "after_k3":
