@@ -247,6 +247,11 @@ double plan_sk(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
     double cost = units * VLUT_KG_TILE * (double)(mcta + half_rows);
     cost += 6000.0;                             // start + last epilogue
     cost += (double)mcta * 256.0 * 3.0 / 64.0;  // partial write + read + output
+    // the owner of a split tile reads every producer's int32 partial
+    // (mcta x 64 x 4 B) one after another at ~64 B/clk: with few tiles a
+    // tile is split over many CTAs and this serial fixup dominates
+    const double per_tile = (double)grid / (double)(MT * NT);
+    if (per_tile > 1.0) cost += (per_tile - 1.0) * (double)mcta * 256.0 / 64.0;
     if (cost < best_cost * 0.995) {
       best_cost = cost;
       best->warps = warps;

@@ -539,22 +539,35 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
     e_end = (int)(((long long)elems * (rank + 1)) / S);
   }
   if (warp < kLW) {
-#pragma unroll 4
-    for (int e = e_begin + tid; e < e_end; e += kLookupThreads) {
-      const int r = e / ntok_valid, c = e - r * ntok_valid;
-      const size_t o = (size_t)(m0 + r) * p.N + n0 + c;
-      int32_t a;
-      if (S > 1) {
-        a = __ldcg(p.ws_acc + o);
-        __stcg(p.ws_acc + o, 0);  // keep the workspace zero for the next launch
-      } else {
-        a = tile_c[r * ld + c];
+    // batches of EB elements per thread: every workspace load of a batch is
+    // issued before its stores (out / ws may alias as far as the compiler
+    // knows, so a fused load-store loop would serialise the L2 round trips)
+    constexpr int EB = 8;
+    for (int e0 = e_begin + tid; e0 < e_end; e0 += EB * kLookupThreads) {
+      int32_t a[EB];
+#pragma unroll
+      for (int b = 0; b < EB; ++b) {
+        const int e = e0 + b * kLookupThreads;
+        a[b] = 0;
+        if (e < e_end) {
+          const int r = e / ntok_valid, c = e - r * ntok_valid;
+          if (S > 1) a[b] = __ldcg(p.ws_acc + (size_t)(m0 + r) * p.N + n0 + c);
+          else a[b] = tile_c[r * ld + c];
+        }
       }
-      if (p.acc_only) {
-        reinterpret_cast<int32_t*>(p.out)[o] = a;
-      } else {
-        const float sc = __fmul_rn(__ldg(p.a_scale + n0 + c), p.w_scale);
-        reinterpret_cast<float*>(p.out)[o] = __fmul_rn((float)a, sc);
+#pragma unroll
+      for (int b = 0; b < EB; ++b) {
+        const int e = e0 + b * kLookupThreads;
+        if (e >= e_end) break;
+        const int r = e / ntok_valid, c = e - r * ntok_valid;
+        const size_t o = (size_t)(m0 + r) * p.N + n0 + c;
+        if (S > 1) __stcg(p.ws_acc + o, 0);  // keep the workspace zero for the next launch
+        if (p.acc_only) {
+          reinterpret_cast<int32_t*>(p.out)[o] = a[b];
+        } else {
+          const float sc = __fmul_rn(__ldg(p.a_scale + n0 + c), p.w_scale);
+          reinterpret_cast<float*>(p.out)[o] = __fmul_rn((float)a[b], sc);
+        }
       }
     }
   }
