@@ -172,7 +172,29 @@ __device__ __forceinline__ void sk_epilogue(const Params& p, const SkParams& sk,
         const int rr = e >> 4;
         acc4[i] = red[rr * 16 + ((e & 15) ^ ((rr >> 2) & 1))];
       }
-      for (int c2 = cta - 1; c2 >= c_lo; --c2) {
+      // PP producers per round, all their loads issued before any add: with
+      // few tiles a tile has many producers and one round trip per producer
+      // would serialise the fixup
+      constexpr int PP = (WARPS >= 16) ? 2 : 4;
+      int c2 = cta - 1;
+      for (; c2 - (PP - 1) >= c_lo; c2 -= PP) {
+        int4 w4[PP][UPT];
+#pragma unroll
+        for (int pp = 0; pp < PP; ++pp) {
+          const int4* prow =
+              reinterpret_cast<const int4*>(sk.ws + (size_t)(c2 - pp) * L::MCTA * kNcta);
+#pragma unroll
+          for (int i = 0; i < UPT; ++i) w4[pp][i] = __ldcg(prow + tid + (half * UPT + i) * L::MCTA);
+        }
+#pragma unroll
+        for (int pp = 0; pp < PP; ++pp)
+#pragma unroll
+          for (int i = 0; i < UPT; ++i) {
+            acc4[i].x += w4[pp][i].x; acc4[i].y += w4[pp][i].y;
+            acc4[i].z += w4[pp][i].z; acc4[i].w += w4[pp][i].w;
+          }
+      }
+      for (; c2 >= c_lo; --c2) {
         const int4* prow = reinterpret_cast<const int4*>(sk.ws + (size_t)c2 * L::MCTA * kNcta);
         int4 w4[UPT];
 #pragma unroll
