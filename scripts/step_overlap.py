@@ -6,6 +6,8 @@ import os, sys
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2512_06443_b200 as v
+if len(sys.argv) > 1:
+    v.lib_path = sys.argv[1]
 from paper_2512_06443_b200 import synth
 dev = torch.device("cuda")
 M, K, N, g = 6912, 2560, 256, 4
