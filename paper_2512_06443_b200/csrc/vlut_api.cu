@@ -719,6 +719,14 @@ bool internal_workspace(void* stream, void** ws, size_t* bytes) {
       *bytes = std::get<3>(e);
       return true;
     }
+  // never allocate inside a stream capture (cudaMalloc would invalidate it):
+  // the call then runs without a workspace (cluster schedules only)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(static_cast<cudaStream_t>(stream), &cap) != cudaSuccess ||
+      cap != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return false;
+  }
   const size_t need = sk_workspace_bytes(d.sms);
   void* p = nullptr;
   if (cudaMalloc(&p, need) != cudaSuccess) {

@@ -189,3 +189,23 @@ def test_north_star_mpgemm_uses_library_workspace(v):
         ref = oracle.gemm_i32(W[pick], q)
         for o in outs:
             check_fp32(o.cpu().numpy()[pick], ref, s, synth.W_SCALE)
+
+
+def test_north_star_mpgemm_under_graph_capture(v):
+    """First vlut_mpgemm call on a stream inside a CUDA graph capture: the
+    library must not allocate its workspace there (it falls back to the
+    cluster schedules); the captured graph replays correctly."""
+    M, K, N = 700, 1280, 8
+    W = synth.ternary_weights(M, K, seed=21)
+    x = synth.activations_f32(K, N, seed=22)
+    q, s = oracle.quantize(x)
+    pw = v.pack_weights(W, 4, device=dev())
+    qd, sd = to_dev(q), to_dev(s)
+    out = torch.empty((M, N), device=dev())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        v.mpgemm(pw, qd, sd, synth.W_SCALE, out=out)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    check_fp32(out.cpu().numpy(), oracle.gemm_i32(W, q), s, synth.W_SCALE)
