@@ -52,6 +52,13 @@ constexpr int kKgTile = 16;           // groups per K-tile (16-byte index vector
 constexpr int kRowBytes = kNcta * 2;  // one table row: 64 tokens x int16
 constexpr int kFlushTiles = 3;        // widen SWAR fields every 3 K-tiles = 48 groups
 constexpr int kStageBufs = 3;         // A / index staging buffers
+#ifndef VLUT_TABLE_BUFS
+#define VLUT_TABLE_BUFS 2
+#endif
+// mbarrier slots (byte offsets from MBAR_OFF): FULL[b], EMPTY[b], STAGE[s]
+__host__ __device__ constexpr int mb_full(int b) { return 8 * b; }
+__host__ __device__ constexpr int mb_empty(int b) { return 8 * VLUT_TABLE_BUFS + 8 * b; }
+__host__ __device__ constexpr int mb_stage(int s) { return 16 * VLUT_TABLE_BUFS + 8 * s; }
 
 __host__ __device__ constexpr int pow3(int g) { return g == 0 ? 1 : 3 * pow3(g - 1); }
 
@@ -60,7 +67,10 @@ struct Cfg {
   static constexpr int R = pow3(G);             // full table rows 3^g
   static constexpr int ZERO = (R - 1) / 2;      // index of the all-zero pattern
   static constexpr int HR = (R + 1) / 2;        // stored (half) rows
-  static constexpr int GS = (G == 4) ? 16 : 4;  // groups per table sub-stage
+  // table buffers and groups per sub-stage: NBUF x GS x half rows is the
+  // table region; more, smaller buffers let the builders run further ahead
+  static constexpr int NBUF = VLUT_TABLE_BUFS;
+  static constexpr int GS = (G == 4) ? (NBUF == 4 ? 8 : 16) : (NBUF == 4 ? 2 : 4);
   static constexpr int SUBS = kKgTile / GS;     // sub-stages per K-tile
   static constexpr int BIAS = 128 * G;          // field bias: T + BIAS in [0, 256 g]
   static constexpr int TAB_BYTES = GS * HR * kRowBytes;  // one table buffer
@@ -81,14 +91,14 @@ struct Layout {
   static constexpr int BUILDER0 = WARPS * 32;             // first builder thread
   static constexpr int MCTA = WARPS * 32;                 // output rows per CTA
   static constexpr int RED_BYTES = MCTA * kNcta * 4;      // int32 reduction tile
-  static constexpr int TAB_REGION = 2 * Cfg<G>::TAB_BYTES > RED_BYTES
-                                        ? 2 * Cfg<G>::TAB_BYTES : RED_BYTES;
+  static constexpr int TAB_REGION = Cfg<G>::NBUF * Cfg<G>::TAB_BYTES > RED_BYTES
+                                        ? Cfg<G>::NBUF * Cfg<G>::TAB_BYTES : RED_BYTES;
   static constexpr int IDX_OFF = TAB_REGION;
   static constexpr int IDX_BYTES = MCTA * 16;
   static constexpr int A_OFF = IDX_OFF + kStageBufs * IDX_BYTES;
   static constexpr int MISC_OFF = A_OFF + kStageBufs * Cfg<G>::A_BYTES;  // tmem address
-  static constexpr int MBAR_OFF = MISC_OFF + 16;  // FULL[2], EMPTY[2], STAGE[3] (8 B each)
-  static constexpr int SCALE_OFF = MBAR_OFF + 64;  // fl(a_scale[n] * w_scale), 64 floats
+  static constexpr int MBAR_OFF = MISC_OFF + 16;  // FULL[NBUF], EMPTY[NBUF], STAGE[3] (8 B each)
+  static constexpr int SCALE_OFF = MBAR_OFF + 96;  // fl(a_scale[n] * w_scale), 64 floats
   static constexpr int AMAX_OFF = SCALE_OFF + kNcta * 4;  // per-token |out| max of the CTA
   static constexpr int SMEM = AMAX_OFF + kNcta * 4;
   // epilogue: 16-byte output units per thread (upper bound, splits = 1)
@@ -605,13 +615,12 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
   const uint32_t mbar = smem_u32(smem + L::MBAR_OFF);  // FULL b at +8b, EMPTY b at +16+8b
 
   if (tid == L::BUILDER0) {
-    mbar_init(mbar + 0, kBuilderWarps);
-    mbar_init(mbar + 8, kBuilderWarps);
-    mbar_init(mbar + 16, WARPS);
-    mbar_init(mbar + 24, WARPS);
-    mbar_init(mbar + 32, 1);  // STAGE[0..2]: bulk-copy completion of a staged tile
-    mbar_init(mbar + 40, 1);
-    mbar_init(mbar + 48, 1);
+    for (int b = 0; b < C::NBUF; ++b) {
+      mbar_init(mbar + mb_full(b), kBuilderWarps);
+      mbar_init(mbar + mb_empty(b), WARPS);
+    }
+    for (int st = 0; st < kStageBufs; ++st)
+      mbar_init(mbar + mb_stage(st), 1);  // bulk-copy completion of a staged tile
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();  // mbarriers initialised
@@ -626,9 +635,9 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
       // the packed weights do not depend on the previous kernel: stage tile
       // 0's indices before waiting for it, then its activations
       if (bulk) {
-        stage_tile_bulk<G, WARPS>(p, kt_begin, 0, m0, n0, smem, bt, mbar + 32, true, false, true);
+        stage_tile_bulk<G, WARPS>(p, kt_begin, 0, m0, n0, smem, bt, mbar + mb_stage(0), true, false, true);
         pdl_wait();
-        stage_tile_bulk<G, WARPS>(p, kt_begin, 0, m0, n0, smem, bt, mbar + 32, false, true, false);
+        stage_tile_bulk<G, WARPS>(p, kt_begin, 0, m0, n0, smem, bt, mbar + mb_stage(0), false, true, false);
       } else {
         stage_tile<G, WARPS>(p, kt_begin, 0, m0, n0, smem, bt, /*what=*/1);
         pdl_wait();
@@ -642,18 +651,19 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
       scale_s[bt] = (n < p.N) ? __fmul_rn(__ldg(p.a_scale + n), p.w_scale) : 0.f;
     }
 #pragma unroll 1
-    for (int u = 0; u < nsub + 2; ++u) {
-      if (u >= 2) mbar_wait(mbar + 16 + 8 * (u & 1), ((u >> 1) - 1) & 1);  // lookups of u-2 done
+    for (int u = 0; u < nsub + C::NBUF; ++u) {
+      if (u >= C::NBUF)  // lookups of u - NBUF done with this buffer
+        mbar_wait(mbar + mb_empty(u % C::NBUF), ((u / C::NBUF) - 1) & 1);
       if (u >= nsub) continue;
       const int T = u / C::SUBS, sub = u - T * C::SUBS;
       if (sub == 0) {
         if (bulk) {
           if (T + 1 < ntiles) {
             const int b1 = (T + 1) % kStageBufs;
-            stage_tile_bulk<G, WARPS>(p, kt_begin + T + 1, b1, m0, n0, smem, bt, mbar + 32 + 8 * b1,
+            stage_tile_bulk<G, WARPS>(p, kt_begin + T + 1, b1, m0, n0, smem, bt, mbar + mb_stage(b1),
                                       true, true, true);
           }
-          mbar_wait(mbar + 32 + 8 * (T % kStageBufs), (T / kStageBufs) & 1);
+          mbar_wait(mbar + mb_stage(T % kStageBufs), (T / kStageBufs) & 1);
         } else if (T + 1 < ntiles) {
           stage_tile<G, WARPS>(p, kt_begin + T + 1, (T + 1) % kStageBufs, m0, n0, smem, bt, 3);
           asm volatile("cp.async.wait_group 1;\n" ::: "memory");
@@ -662,10 +672,10 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
         }
         bar_sync(5, kBuilderWarps * 32);  // tile T's A rows visible to all builders
       }
-      build_tables<G>(tab_s + (uint32_t)((u & 1) * C::TAB_BYTES),
+      build_tables<G>(tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES),
                       a_s0 + (uint32_t)((T % kStageBufs) * C::A_BYTES), sub * C::GS, bw, lane);
       __syncwarp();
-      if (lane == 0) mbar_arrive(mbar + 8 * (u & 1));  // table u (and tile T's indices) ready
+      if (lane == 0) mbar_arrive(mbar + mb_full(u % C::NBUF));  // table u (and tile T's indices) ready
     }
   } else {
     // =========================== lookup warps: one output row per thread
@@ -703,16 +713,16 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
 #pragma unroll
       for (int sub = 0; sub < C::SUBS; ++sub) {
         const int u = t * C::SUBS + sub;
-        mbar_wait(mbar + 8 * (u & 1), (u >> 1) & 1);  // table u built
+        mbar_wait(mbar + mb_full(u % C::NBUF), (u / C::NBUF) & 1);  // table u built
         if (u == 0) VLUT_STAMP(2);
         if (sub == 0) {
           const uint4 iw = lds128(idx_s + (t % kStageBufs) * L::IDX_BYTES + tid * 16);
           iwa[0] = iw.x; iwa[1] = iw.y; iwa[2] = iw.z; iwa[3] = iw.w;
         }
-        lookup_sub<G, kLookupGP<WARPS>>(sub, tab_s + (uint32_t)((u & 1) * C::TAB_BYTES), iwa, rot, sw,
+        lookup_sub<G, kLookupGP<WARPS>>(sub, tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES), iwa, rot, sw,
                                         nneg);
         __syncwarp();
-        if (lane == 0) mbar_arrive(mbar + 16 + 8 * (u & 1));  // table buffer u & 1 free
+        if (lane == 0) mbar_arrive(mbar + mb_empty(u % C::NBUF));  // table buffer u & 1 free
       }
       if (++since_flush >= kFlushTiles || t + 1 == ntiles) {
         since_flush = 0;

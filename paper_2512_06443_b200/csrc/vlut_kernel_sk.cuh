@@ -348,13 +348,11 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
   const uint32_t mbar = smem_u32(smem + L::MBAR_OFF);
 
   if (tid == L::BUILDER0) {
-    mbar_init(mbar + 0, kBuilderWarps);
-    mbar_init(mbar + 8, kBuilderWarps);
-    mbar_init(mbar + 16, WARPS);
-    mbar_init(mbar + 24, WARPS);
-    mbar_init(mbar + 32, 1);
-    mbar_init(mbar + 40, 1);
-    mbar_init(mbar + 48, 1);
+    for (int b = 0; b < C::NBUF; ++b) {
+      mbar_init(mbar + mb_full(b), kBuilderWarps);
+      mbar_init(mbar + mb_empty(b), WARPS);
+    }
+    for (int st = 0; st < kStageBufs; ++st) mbar_init(mbar + mb_stage(st), 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -372,9 +370,9 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
     if (nunits > 0) {
       const int m0 = tile_m0(nxt.seg.tile), n0 = tile_n0(nxt.seg.tile);
       if (bulk) {
-        stage_tile_bulk<G, WARPS>(p, nxt.kt, 0, m0, n0, smem, bt, mbar + 32, true, false, true);
+        stage_tile_bulk<G, WARPS>(p, nxt.kt, 0, m0, n0, smem, bt, mbar + mb_stage(0), true, false, true);
         pdl_wait();
-        stage_tile_bulk<G, WARPS>(p, nxt.kt, 0, m0, n0, smem, bt, mbar + 32, false, true, false);
+        stage_tile_bulk<G, WARPS>(p, nxt.kt, 0, m0, n0, smem, bt, mbar + mb_stage(0), false, true, false);
       } else {
         stage_tile<G, WARPS>(p, nxt.kt, 0, m0, n0, smem, bt, 1);
         pdl_wait();
@@ -385,8 +383,9 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
       pdl_wait();
     }
 #pragma unroll 1
-    for (int u = 0; u < nsub + 2; ++u) {
-      if (u >= 2) mbar_wait(mbar + 16 + 8 * (u & 1), ((u >> 1) - 1) & 1);  // lookups of u-2 done
+    for (int u = 0; u < nsub + C::NBUF; ++u) {
+      if (u >= C::NBUF)  // lookups of u - NBUF done with this buffer
+        mbar_wait(mbar + mb_empty(u % C::NBUF), ((u / C::NBUF) - 1) & 1);
       if (u >= nsub) continue;
       const int T = u / C::SUBS, sub = u - T * C::SUBS;
       if (sub == 0) {
@@ -395,7 +394,7 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
           const int b1 = (T + 1) % kStageBufs;
           const int m0 = tile_m0(nxt.seg.tile), n0 = tile_n0(nxt.seg.tile);
           if (bulk) {
-            stage_tile_bulk<G, WARPS>(p, nxt.kt, b1, m0, n0, smem, bt, mbar + 32 + 8 * b1, true,
+            stage_tile_bulk<G, WARPS>(p, nxt.kt, b1, m0, n0, smem, bt, mbar + mb_stage(b1), true,
                                       true, true);
           } else {
             stage_tile<G, WARPS>(p, nxt.kt, b1, m0, n0, smem, bt, 3);
@@ -405,13 +404,13 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
         } else if (!bulk) {
           cp_async_wait_all();
         }
-        if (bulk) mbar_wait(mbar + 32 + 8 * (T % kStageBufs), (T / kStageBufs) & 1);
+        if (bulk) mbar_wait(mbar + mb_stage(T % kStageBufs), (T / kStageBufs) & 1);
         bar_sync(5, kBuilderWarps * 32);
       }
-      build_tables<G>(tab_s + (uint32_t)((u & 1) * C::TAB_BYTES),
+      build_tables<G>(tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES),
                       a_s0 + (uint32_t)((T % kStageBufs) * C::A_BYTES), sub * C::GS, bw, lane);
       __syncwarp();
-      if (lane == 0) mbar_arrive(mbar + 8 * (u & 1));
+      if (lane == 0) mbar_arrive(mbar + mb_full(u % C::NBUF));
     }
   } else {
     // =========================== lookup warps
@@ -447,15 +446,15 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
 #pragma unroll
       for (int sub = 0; sub < C::SUBS; ++sub) {
         const int u = t * C::SUBS + sub;
-        mbar_wait(mbar + 8 * (u & 1), (u >> 1) & 1);
+        mbar_wait(mbar + mb_full(u % C::NBUF), (u / C::NBUF) & 1);
         if (sub == 0) {
           const uint4 iw = lds128(idx_s + (t % kStageBufs) * L::IDX_BYTES + tid * 16);
           iwa[0] = iw.x; iwa[1] = iw.y; iwa[2] = iw.z; iwa[3] = iw.w;
         }
-        lookup_sub<G, kLookupGP<WARPS>>(sub, tab_s + (uint32_t)((u & 1) * C::TAB_BYTES), iwa, rot, sw,
+        lookup_sub<G, kLookupGP<WARPS>>(sub, tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES), iwa, rot, sw,
                                         nneg);
         __syncwarp();
-        if (lane == 0) mbar_arrive(mbar + 16 + 8 * (u & 1));
+        if (lane == 0) mbar_arrive(mbar + mb_empty(u % C::NBUF));
       }
       const bool seg_end = (cur.kt + 1 == cur.seg.kb);
       if (++since_flush >= kFlushTiles || seg_end) {

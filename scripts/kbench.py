@@ -11,6 +11,8 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2512_06443_b200 as v  # noqa: E402
+if os.environ.get("VLUT_LIB"):
+    v.lib_path = os.environ["VLUT_LIB"]
 from paper_2512_06443_b200 import synth  # noqa: E402
 
 R_LU = 148 * 64 * 1965e6  # int16 lookup-adds/s at 128 B/clk/SM, 1965 MHz
