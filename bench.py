@@ -287,14 +287,29 @@ def main():
             v.quantize(x, q=q, scale=s, stream=stream)
             v.mpgemm_ws(pw, q, s, synth.W_SCALE, out=out_r, ws=ws, stream=stream)
             dist.all_gather_into_tensor(out_full, out_r)
-            for _ in range(2):  # both alternating buffers
-                buf, peers, barrier = peer.get(M, N, dev)
-                v.mpgemm_allgather(pw, q, s, synth.W_SCALE, buf, rank * Ms, peers, stream=stream)
-                barrier()
-                okt = torch.tensor([1 if torch.equal(buf, out_full) else 0], device=dev)
-                dist.all_reduce(okt, op=dist.ReduceOp.MIN)
-                if int(okt.item()) != 1:
-                    raise RuntimeError("fused all-gather result differs from NCCL all-gather")
+            def validate(pe):
+                for _ in range(2):  # both alternating buffers
+                    buf, target, peers, barrier = pe.get(M, N, dev)
+                    buf.fill_(float("nan"))
+                    torch.cuda.synchronize()
+                    dist.barrier()
+                    v.mpgemm_allgather(pw, q, s, synth.W_SCALE, target, rank * Ms, peers,
+                                       stream=stream)
+                    barrier()
+                    torch.cuda.synchronize()
+                    okt = torch.tensor([1 if torch.equal(buf, out_full) else 0], device=dev)
+                    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+                    if int(okt.item()) != 1:
+                        raise RuntimeError("fused all-gather result differs from NCCL")
+            try:
+                validate(peer)
+                gather = "p2p " + peer.transport(M, N, dev)
+            except Exception:
+                if peer.transport(M, N, dev) != "multicast":
+                    raise
+                peer = PeerOutputs(mode="unicast")  # multicast failed: unicast peer stores
+                validate(peer)
+                gather = "p2p unicast (multicast failed validation)"
         except Exception as ex:  # keep measuring, on the NCCL path
             gather = f"nccl (p2p unavailable: {str(ex)[:120]})"
             peer = None
@@ -302,8 +317,8 @@ def main():
     def step():
         v.quantize(x, q=q, scale=s, stream=stream)
         if peer is not None:
-            buf, peers, barrier = peer.get(M, N, dev)
-            v.mpgemm_allgather(pw, q, s, synth.W_SCALE, buf, rank * Ms, peers, stream=stream)
+            buf, target, peers, barrier = peer.get(M, N, dev)
+            v.mpgemm_allgather(pw, q, s, synth.W_SCALE, target, rank * Ms, peers, stream=stream)
             barrier()
             return
         v.mpgemm_ws(pw, q, s, synth.W_SCALE, out=out_r, ws=ws, stream=stream)

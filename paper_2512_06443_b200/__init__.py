@@ -559,13 +559,16 @@ def mpgemm_scalar_lut(W: PackedWeights, A, a_scale, w_scale: float, out=None,
 # ---------------------------------------------------------------- fused all-gather (a8)
 def mpgemm_allgather(W: PackedWeights, A, a_scale, w_scale: float, out_full, row0: int,
                      peer_ptrs=(), stream=None):
-    """Shard rows [row0, row0 + W.M) of out_full [M_total][N], stored locally
-    and to every peer buffer in ``peer_ptrs`` (device pointers mapped into
-    this process) by the K1 epilogue.  Returns out_full."""
+    """Shard rows [row0, row0 + W.M) of out_full [M_total][N] (a tensor or a
+    raw device address, e.g. a multicast address), stored there and to every
+    peer buffer in ``peer_ptrs`` (device pointers mapped into this process)
+    by the K1 epilogue.  Returns out_full."""
     K, N = A.shape
     arr = (ctypes.c_void_p * max(1, len(peer_ptrs)))(*[ctypes.c_void_p(int(x)) for x in peer_ptrs])
+    # out_full: a tensor, or a raw device address (e.g. a multicast address)
+    out_p = ctypes.c_void_p(int(out_full)) if isinstance(out_full, int) else _dev_ptr(out_full)
     _check(lib().vlut_mpgemm_allgather(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(a_scale),
-                                       float(w_scale), _dev_ptr(out_full), W.M, K, N, int(row0),
+                                       float(w_scale), out_p, W.M, K, N, int(row0),
                                        ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p)),
                                        len(peer_ptrs), _stream_ptr(stream)))
     return out_full

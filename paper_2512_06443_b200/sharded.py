@@ -47,35 +47,68 @@ class PeerOutputs:
     its row shard into all of them.  Two buffers per N alternate between
     calls: a rank can only be one call ahead of a peer (every call ends with a
     cross-GPU barrier on the stream), so it never overwrites a buffer a peer
-    is still reading.  Plumbing only -- the stores are the kernel's."""
+    is still reading.  Plumbing only -- the stores are the kernel's.
 
-    def __init__(self, group=None):
+    mode "multicast" (NVLS, when the device supports multicast objects): the
+    kernel stores each unit ONCE to the buffer's multicast address and the
+    NVSwitch replicates it into every rank's copy (the local one included);
+    mode "unicast": one store to the local copy plus one per peer."""
+
+    def __init__(self, group=None, mode: str = "auto"):
         import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm_mem
         self.symm = symm_mem
         self.group = group or dist.group.WORLD
         self.rank = dist.get_rank(self.group)
         self.world = dist.get_world_size(self.group)
+        self.mode = mode
         self._bufs = {}
         self._turn = {}
 
+    def _multicast_ok(self, device) -> bool:
+        if self.mode == "unicast":
+            return False
+        try:
+            from torch._C._distributed_c10d import _SymmetricMemory
+            from torch._C._autograd import DeviceType
+            import torch
+            idx = torch.device(device).index
+            if idx is None:
+                idx = torch.cuda.current_device()
+            return bool(_SymmetricMemory.has_multicast_support(DeviceType.CUDA, idx))
+        except Exception:
+            return False
+
     def get(self, M: int, N: int, device):
-        """(buffer [M][N] fp32, [peer device pointers], barrier) for this call."""
+        """(buffer [M][N] fp32, store target (device pointer), [peer device
+        pointers], barrier) for this call: the kernel stores to the target
+        (the local copy, or the multicast address) and to each peer."""
         key = (M, N)
         if key not in self._bufs:
             import torch
+            mc = self._multicast_ok(device)
             pair = []
             for _ in range(2):
                 t = self.symm.empty((M, N), dtype=torch.float32, device=device)
                 h = self.symm.rendezvous(t, self.group)
-                peers = [int(h.buffer_ptrs[r]) for r in range(self.world) if r != self.rank]
-                pair.append((t, peers, h))
+                mptr = int(getattr(h, "multicast_ptr", 0) or 0) if mc else 0
+                if mptr:
+                    target, peers = mptr, []
+                else:
+                    target = t.data_ptr()
+                    peers = [int(h.buffer_ptrs[r]) for r in range(self.world) if r != self.rank]
+                pair.append((t, target, peers, h))
             self._bufs[key] = pair
             self._turn[key] = 0
         i = self._turn[key]
         self._turn[key] = 1 - i
-        t, peers, h = self._bufs[key][i]
-        return t, peers, (lambda: h.barrier(channel=0))
+        t, target, peers, h = self._bufs[key][i]
+        return t, target, peers, (lambda: h.barrier(channel=0))
+
+    def transport(self, M: int, N: int, device) -> str:
+        _, target, peers, _ = self.get(M, N, device)
+        self.get(M, N, device)  # restore the alternation
+        return "unicast" if (peers or self.world == 1) and target else "multicast"
 
 
 class RowShardedLinear:
@@ -193,9 +226,9 @@ class RowShardedLinear:
             # fused all-gather: the K1 epilogue stores this rank's rows into
             # every rank's copy over NVLink; one cross-GPU barrier completes it
             import paper_2512_06443_b200 as v
-            buf, peer_ptrs, barrier = self.peers.get(self.M, N, dev)
+            buf, target, peer_ptrs, barrier = self.peers.get(self.M, N, dev)
             if self.rows:
-                v.mpgemm_allgather(self.shard, A, a_scale, self.w_scale, buf, self.r0, peer_ptrs)
+                v.mpgemm_allgather(self.shard, A, a_scale, self.w_scale, target, self.r0, peer_ptrs)
             barrier()
             if out is not None:
                 out.copy_(buf)

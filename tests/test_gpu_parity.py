@@ -456,19 +456,22 @@ def test_peer_outputs_symmetric_memory_world1(v):
     os.environ.setdefault("MASTER_PORT", "29531")
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev())
     try:
-        po = PeerOutputs()
-        b0, peers0, bar0 = po.get(128, 64, dev())
-        b1, peers1, bar1 = po.get(128, 64, dev())
-        b2, _, _ = po.get(128, 64, dev())
-        assert peers0 == [] and peers1 == []
-        assert b0.data_ptr() != b1.data_ptr() and b2.data_ptr() == b0.data_ptr()
         W = synth.ternary_weights(128, 256, seed=5)
         x = synth.activations_f32(256, 64, seed=6)
         q, s = oracle.quantize(x)
         pw = v.pack_weights(W, 4, device=dev())
-        v.mpgemm_allgather(pw, to_dev(q), to_dev(s), synth.W_SCALE, b0, 0, peers0)
-        bar0()
-        torch.cuda.synchronize()
-        check_fp32(b0.cpu().numpy(), oracle.gemm_i32(W, q), s, synth.W_SCALE)
+        for mode in ("unicast", "auto"):  # auto: the multicast address when supported
+            po = PeerOutputs(mode=mode)
+            b0, t0, peers0, bar0 = po.get(128, 64, dev())
+            b1, t1, peers1, bar1 = po.get(128, 64, dev())
+            b2, _, _, _ = po.get(128, 64, dev())
+            assert peers0 == [] and peers1 == []
+            assert b0.data_ptr() != b1.data_ptr() and b2.data_ptr() == b0.data_ptr()
+            b0.fill_(float("nan"))
+            v.mpgemm_allgather(pw, to_dev(q), to_dev(s), synth.W_SCALE, t0, 0, peers0)
+            bar0()
+            torch.cuda.synchronize()
+            check_fp32(b0.cpu().numpy(), oracle.gemm_i32(W, q), s, synth.W_SCALE)
+            print(mode, "transport:", po.transport(128, 64, dev()))
     finally:
         dist.destroy_process_group()
