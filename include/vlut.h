@@ -187,9 +187,12 @@ vlut_status vlut_mpgemm_ex(const vlut_packed_weights* W, const int8_t* A,
  * for small N, the K2 lane-slot kernel (split-K through the workspace) by its
  * cost model (plan == NULL) unless plan->streamk / plan->slot forces one.
  *   workspace : device, >= vlut_workspace_bytes() bytes, 16-B aligned, ZEROED
- *               ONCE before its first use (flags are per-launch epochs), and
- *               used by one stream at a time.
- * vlut_workspace_bytes() returns 0 without a CUDA device.
+ *               ONCE before its first use, and used by one stream at a time.
+ *               Regions: stream-K partials and epoch flags (flags are
+ *               per-launch epochs), K2 split-K arrival counters and int32
+ *               accumulators (every K2 launch leaves them zero again; a K2
+ *               split-K launch is cooperative: its CTAs must be co-resident).
+ * vlut_workspace_bytes() returns 0 without a CUDA device (~36 MB on B200).
  */
 size_t vlut_workspace_bytes(void);
 vlut_status vlut_mpgemm_ws(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,
