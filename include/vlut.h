@@ -189,9 +189,10 @@ vlut_status vlut_mpgemm_ex(const vlut_packed_weights* W, const int8_t* A,
  *   workspace : device, >= vlut_workspace_bytes() bytes, 16-B aligned, ZEROED
  *               ONCE before its first use, and used by one stream at a time.
  *               Regions: stream-K partials and epoch flags (flags are
- *               per-launch epochs), K2 split-K arrival counters and int32
- *               accumulators (every K2 launch leaves them zero again; a K2
- *               split-K launch is cooperative: its CTAs must be co-resident).
+ *               per-launch epochs), K2 split-K arrival counts and int32
+ *               accumulators (every K2 launch leaves them zero again) and
+ *               per-tile generation words (monotonic).  A K2 split-K launch
+ *               is cooperative: its CTAs must be co-resident.
  * vlut_workspace_bytes() returns 0 without a CUDA device (~36 MB on B200).
  */
 size_t vlut_workspace_bytes(void);

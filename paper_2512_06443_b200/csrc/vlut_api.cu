@@ -572,6 +572,8 @@ vlut_status run_slot(const vlut_packed_weights* W, const int8_t* A, const float*
     p.ws_cnt = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + slot_cnt_off(d.sms));
     p.ws_acc = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + slot_acc_off(d.sms));
   }
+  p.last_only =
+      ((long long)pl.m_cta * std::min(N, pl.n_cta) * 4 <= vlut::slot::kLastOnlyBytes) ? 1 : 0;
   vlut_status st = dispatch_slot(g, pl.nw, tpw, p, S, (int)NTt, (int)MT,
                                  static_cast<cudaStream_t>(stream));
   if (st != VLUT_OK) return st;

@@ -39,10 +39,13 @@
 //                 int32 tile goes through shared memory; with S > 1 it is
 //                 added into a zero-kept workspace by bulk reduce-add copies
 //                 (cp.reduce.async.bulk .add.s32: one per CTA when its rows
-//                 are contiguous there), the CTAs of the tile meet at an
-//                 acq_rel arrival counter (co-resident: cooperative launch),
-//                 and each finishes 1/S of the tile's elements (epilogue +
-//                 re-zeroing), so no single CTA serialises the epilogue.
+//                 are contiguous there) and the CTAs arrive at an acq_rel
+//                 counter; the last to arrive re-arms it.  Tiles <= 8 KB
+//                 (decode): that last CTA alone finishes the tile (epilogue +
+//                 re-zeroing), the others exit without waiting.  Larger
+//                 tiles: the last one bumps the tile's generation word, the
+//                 CTAs (co-resident: cooperative launch) wait for it and each
+//                 finishes 1/S of the tile, so no single CTA serialises it.
 //                 Integer addition is associative: bit-exact for every split.
 //   epilogue (a6) out = fl((float)acc * fl(a_scale[n] * w_scale)), or raw int32.
 //
@@ -69,6 +72,7 @@ constexpr int kMaxCounters = 8192;                // split-K tiles (2 counters e
 constexpr int kActNMax = 64;                      // activations staged by TMA when N <= 64
 constexpr int kMaxStages = 8;                     // staging ring depth (bytes in flight at N = 1)
 constexpr int kRampStages = 2;                    // stages issued before the first tile lands
+constexpr int kLastOnlyBytes = 8192;              // split-K tiles up to this size: the last CTA finishes them
 
 template <int G, int NW, int TPW>
 struct SL {
@@ -109,7 +113,10 @@ struct SlotParams {
   int acc_only;
   int act_tma;             // 1: A is staged by bulk copies (N <= 64, 16-B aligned A)
   int32_t* ws_acc;         // splits > 1: int32 [M][N], all zero between launches
-  unsigned* ws_cnt;        // splits > 1: per-tile (arrived, done) counters, zero between launches
+  unsigned* ws_cnt;        // splits > 1: per-tile (arrivals, generation) words; arrivals zero
+                           // between launches, generation monotonic
+  int last_only;           // splits > 1: 1 = the last CTA to arrive finishes the whole tile
+                           // (small tiles), 0 = every CTA finishes 1/S of it
 };
 
 __device__ __forceinline__ void red_add_s32(int32_t* p, int32_t v) {
@@ -134,6 +141,11 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
   uint32_t v;
@@ -225,6 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
   const int kt0 = (int)(((long long)rank * p.kg_tiles) / S);
   const int kt1 = (int)(((long long)(rank + 1) * p.kg_tiles) / S);
   const int ntiles = kt1 - kt0;
+  unsigned g0 = 0;  // split-K generation word before this CTA arrives (tid 0)
   VLUT_STAMP(0);
 
   const uint32_t tab_s = smem_u32(smem);
@@ -382,6 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
       const int st = t % L::STAGES;
       mbar_wait(mbar + 32 + 8 * st, (t / L::STAGES) & 1);  // index rows landed
       if (t == 0) VLUT_STAMP(1);
+      if (t == ntiles - 1) VLUT_STAMP(7);
       uint4 v[L::RPL];
 #pragma unroll
       for (int q = 0; q < L::RPL; ++q) {
@@ -481,6 +495,10 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
     }
     fence_proxy_async_smem();  // the tile is read by bulk-reduce copies
     pdl_wait();  // epilogue reads a_scale / the workspace of the previous kernel
+    // the tile's generation before this CTA arrives (it cannot move before
+    // then; read after pdl_wait so a previous launch's bump is visible)
+    if (tid == 0 && S > 1 && !p.last_only)
+      g0 = ld_relaxed_gpu(p.ws_cnt + 2 * (blockIdx.z * gridDim.y + blockIdx.y) + 1);
   }
   pdl_launch_dependents();
   __syncthreads();  // int32 tile complete
@@ -520,23 +538,39 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
     }
     fence_proxy_async_global();
     __syncthreads();
-    // (2) arrive, then wait for the tile's S CTAs (co-resident: cooperative
-    // launch).  Bounded spin: a schedule bug must fail loudly, never hang.
+    // (2) arrive (the release of the acq_rel add covers this CTA's reductions:
+    // completed, and ordered before it by the proxy fence).  The last CTA of
+    // the tile to arrive re-arms the count.  last_only (small tiles): that CTA
+    // alone goes on and finishes the whole tile, the others exit -- no
+    // waiting.  Otherwise it also bumps the tile's generation word (release)
+    // and every CTA (co-resident: cooperative launch) waits for that and
+    // finishes 1/S of the tile.  Bounded spin: a schedule bug must fail
+    // loudly, never hang.
     unsigned* cnt = p.ws_cnt + 2 * (blockIdx.z * gridDim.y + blockIdx.y);
+    __shared__ int s_last;
     if (tid == 0) {
-      __threadfence();  // cumulative: every reduction of this CTA precedes the arrival
-      atom_add_acq_rel(cnt, 1u);
-      unsigned spins = 0;
-      while (ld_acquire_gpu(cnt) < (unsigned)S) {
-        __nanosleep(32);
-        if (++spins > (1u << 26)) __trap();
+      const bool last = atom_add_acq_rel(cnt, 1u) == (unsigned)(S - 1);
+      if (last) {
+        cnt[0] = 0u;  // all S arrivals are in: re-arm for the next launch
+        if (!p.last_only) st_release_gpu(cnt + 1, g0 + 1u);  // ordered after the reset
+      } else if (!p.last_only) {
+        unsigned spins = 0;
+        while (ld_acquire_gpu(cnt + 1) == g0) {
+          __nanosleep(32);
+          if (++spins > (1u << 26)) __trap();
+        }
       }
+      s_last = last ? 1 : 0;
     }
     __syncthreads();
     VLUT_STAMP(5);
     // (3) this CTA finishes elements [e_begin, e_end) of the tile
-    e_begin = (int)(((long long)elems * rank) / S);
-    e_end = (int)(((long long)elems * (rank + 1)) / S);
+    if (p.last_only) {
+      if (!s_last) return;
+    } else {
+      e_begin = (int)(((long long)elems * rank) / S);
+      e_end = (int)(((long long)elems * (rank + 1)) / S);
+    }
   }
   if (warp < kLW) {
     // batches of EB elements per thread: every workspace load of a batch is
@@ -568,18 +602,6 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
           const float sc = __fmul_rn(__ldg(p.a_scale + n0 + c), p.w_scale);
           reinterpret_cast<float*>(p.out)[o] = __fmul_rn((float)a[b], sc);
         }
-      }
-    }
-  }
-  if (S > 1) {
-    // (4) the last CTA through re-arms both counters for the next launch
-    // (every CTA of the tile has passed its wait by then)
-    __syncthreads();
-    if (tid == 0) {
-      unsigned* cnt = p.ws_cnt + 2 * (blockIdx.z * gridDim.y + blockIdx.y);
-      if (atom_add_acq_rel(cnt + 1, 1u) == (unsigned)(S - 1)) {
-        cnt[0] = 0u;
-        cnt[1] = 0u;
       }
     }
   }

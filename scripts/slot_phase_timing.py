@@ -10,7 +10,7 @@ sys.path.insert(0, ROOT)
 from paper_2512_06443_b200 import build as B
 lib = "/tmp/libvlut_timing.so"
 subprocess.check_call([B.nvcc()] + [f for f in B.NVCC_FLAGS if f != "-v" and f != "-Xptxas"] +
-                      ["-DVLUT_TIMING", "-o", lib] + B.SOURCES)
+                      ["-DVLUT_TIMING", "-o", lib] + os.environ.get("VLUT_EXTRA", "").split() + B.SOURCES)
 import paper_2512_06443_b200 as v
 v.lib_path = lib
 from paper_2512_06443_b200 import synth
@@ -36,7 +36,7 @@ for it in range(4):
 t = buf.view(-1, 8).cpu().numpy().astype(np.int64)
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
-names = ["entry", "idx0", "table0", "loop_end", "tile_smem", "arrived", "stored"]
+names = os.environ.get("NAMES", "entry idx0 table0 loop_end tile_smem arrived stored idx_last").split()
 print("CTAs", len(t), "rc", rc, v.plan_ws(M, K, N, g))
 for i, n in enumerate(names):
     col = t[:, i]
