@@ -1141,7 +1141,7 @@ vlut_status vlut_quantize(const float* x, const float* y, int K, int N, int8_t* 
   // when possible (<= 8, portable), and >= ~2 waves of CTAs over the GPU.
   const long long tok_blocks = (N + vlut::kQTok - 1) / vlut::kQTok;
   int CL = 1;
-  while (CL < 8 && ((long long)K > (long long)CL * 64 * vlut::kQCache || tok_blocks * CL < 296))
+  while (CL < 8 && ((long long)K > (long long)CL * vlut::kQRows * vlut::kQCache || tok_blocks * CL < 296))
     CL *= 2;
   if (CL > K) CL = 1;
   if (tok_blocks > 65535) return fail(VLUT_ERR_SHAPE, "N too large");

@@ -15,9 +15,13 @@ namespace vlut {
 // and the codes are written from the registers (rows beyond the register
 // cache are re-read).  IEEE single ops only (no fast math):
 //   s = amax / 127 (1 if amax == 0), q = clamp(roundf(x / s), -127, 127).
-constexpr int kQThreads = 256;   // 64 rows x 4 float4 columns per pass
-constexpr int kQTok = 16;        // tokens per cluster
-constexpr int kQCache = 12;      // float4 register cache per thread
+#ifndef VLUT_QTHREADS
+#define VLUT_QTHREADS 512
+#endif
+constexpr int kQThreads = VLUT_QTHREADS;  // kQRows rows x 4 float4 columns per pass
+constexpr int kQRows = kQThreads / 4;
+constexpr int kQTok = 16;                 // tokens per cluster
+constexpr int kQCache = 768 / kQRows;     // float4 register cache per thread (768 rows per CTA)
 
 // One operand's float4 (4 tokens of row k), zeros outside N.
 template <bool ALIGNED>
@@ -69,7 +73,7 @@ __global__ void __launch_bounds__(kQThreads)
     vlut_quantize_kernel(const float* __restrict__ x, const float* __restrict__ y, int K, int N,
                          int8_t* __restrict__ q, float* __restrict__ scale) {
   __shared__ float red[kQThreads / 32][kQTok];
-  __shared__ float cta_amax[kQTok];
+  __shared__ float all_max[8][kQTok];  // [cluster rank][token]: every CTA's maxima
   __shared__ float s_scale[kQTok];
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
@@ -77,7 +81,7 @@ __global__ void __launch_bounds__(kQThreads)
   const int rank = (int)cluster.block_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int col = tid & 3;              // float4 column within the 16 tokens
-  const int rsub = tid >> 2;            // row within a 64-row pass
+  const int rsub = tid >> 2;            // row within a kQRows-row pass
   const int n = blockIdx.y * kQTok + col * 4;
   const int k_begin = (int)(((long long)rank * K) / CL);
   const int k_end = (int)(((long long)(rank + 1) * K) / CL);
@@ -92,7 +96,7 @@ __global__ void __launch_bounds__(kQThreads)
   // right behind each load would serialise the DRAM round trips)
 #pragma unroll
   for (int i = 0; i < kQCache; ++i) {
-    const int k = k_begin + rsub + 64 * i;
+    const int k = k_begin + rsub + kQRows * i;
     cache[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (k < k_end && n < N) cache[i] = q_load1<ALIGNED>(x, k, N, n);
   }
@@ -100,7 +104,7 @@ __global__ void __launch_bounds__(kQThreads)
     float4 yc[kQCache];
 #pragma unroll
     for (int i = 0; i < kQCache; ++i) {
-      const int k = k_begin + rsub + 64 * i;
+      const int k = k_begin + rsub + kQRows * i;
       yc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (k < k_end && n < N) yc[i] = q_load1<ALIGNED>(y, k, N, n);
     }
@@ -112,7 +116,7 @@ __global__ void __launch_bounds__(kQThreads)
     m[0] = fmaxf(m[0], fabsf(cache[i].x)); m[1] = fmaxf(m[1], fabsf(cache[i].y));
     m[2] = fmaxf(m[2], fabsf(cache[i].z)); m[3] = fmaxf(m[3], fabsf(cache[i].w));
   }
-  for (int k = k_begin + rsub + 64 * kQCache; k < k_end; k += 64) {
+  for (int k = k_begin + rsub + kQRows * kQCache; k < k_end; k += kQRows) {
     if (n >= N) break;
     const float4 a = q_load<ALIGNED>(x, y, k, N, n);
     m[0] = fmaxf(m[0], fabsf(a.x)); m[1] = fmaxf(m[1], fabsf(a.y));
@@ -129,38 +133,35 @@ __global__ void __launch_bounds__(kQThreads)
     for (int i = 0; i < 4; ++i) red[warp][lane * 4 + i] = m[i];
   }
   __syncthreads();
+  // push model: the 16 combining threads store this CTA's maxima into slot
+  // `rank` of every cluster CTA's table (DSMEM stores), one cluster barrier
+  // (release / acquire), then every CTA reduces its own table locally -- no
+  // remote round trip, no second barrier (no remote access after it)
   if (tid < kQTok) {
     float a = red[0][tid];
 #pragma unroll
     for (int w = 1; w < kQThreads / 32; ++w) a = fmaxf(a, red[w][tid]);
-    cta_amax[tid] = a;
+    for (int r = 0; r < CL; ++r) cluster.map_shared_rank(&all_max[0][0], r)[rank * kQTok + tid] = a;
   }
   VLUT_STAMP(3);
-  cluster.sync();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   VLUT_STAMP(4);
-  // 16 threads combine the cluster's partial maxima (DSMEM), the rest wait
   if (tid < kQTok) {
     float a = 0.f;
-    float part[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) part[r] = (r < CL) ? cluster.map_shared_rank(cta_amax, r)[tid] : 0.f;
-#pragma unroll
-    for (int r = 0; r < 8; ++r) a = fmaxf(a, part[r]);
+    for (int r = 0; r < CL; ++r) a = fmaxf(a, all_max[r][tid]);
     const float sc = (a == 0.f) ? 1.f : __fdiv_rn(a, 127.f);
     s_scale[tid] = sc;
     if (rank == 0 && blockIdx.y * kQTok + tid < N) scale[blockIdx.y * kQTok + tid] = sc;
   }
-  // this CTA's remote reads are done once its 16 readers pass here: arrive
-  // early, wait only before exit (keeps cta_amax alive for the other CTAs)
   __syncthreads();
   VLUT_STAMP(5);
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
   float s[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) s[i] = s_scale[col * 4 + i];
 #pragma unroll
   for (int i = 0; i < kQCache; ++i) {
-    const int k = k_begin + rsub + 64 * i;
+    const int k = k_begin + rsub + kQRows * i;
     if (k < k_end && n < N) {
       const size_t o = (size_t)k * N + n;
       const int8_t c0 = q_code(cache[i].x, s[0]), c1 = q_code(cache[i].y, s[1]);
@@ -175,15 +176,13 @@ __global__ void __launch_bounds__(kQThreads)
       }
     }
   }
-  for (int k = k_begin + rsub + 64 * kQCache; k < k_end; k += 64) {
+  for (int k = k_begin + rsub + kQRows * kQCache; k < k_end; k += kQRows) {
     if (n >= N) break;
     const float4 a = q_load<ALIGNED>(x, y, k, N, n);
     const float v[4] = {a.x, a.y, a.z, a.w};
     for (int t = 0; t < 4 && n + t < N; ++t) q[(size_t)k * N + n + t] = q_code(v[t], s[t]);
   }
   VLUT_STAMP(6);
-  asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
-  VLUT_STAMP(7);
 }
 
 // ---------------------------------------------------------------- K3t: fused transposition (f3)
