@@ -51,8 +51,24 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--plans", action="store_true")
     ap.add_argument("--ws", action="store_true", help="workspace path (stream-K allowed)")
+    ap.add_argument("--shape", type=int, nargs=4, metavar=("M", "K", "N", "G"),
+                    help="sweep every K1 plan (cluster w x s, stream-K w) on this shape only")
     a = ap.parse_args()
     rows = []
+    if a.shape:
+        M, K, N, g = a.shape
+        rows.append(time_one(M, K, N, g, ws=True))
+        for w in (8, 12, 16):
+            rows.append(time_one(M, K, N, g, plan=v.LaunchPlan(w, 1, streamk=1), ws=True))
+            for sp in range(1, 9):
+                try:
+                    rows.append(time_one(M, K, N, g, plan=v.LaunchPlan(w, sp)))
+                except Exception as e:  # plan not launchable for this shape
+                    print(f"w{w} s{sp}: {e}")
+        for r in rows:
+            print(f"M={r['M']:6d} K={r['K']:6d} N={r['N']:5d} g={r['g']} plan={r['plan'][:24]:24s} "
+                  f"us={r['us']:9.2f} frac={r['frac_roof']:.3f}")
+        return
     rows.append(time_one(6912, 2560, 256, 4, p_zero=0.4, ws=a.ws))
     for N in (256, 1024, 4096):
         for g in (4, 5):
