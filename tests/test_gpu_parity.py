@@ -62,6 +62,38 @@ def test_quantize_bit_exact(v, K, N):
     assert np.array_equal(q.cpu().numpy(), qr)
 
 
+def test_quantize_half_boundaries(v):
+    """Values whose quotient x / s sits on, or a few ulps around, a k + 1/2
+    rounding boundary for every k in [-127, 126] and several scales: the
+    kernel's reciprocal fast path must hand all of these to the IEEE
+    division (round half away from zero of fl(x / s), as the oracle)."""
+    rng = synth.rng(77)
+    N = 24
+    amax = np.float32(rng.uniform(0.01, 50.0, N)).astype(np.float32)
+    amax[0], amax[1] = np.float32(127.0), np.float32(1.0)
+    cols = []
+    for n in range(N):
+        s = np.float32(amax[n] / np.float32(127.0))
+        col = [amax[n], -amax[n]]
+        for k in range(-127, 127):
+            b = np.float32(np.float32(k + 0.5) * s)
+            for d in (-3, -2, -1, 0, 1, 2, 3):
+                x = b
+                for _ in range(abs(d)):
+                    x = np.nextafter(x, np.float32(np.inf if d > 0 else -np.inf), dtype=np.float32)
+                if abs(x) <= amax[n]:
+                    col.append(x)
+        cols.append(np.array(col, np.float32))
+    K = max(len(c) for c in cols)
+    x = np.zeros((K, N), np.float32)
+    for n, c in enumerate(cols):
+        x[:len(c), n] = c
+    q, s = v.quantize(to_dev(x))
+    qr, sr = oracle.quantize(x)
+    assert np.array_equal(s.cpu().numpy().view(np.int32), sr.view(np.int32))
+    assert np.array_equal(q.cpu().numpy(), qr)
+
+
 def test_quantize_mul_bit_exact(v):
     K, N = 700, 96
     a = synth.activations_f32(K, N, seed=1)
