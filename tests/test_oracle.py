@@ -324,6 +324,31 @@ def test_config5_layer_smoke():
     assert np.all(s > 0) and np.abs(q.astype(int)).max() <= 127
 
 
+def test_config5_layer_identity_closed_form():
+    """Pin of the config-5 glue (reading c14) by a special case with a closed
+    form: identity weights (ternary 0/1) make every linear pass its input
+    through up to the per-token scales, so x' = Q(Q(h)) with h = u * u and
+    u = x: the final codes are round_half_away(x^2 / 127) for int8 codes x
+    whose column reaches |x| = 127 (x^2 / 127 kept away from .5 ties), and
+    the input's sign is lost.  A dropped re-quantization, the product taken
+    before Q, a wrong q_rows slice or a sign error all change the codes."""
+    K, N = 64, 5
+    rng = synth.rng(11)
+    xq = rng.integers(-127, 128, size=(K, N)).astype(np.int8)
+    xq[0, :] = 127
+    xq[1, :] = -127
+    frac = (xq.astype(np.int64) ** 2 % 127) / 127.0
+    xq[np.abs(frac - 0.5) < 0.02] = 3  # 9 / 127 is far from a tie
+    xs = np.full(N, 0.05, np.float32)
+    I = np.eye(K, dtype=np.int8)
+    W_qkv = np.concatenate([I, np.zeros((2 * K, K), np.int8)])  # rows K.. are ignored
+    q, s = oracle.config5_layer((W_qkv, I, I, I, I), synth.W_SCALE, xq, xs, q_rows=K)
+    x2 = xq.astype(np.int64) ** 2
+    expect = (2 * x2 + 127) // 254  # round half away of x^2 / 127 (non-negative)
+    assert np.array_equal(q.astype(np.int64), expect)
+    assert np.all(q >= 0)
+
+
 # ------------------------------------------------------------------ mixed g=5/g=4 schedule (f2)
 def test_group_schedule_examples():
     # S:121-124: (K=20, I1) -> all 5s; K=4096 mixed -> 816 fives then 4 fours,
