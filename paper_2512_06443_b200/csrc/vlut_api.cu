@@ -141,7 +141,8 @@ vlut_status encode_a_map(CUtensorMap* map, const int8_t* A, int K, int N, int g)
 }
 
 // ------------------------------------------------------------ planner
-int smem_bytes_for(int g, int warps) {
+int smem_bytes_for(int g, int warps, int rpt = 1) {
+  if (rpt == 2) return g == 4 ? vlut::Layout<4, 12, 2>::SMEM : vlut::Layout<5, 12, 2>::SMEM;
   if (g == 4) {
     if (warps == 8) return vlut::Layout<4, 8>::SMEM;
     if (warps == 12) return vlut::Layout<4, 12>::SMEM;
@@ -218,11 +219,11 @@ int active_clusters_for(int g, int warps, int S) {
 inline bool valid_split(int warps, int S) { return warps > 0 && S >= 1 && S <= 8; }
 
 // Workspace layout (caller-provided, zeroed once):
-//   [0, SK)             stream-K int32 partials [sms][512 x 64]
+//   [0, SK)             stream-K int32 partials [sms][768 x 64] (m_cta <= 768)
 //   [SK, SK + 4096)     stream-K epoch flags
 //   [.., + 64 KB)       K2 split-K arrival counters (kept zero between launches)
 //   [.., + 16 MB)       K2 split-K int32 accumulators [M][N] (kept zero)
-size_t sk_part_bytes(int sms) { return (size_t)sms * 512 * 64 * 4; }
+size_t sk_part_bytes(int sms) { return (size_t)sms * 768 * 64 * 4; }  // max m_cta 768
 size_t slot_cnt_off(int sms) { return sk_part_bytes(sms) + 4096; }
 size_t slot_acc_off(int sms) { return slot_cnt_off(sms) + (size_t)vlut::slot::kMaxCounters * 8; }
 constexpr size_t kSlotAccBytes = (size_t)16 << 20;
@@ -236,15 +237,23 @@ double plan_sk(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
   const int NT = (N + vlut::kNcta - 1) / vlut::kNcta;
   const int half_rows = (pow3i(g) + 1) / 2;
   double best_cost = 1e300;
-  const int warps_opts[3] = {16, 12, 8};
-  for (int wi = 0; wi < 3; ++wi) {
+  // (warps, rows per lookup thread): 12 warps x 2 rows = 768 rows share each table
+  const int warps_opts[4] = {16, 12, 8, 12};
+  const int rpt_opts[4] = {1, 1, 1, 2};
+  for (int wi = 0; wi < 4; ++wi) {
     const int warps = warps_opts[wi];
-    const int mcta = 32 * warps;
+    const int rpt = rpt_opts[wi];
+    if (rpt == 2 && getenv("VLUT_NO_RPT2")) continue;
+    const int mcta = 32 * warps * rpt;
     const long long MT = (M + mcta - 1) / mcta;
     const long long U = MT * NT * kgt;
     const long long grid = U < sms ? U : sms;
     const double units = (double)((U + grid - 1) / grid);
-    double cost = units * VLUT_KG_TILE * (double)(mcta + half_rows);
+    // two rows per thread: 12 warps with one group per load batch keep the
+    // pipe a little less busy than 16 warps (measured: ~5 % per lookup row at
+    // g = 4, ~1 % at g = 5, where the halved table-build share dominates)
+    const double row_cost = rpt == 2 ? (g == 4 ? 1.05 : 1.01) : 1.0;
+    double cost = units * VLUT_KG_TILE * ((double)mcta * row_cost + half_rows);
     cost += 6000.0;                             // start + last epilogue
     cost += (double)mcta * 256.0 * 3.0 / 64.0;  // partial write + read + output
     // the owner of a split tile reads every producer's int32 partial
@@ -259,7 +268,7 @@ double plan_sk(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
       best->m_cta = mcta;
       best->n_cta = vlut::kNcta;
       best->grid_ctas = (int)grid;
-      best->smem_bytes = smem_bytes_for(g, warps);
+      best->smem_bytes = smem_bytes_for(g, warps, rpt);
       best->streamk = 1;
     }
   }
@@ -461,11 +470,11 @@ vlut_status launch_k1(const vlut::Params& p, int S, int NT, int MT, cudaStream_t
   return VLUT_OK;
 }
 
-template <int G, int WARPS, bool ACC>
+template <int G, int WARPS, bool ACC, int RPT = 1>
 vlut_status launch_sk(const vlut::Params& p, const vlut::SkParams& sk, int grid,
                       cudaStream_t st) {
-  using L = vlut::Layout<G, WARPS>;
-  auto kern = vlut::vlut_mpgemm_sk_kernel<G, WARPS, ACC>;
+  using L = vlut::Layout<G, WARPS, RPT>;
+  auto kern = vlut::vlut_mpgemm_sk_kernel<G, WARPS, RPT, ACC>;
   static std::once_flag flags[64];
   static cudaError_t errs[64];
   int dev = 0;
@@ -489,8 +498,13 @@ vlut_status launch_sk(const vlut::Params& p, const vlut::SkParams& sk, int grid,
 }
 
 template <bool ACC>
-vlut_status dispatch_sk(int g, int warps, const vlut::Params& p, const vlut::SkParams& sk,
+vlut_status dispatch_sk(int g, int warps, int rpt, const vlut::Params& p, const vlut::SkParams& sk,
                         int grid, cudaStream_t st) {
+  if (rpt == 2) {
+    if (warps == 12) return g == 4 ? launch_sk<4, 12, ACC, 2>(p, sk, grid, st)
+                                   : launch_sk<5, 12, ACC, 2>(p, sk, grid, st);
+    return fail(VLUT_ERR_UNSUPPORTED, "two rows per thread: 12 warps only");
+  }
   if (g == 4) {
     if (warps == 8) return launch_sk<4, 8, ACC>(p, sk, grid, st);
     if (warps == 12) return launch_sk<4, 12, ACC>(p, sk, grid, st);
@@ -615,6 +629,12 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
                   plan.splits);
     if (plan.streamk && (!ws || acc_in || out_t))
       return fail(VLUT_ERR_INVALID_ARGUMENT, "stream-K plan needs a workspace and [M][N] output");
+    // m_cta selects the rows per lookup thread: 0 or 32 * warps -> 1; 64 * warps
+    // -> 2 (stream-K with 12 warps only)
+    if (plan.m_cta && plan.m_cta != 32 * plan.warps &&
+        !(plan.m_cta == 64 * plan.warps && plan.warps == 12 && plan.streamk))
+      return fail(VLUT_ERR_UNSUPPORTED, "m_cta=%d: 32*warps, or 768 with 12 warps stream-K",
+                  plan.m_cta);
   } else {
     double c_best = plan_for(M, K, N, W->g, d.sms, &plan);
     if (ws && !acc_in && !out_t) {
@@ -641,7 +661,8 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
                 sk_workspace_bytes(d.sms));
   if (plan.streamk && (((uintptr_t)ws) & 15)) return fail(VLUT_ERR_MISALIGNED, "workspace not 16-B aligned");
   if (plan.splits > W->kg_tiles) plan.splits = 1;
-  const int smem = smem_bytes_for(W->g, plan.warps);
+  const int rpt = (plan.streamk && plan.m_cta == 64 * plan.warps) ? 2 : 1;
+  const int smem = smem_bytes_for(W->g, plan.warps, rpt);
   if (smem > d.smem_optin)
     return fail(VLUT_ERR_UNSUPPORTED, "needs %d B shared memory, device allows %d", smem,
                 d.smem_optin);
@@ -674,7 +695,7 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
   p.amax_out = amax_out;
   p.amax_rows = amax_rows;
   p.out_vec4 = ((out_t ? M : N) % 4 == 0 && (((uintptr_t)out) & 15) == 0) ? 1 : 0;
-  const int mcta = 32 * plan.warps;
+  const int mcta = 32 * plan.warps * rpt;
   const long long NT = (N + vlut::kNcta - 1) / vlut::kNcta;
   const long long MT = (M + mcta - 1) / mcta;
   if (NT > 65535 || MT > 65535) return fail(VLUT_ERR_SHAPE, "grid too large");
@@ -691,8 +712,8 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
     if (e == 0) e = ++epoch;
     sk.epoch = e;
     const int grid = (int)(sk.U < d.sms ? sk.U : d.sms);
-    st = acc_only ? dispatch_sk<true>(W->g, plan.warps, p, sk, grid, s)
-                  : dispatch_sk<false>(W->g, plan.warps, p, sk, grid, s);
+    st = acc_only ? dispatch_sk<true>(W->g, plan.warps, rpt, p, sk, grid, s)
+                  : dispatch_sk<false>(W->g, plan.warps, rpt, p, sk, grid, s);
     if (st != VLUT_OK) return st;
     return ok();
   }

@@ -85,12 +85,18 @@ struct Cfg {
 constexpr int kBuilderWarps = 4;
 constexpr int kTmemCols = 256;  // int32 accumulators: 64 columns per 4 lookup warps
 
-template <int G, int WARPS>
+// RPT = output rows per lookup thread: 1 (K1, both schedules) or 2 (the
+// stream-K variant with 12 lookup warps: 768 rows share every table, halving
+// the table-build share of the shared-memory pipe).
+template <int G, int WARPS, int RPT = 1>
 struct Layout {
-  static constexpr int THREADS = (WARPS + kBuilderWarps) * 32;
-  static constexpr int BUILDER0 = WARPS * 32;             // first builder thread
-  static constexpr int MCTA = WARPS * 32;                 // output rows per CTA
-  static constexpr int RED_BYTES = MCTA * kNcta * 4;      // int32 reduction tile
+  static_assert(RPT == 1 || RPT == 2, "one or two rows per lookup thread");
+  static constexpr int NLT = WARPS * 32;                  // lookup threads
+  static constexpr int THREADS = NLT + kBuilderWarps * 32;
+  static constexpr int BUILDER0 = NLT;                    // first builder thread
+  static constexpr int MCTA = NLT * RPT;                  // output rows per CTA
+  static constexpr int RED_BYTES = NLT * kNcta * 4;       // int32 tile of one row block
+  static constexpr int TMEM_COLS = 256 * RPT;             // 64 columns per 4 warps per row block
   static constexpr int TAB_REGION = Cfg<G>::NBUF * Cfg<G>::TAB_BYTES > RED_BYTES
                                         ? Cfg<G>::NBUF * Cfg<G>::TAB_BYTES : RED_BYTES;
   static constexpr int IDX_OFF = TAB_REGION;
@@ -297,11 +303,11 @@ struct alignas(64) Params {
 // ---------------------------------------------------------------- staging (a2)
 // Issued by the builder threads (bt in [0, 128)).  what: 1 = index vectors,
 // 2 = activations, 3 = both; a commit group is closed after the activations.
-template <int G, int WARPS>
+template <int G, int WARPS, int RPT = 1>
 __device__ __forceinline__ void stage_tile(const Params& p, int kt, int buf, int m0, int n0,
                                            uint8_t* smem, int bt, int what) {
   using C = Cfg<G>;
-  using L = Layout<G, WARPS>;
+  using L = Layout<G, WARPS, RPT>;
   constexpr int NB = kBuilderWarps * 32;
   if (what & 1) {
     // index vectors: one 16-byte row per CTA row (rows past m_pad -> zero fill)
@@ -369,12 +375,12 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
-template <int G, int WARPS>
+template <int G, int WARPS, int RPT = 1>
 __device__ __forceinline__ void stage_tile_bulk(const Params& p, int kt, int buf, int m0, int n0,
                                                 uint8_t* smem, int bt, uint32_t stg_mbar,
                                                 bool do_idx, bool do_act, bool arm) {
   using C = Cfg<G>;
-  using L = Layout<G, WARPS>;
+  using L = Layout<G, WARPS, RPT>;
   constexpr int NB = kBuilderWarps * 32;
   const int idx_rows = max(0, min(L::MCTA, p.m_pad - m0));
   const int k0 = kt * kKgTile * G;
@@ -466,6 +472,10 @@ __device__ __forceinline__ void build_tables(uint32_t tab_s, uint32_t a_s, int g
 // ---------------------------------------------------------------- lookups (a4)
 template <int WARPS>
 constexpr int kLookupGP = (WARPS >= 16) ? 1 : 2;
+// two rows per thread: one group per load batch (the second row's
+// accumulators take the registers of the second batch)
+template <int WARPS, int RPT>
+constexpr int kLookupGP2 = (RPT > 1) ? 1 : kLookupGP<WARPS>;
 
 // Groups [SUB*GS, SUB*GS+GS) of the K-tile whose index vector is iwa.
 // GP = groups per load batch: 2 (16 LDS.128 in flight, half the negations on

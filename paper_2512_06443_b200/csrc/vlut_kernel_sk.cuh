@@ -95,18 +95,18 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 
 // Segment epilogue of K1-SK, kept out of the lookup loop's register
 // allocation (__noinline__): full tiles and producers straight from TMEM (one
-// row per thread, four 16-column chunks); the owner (always the CTA's last
-// segment, so the table region is free) through a shared int32 tile and a
-// flat, coalesced reduction of the producers' partials.
-template <int G, int WARPS, bool ACC_ONLY>
+// row per thread and row block, four 16-column chunks); the owner (always the
+// CTA's last segment, so the table region is free) through a shared int32
+// tile -- one row block of NLT rows at a time -- and a flat, coalesced
+// reduction of the producers' partials.
+template <int G, int WARPS, int RPT, bool ACC_ONLY>
 __device__ __forceinline__ void sk_epilogue(const Params& p, const SkParams& sk, const SkSeg sg,
                                          int KT, int cta, int NCTA, int tid, int lane,
-                                         uint32_t taddr, uint32_t tab_s, const uint8_t* smem) {
+                                         uint32_t taddr0, uint32_t tab_s, const uint8_t* smem) {
   using C = Cfg<G>;
-  using L = Layout<G, WARPS>;
-  const int r = tid;
-        // ---- segment epilogue, straight from TMEM (one row per thread), in
-  // four 16-column chunks to keep the register footprint small
+  using L = Layout<G, WARPS, RPT>;
+  constexpr int NLT = L::NLT;
+  const int r = tid;  // row within a row block
   const int m0 = (sg.tile / sk.NT) * L::MCTA, n0 = (sg.tile % sk.NT) * kNcta;
   const int32_t bias_total = C::BIAS * kKgTile * (sg.kb - sg.ka);
   const bool producer = sg.kb < KT;
@@ -116,125 +116,130 @@ __device__ __forceinline__ void sk_epilogue(const Params& p, const SkParams& sk,
   const bool want_max = !ACC_ONLY && p.amax_out != nullptr && !producer;
   if (want_max) {
     if (tid < kNcta) cta_max[tid] = 0u;
-    bar_sync(6, L::MCTA);
+    bar_sync(6, NLT);
   }
   if (owner) {
-    // the owner segment is the CTA's last: every table read is done once
-    // all lookup warps get here, so the table region holds the tile.
-    // TMEM -> shared int32 tile (XOR-swizzled rows, as in K1)
-    bar_sync(6, L::MCTA);
-    {
-      const uint32_t swz = (uint32_t)((r >> 2) & 1);
-#pragma unroll 1
-      for (int h = 0; h < 4; ++h) {
-        uint32_t v[16];
-        tmem_ld16(taddr + 16 * h, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const uint32_t c = (uint32_t)((lane + 2 * h + e) & 7);
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const uint32_t uu = (2 * c + hh) ^ swz;
-            const uint32_t* x = v + 8 * e + 4 * hh;
-            sts128(tab_s + r * 256 + uu * 16, x[0] - bias_total, x[1] - bias_total,
-                   x[2] - bias_total, x[3] - bias_total);
-          }
-        }
-      }
-    }
     // the tile's units [tile*KT, tile*KT + ka) were produced by the
     // preceding CTA(s)
     int c_lo = cta - 1;
     while (c_lo > 0 && sk_begin(sk.U, NCTA, c_lo) > head) --c_lo;
-    if (tid == 0) {
-      for (int c2 = cta - 1; c2 >= c_lo; --c2) {
-        // bounded wait: a schedule bug must fail loudly, never hang
-        unsigned spins = 0;
-        while (ld_acquire_gpu(sk.flags + c2) != sk.epoch) {
-          __nanosleep(64);
-          if (++spins > (1u << 26)) __trap();
-        }
-      }
-    }
-    bar_sync(6, L::MCTA);
-    // flat reduction: unit e = (row e/16, tokens 4(e%16)..+3), in two
-    // halves of 8 units per thread; all loads of a producer issued together
-    constexpr int UPT = 4;
-    const int4* red = reinterpret_cast<const int4*>(smem);
     float tok_max[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 1
-    for (int half = 0; half < 16 / UPT; ++half) {
-      int4 acc4[UPT];
+    for (int rb = 0; rb < RPT; ++rb) {
+      // the owner segment is the CTA's last: every table read is done once
+      // all lookup warps get here, so the table region holds the row block.
+      // TMEM -> shared int32 tile (XOR-swizzled rows, as in K1)
+      bar_sync(6, NLT);
+      {
+        const uint32_t swz = (uint32_t)((r >> 2) & 1);
+        const uint32_t taddr = taddr0 + 256u * (uint32_t)rb;
+#pragma unroll 1
+        for (int h = 0; h < 4; ++h) {
+          uint32_t v[16];
+          tmem_ld16(taddr + 16 * h, v);
+          tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < UPT; ++i) {
-        const int e = tid + (half * UPT + i) * L::MCTA;
-        const int rr = e >> 4;
-        acc4[i] = red[rr * 16 + ((e & 15) ^ ((rr >> 2) & 1))];
-      }
-      // PP producers per round, all their loads issued before any add: with
-      // few tiles a tile has many producers and one round trip per producer
-      // would serialise the fixup
-      constexpr int PP = (WARPS >= 16) ? 2 : 4;
-      int c2 = cta - 1;
-      for (; c2 - (PP - 1) >= c_lo; c2 -= PP) {
-        int4 w4[PP][UPT];
+          for (int e = 0; e < 2; ++e) {
+            const uint32_t c = (uint32_t)((lane + 2 * h + e) & 7);
 #pragma unroll
-        for (int pp = 0; pp < PP; ++pp) {
-          const int4* prow =
-              reinterpret_cast<const int4*>(sk.ws + (size_t)(c2 - pp) * L::MCTA * kNcta);
-#pragma unroll
-          for (int i = 0; i < UPT; ++i) w4[pp][i] = __ldcg(prow + tid + (half * UPT + i) * L::MCTA);
-        }
-#pragma unroll
-        for (int pp = 0; pp < PP; ++pp)
-#pragma unroll
-          for (int i = 0; i < UPT; ++i) {
-            acc4[i].x += w4[pp][i].x; acc4[i].y += w4[pp][i].y;
-            acc4[i].z += w4[pp][i].z; acc4[i].w += w4[pp][i].w;
+            for (int hh = 0; hh < 2; ++hh) {
+              const uint32_t uu = (2 * c + hh) ^ swz;
+              const uint32_t* x = v + 8 * e + 4 * hh;
+              sts128(tab_s + r * 256 + uu * 16, x[0] - bias_total, x[1] - bias_total,
+                     x[2] - bias_total, x[3] - bias_total);
+            }
           }
+        }
       }
-      for (; c2 >= c_lo; --c2) {
-        const int4* prow = reinterpret_cast<const int4*>(sk.ws + (size_t)c2 * L::MCTA * kNcta);
-        int4 w4[UPT];
-#pragma unroll
-        for (int i = 0; i < UPT; ++i) w4[i] = __ldcg(prow + tid + (half * UPT + i) * L::MCTA);
+      if (rb == 0 && tid == 0) {
+        for (int c2 = cta - 1; c2 >= c_lo; --c2) {
+          // bounded wait: a schedule bug must fail loudly, never hang
+          unsigned spins = 0;
+          while (ld_acquire_gpu(sk.flags + c2) != sk.epoch) {
+            __nanosleep(64);
+            if (++spins > (1u << 26)) __trap();
+          }
+        }
+      }
+      bar_sync(6, NLT);
+      // flat reduction: unit e = (row e/16 of the block, tokens 4(e%16)..+3),
+      // UPT units per thread per round; all loads of a producer issued together
+      constexpr int UPT = 4;
+      const int4* red = reinterpret_cast<const int4*>(smem);
+      const size_t blk = (size_t)rb * NLT * 16;  // int4 offset of the row block in a slot
+#pragma unroll 1
+      for (int half = 0; half < 16 / UPT; ++half) {
+        int4 acc4[UPT];
 #pragma unroll
         for (int i = 0; i < UPT; ++i) {
-          acc4[i].x += w4[i].x; acc4[i].y += w4[i].y; acc4[i].z += w4[i].z; acc4[i].w += w4[i].w;
+          const int e = tid + (half * UPT + i) * NLT;
+          const int rr = e >> 4;
+          acc4[i] = red[rr * 16 + ((e & 15) ^ ((rr >> 2) & 1))];
         }
-      }
+        // PP producers per round, all their loads issued before any add: with
+        // few tiles a tile has many producers and one round trip per producer
+        // would serialise the fixup
+        constexpr int PP = (WARPS >= 16) ? 2 : 4;
+        int c2 = cta - 1;
+        for (; c2 - (PP - 1) >= c_lo; c2 -= PP) {
+          int4 w4[PP][UPT];
 #pragma unroll
-      for (int i = 0; i < UPT; ++i) {
-        const int e = tid + (half * UPT + i) * L::MCTA;
-        const int mm = m0 + (e >> 4), n = n0 + 4 * (e & 15);
-        if (mm >= p.M || n >= p.N) continue;
-        const int32_t x[4] = {acc4[i].x, acc4[i].y, acc4[i].z, acc4[i].w};
-        if constexpr (ACC_ONLY) {
-          int32_t* o = reinterpret_cast<int32_t*>(p.out) + (size_t)mm * p.N + n;
-          if (p.out_vec4 && n + 3 < p.N) *reinterpret_cast<int4*>(o) = acc4[i];
-          else for (int k = 0; k < 4 && n + k < p.N; ++k) o[k] = x[k];
-        } else {
-          float f[4];
+          for (int pp = 0; pp < PP; ++pp) {
+            const int4* prow =
+                reinterpret_cast<const int4*>(sk.ws + (size_t)(c2 - pp) * L::MCTA * kNcta) + blk;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float sc = (n + k < p.N) ? __fmul_rn(__ldg(p.a_scale + n + k), p.w_scale) : 0.f;
-            f[k] = __fmul_rn((float)x[k], sc);
+            for (int i = 0; i < UPT; ++i) w4[pp][i] = __ldcg(prow + tid + (half * UPT + i) * NLT);
           }
-          if (p.mul_in) {
-            const float* mi = p.mul_in + (size_t)mm * p.N + n;
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              if (n + k < p.N) f[k] = __fmul_rn(f[k], __ldg(mi + k));
-          }
-          if (want_max && mm < p.amax_rows) {
+          for (int pp = 0; pp < PP; ++pp)
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              if (n + k < p.N) tok_max[k] = fmaxf(tok_max[k], fabsf(f[k]));
+            for (int i = 0; i < UPT; ++i) {
+              acc4[i].x += w4[pp][i].x; acc4[i].y += w4[pp][i].y;
+              acc4[i].z += w4[pp][i].z; acc4[i].w += w4[pp][i].w;
+            }
+        }
+        for (; c2 >= c_lo; --c2) {
+          const int4* prow = reinterpret_cast<const int4*>(sk.ws + (size_t)c2 * L::MCTA * kNcta) + blk;
+          int4 w4[UPT];
+#pragma unroll
+          for (int i = 0; i < UPT; ++i) w4[i] = __ldcg(prow + tid + (half * UPT + i) * NLT);
+#pragma unroll
+          for (int i = 0; i < UPT; ++i) {
+            acc4[i].x += w4[i].x; acc4[i].y += w4[i].y; acc4[i].z += w4[i].z; acc4[i].w += w4[i].w;
           }
-          float* o = p.out + (size_t)mm * p.N + n;
-          if (p.out_vec4 && n + 3 < p.N) *reinterpret_cast<float4*>(o) = make_float4(f[0], f[1], f[2], f[3]);
-          else for (int k = 0; k < 4 && n + k < p.N; ++k) o[k] = f[k];
+        }
+#pragma unroll
+        for (int i = 0; i < UPT; ++i) {
+          const int e = tid + (half * UPT + i) * NLT;
+          const int mm = m0 + rb * NLT + (e >> 4), n = n0 + 4 * (e & 15);
+          if (mm >= p.M || n >= p.N) continue;
+          const int32_t x[4] = {acc4[i].x, acc4[i].y, acc4[i].z, acc4[i].w};
+          if constexpr (ACC_ONLY) {
+            int32_t* o = reinterpret_cast<int32_t*>(p.out) + (size_t)mm * p.N + n;
+            if (p.out_vec4 && n + 3 < p.N) *reinterpret_cast<int4*>(o) = acc4[i];
+            else for (int k = 0; k < 4 && n + k < p.N; ++k) o[k] = x[k];
+          } else {
+            float f[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float sc = (n + k < p.N) ? __fmul_rn(__ldg(p.a_scale + n + k), p.w_scale) : 0.f;
+              f[k] = __fmul_rn((float)x[k], sc);
+            }
+            if (p.mul_in) {
+              const float* mi = p.mul_in + (size_t)mm * p.N + n;
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                if (n + k < p.N) f[k] = __fmul_rn(f[k], __ldg(mi + k));
+            }
+            if (want_max && mm < p.amax_rows) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                if (n + k < p.N) tok_max[k] = fmaxf(tok_max[k], fabsf(f[k]));
+            }
+            float* o = p.out + (size_t)mm * p.N + n;
+            if (p.out_vec4 && n + 3 < p.N) *reinterpret_cast<float4*>(o) = make_float4(f[0], f[1], f[2], f[3]);
+            else for (int k = 0; k < 4 && n + k < p.N; ++k) o[k] = f[k];
+          }
         }
       }
     }
@@ -245,90 +250,96 @@ __device__ __forceinline__ void sk_epilogue(const Params& p, const SkParams& sk,
         tok_max[k] = fmaxf(tok_max[k], __shfl_xor_sync(0xffffffffu, tok_max[k], 16));
         if (lane < 16) atomicMax(cta_max + 4 * (tid & 15) + k, __float_as_uint(tok_max[k]));
       }
-      bar_sync(6, L::MCTA);
+      bar_sync(6, NLT);
       if (tid < kNcta && n0 + tid < p.N && cta_max[tid] != 0u)
         atomicMax(p.amax_out + n0 + tid, cta_max[tid]);
     }
     return;
   }
-  const int m = m0 + r;
 #pragma unroll 1
-  for (int h = 0; h < 4; ++h) {
-    uint32_t v[16];
-    tmem_ld16(taddr + 16 * h, v);
-    tmem_wait_ld();
-    int32_t a[16];
+  for (int rb = 0; rb < RPT; ++rb) {
+    const int rr = rb * NLT + r;  // row within the tile
+    const int m = m0 + rr;
+    const uint32_t taddr = taddr0 + 256u * (uint32_t)rb;
+#pragma unroll 1
+    for (int h = 0; h < 4; ++h) {
+      uint32_t v[16];
+      tmem_ld16(taddr + 16 * h, v);
+      tmem_wait_ld();
+      int32_t a[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) a[i] = (int32_t)(v[i] - bias_total);
-    if (producer) {
-      // int32 partial -> workspace slot [row][token] (the owner reads it
-      // row-contiguous and coalesced)
-      int32_t* wrow = sk.ws + ((size_t)cta * L::MCTA + r) * kNcta;
+      for (int i = 0; i < 16; ++i) a[i] = (int32_t)(v[i] - bias_total);
+      if (producer) {
+        // int32 partial -> workspace slot [row][token] (the owner reads it
+        // row-contiguous and coalesced)
+        int32_t* wrow = sk.ws + ((size_t)cta * L::MCTA + rr) * kNcta;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = (lane + 2 * h + e) & 7;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int32_t* x = a + 8 * e + 4 * hh;
+            __stcg(reinterpret_cast<int4*>(wrow + 8 * c + 4 * hh), make_int4(x[0], x[1], x[2], x[3]));
+          }
+        }
+        continue;
+      }
+      if (m >= p.M) continue;
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int c = (lane + 2 * h + e) & 7;
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
+          const int n = n0 + 8 * c + 4 * hh;
+          if (n >= p.N) continue;
           const int32_t* x = a + 8 * e + 4 * hh;
-          __stcg(reinterpret_cast<int4*>(wrow + 8 * c + 4 * hh), make_int4(x[0], x[1], x[2], x[3]));
-        }
-      }
-      continue;
-    }
-    if (m >= p.M) continue;
+          if constexpr (ACC_ONLY) {
+            int32_t* o = reinterpret_cast<int32_t*>(p.out) + (size_t)m * p.N + n;
+            if (p.out_vec4 && n + 3 < p.N) *reinterpret_cast<int4*>(o) = make_int4(x[0], x[1], x[2], x[3]);
+            else for (int k = 0; k < 4 && n + k < p.N; ++k) o[k] = x[k];
+          } else {
+            float f[4];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int c = (lane + 2 * h + e) & 7;
+            for (int k = 0; k < 4; ++k) {
+              const float sc = (n + k < p.N) ? __fmul_rn(__ldg(p.a_scale + n + k), p.w_scale) : 0.f;
+              f[k] = __fmul_rn((float)x[k], sc);
+            }
+            if (p.mul_in) {
+              const float* mi = p.mul_in + (size_t)m * p.N + n;
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const int n = n0 + 8 * c + 4 * hh;
-        if (n >= p.N) continue;
-        const int32_t* x = a + 8 * e + 4 * hh;
-        if constexpr (ACC_ONLY) {
-          int32_t* o = reinterpret_cast<int32_t*>(p.out) + (size_t)m * p.N + n;
-          if (p.out_vec4 && n + 3 < p.N) *reinterpret_cast<int4*>(o) = make_int4(x[0], x[1], x[2], x[3]);
-          else for (int k = 0; k < 4 && n + k < p.N; ++k) o[k] = x[k];
-        } else {
-          float f[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float sc = (n + k < p.N) ? __fmul_rn(__ldg(p.a_scale + n + k), p.w_scale) : 0.f;
-            f[k] = __fmul_rn((float)x[k], sc);
+              for (int k = 0; k < 4; ++k)
+                if (n + k < p.N) f[k] = __fmul_rn(f[k], __ldg(mi + k));
+            }
+            if (want_max && m < p.amax_rows) {
+              for (int k = 0; k < 4 && n + k < p.N; ++k)
+                atomicMax(cta_max + (n - n0) + k, __float_as_uint(fabsf(f[k])));
+            }
+            float* o = p.out + (size_t)m * p.N + n;
+            if (p.out_vec4 && n + 3 < p.N) *reinterpret_cast<float4*>(o) = make_float4(f[0], f[1], f[2], f[3]);
+            else for (int k = 0; k < 4 && n + k < p.N; ++k) o[k] = f[k];
           }
-          if (p.mul_in) {
-            const float* mi = p.mul_in + (size_t)m * p.N + n;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              if (n + k < p.N) f[k] = __fmul_rn(f[k], __ldg(mi + k));
-          }
-          if (want_max && m < p.amax_rows) {
-            for (int k = 0; k < 4 && n + k < p.N; ++k)
-              atomicMax(cta_max + (n - n0) + k, __float_as_uint(fabsf(f[k])));
-          }
-          float* o = p.out + (size_t)m * p.N + n;
-          if (p.out_vec4 && n + 3 < p.N) *reinterpret_cast<float4*>(o) = make_float4(f[0], f[1], f[2], f[3]);
-          else for (int k = 0; k < 4 && n + k < p.N; ++k) o[k] = f[k];
         }
       }
     }
   }
   if (want_max) {
-    bar_sync(6, L::MCTA);
+    bar_sync(6, NLT);
     if (tid < kNcta && n0 + tid < p.N && cta_max[tid] != 0u)
       atomicMax(p.amax_out + n0 + tid, cta_max[tid]);
   }
   if (producer) {
     __threadfence();
-    bar_sync(6, L::MCTA);
+    bar_sync(6, NLT);
     if (tid == 0) st_release_gpu(sk.flags + cta, sk.epoch);
   }
-      }
+}
 
-template <int G, int WARPS, bool ACC_ONLY>
+template <int G, int WARPS, int RPT, bool ACC_ONLY>
 __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
     vlut_mpgemm_sk_kernel(const __grid_constant__ Params p, const SkParams sk) {
   using C = Cfg<G>;
-  using L = Layout<G, WARPS>;
+  using L = Layout<G, WARPS, RPT>;
+  constexpr int GP = kLookupGP2<WARPS, RPT>;
   extern __shared__ __align__(1024) uint8_t smem[];
 
   const int tid = threadIdx.x;
@@ -370,13 +381,13 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
     if (nunits > 0) {
       const int m0 = tile_m0(nxt.seg.tile), n0 = tile_n0(nxt.seg.tile);
       if (bulk) {
-        stage_tile_bulk<G, WARPS>(p, nxt.kt, 0, m0, n0, smem, bt, mbar + mb_stage(0), true, false, true);
+        stage_tile_bulk<G, WARPS, RPT>(p, nxt.kt, 0, m0, n0, smem, bt, mbar + mb_stage(0), true, false, true);
         pdl_wait();
-        stage_tile_bulk<G, WARPS>(p, nxt.kt, 0, m0, n0, smem, bt, mbar + mb_stage(0), false, true, false);
+        stage_tile_bulk<G, WARPS, RPT>(p, nxt.kt, 0, m0, n0, smem, bt, mbar + mb_stage(0), false, true, false);
       } else {
-        stage_tile<G, WARPS>(p, nxt.kt, 0, m0, n0, smem, bt, 1);
+        stage_tile<G, WARPS, RPT>(p, nxt.kt, 0, m0, n0, smem, bt, 1);
         pdl_wait();
-        stage_tile<G, WARPS>(p, nxt.kt, 0, m0, n0, smem, bt, 2);
+        stage_tile<G, WARPS, RPT>(p, nxt.kt, 0, m0, n0, smem, bt, 2);
       }
       nxt.next();
     } else {
@@ -394,10 +405,10 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
           const int b1 = (T + 1) % kStageBufs;
           const int m0 = tile_m0(nxt.seg.tile), n0 = tile_n0(nxt.seg.tile);
           if (bulk) {
-            stage_tile_bulk<G, WARPS>(p, nxt.kt, b1, m0, n0, smem, bt, mbar + mb_stage(b1), true,
+            stage_tile_bulk<G, WARPS, RPT>(p, nxt.kt, b1, m0, n0, smem, bt, mbar + mb_stage(b1), true,
                                       true, true);
           } else {
-            stage_tile<G, WARPS>(p, nxt.kt, b1, m0, n0, smem, bt, 3);
+            stage_tile<G, WARPS, RPT>(p, nxt.kt, b1, m0, n0, smem, bt, 3);
           }
           nxt.next();
           if (!bulk) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
@@ -413,34 +424,40 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
       if (lane == 0) mbar_arrive(mbar + mb_full(u % C::NBUF));
     }
   } else {
-    // =========================== lookup warps
+    // =========================== lookup warps (RPT rows per thread: r, r + NLT)
     if (warp == 0) {
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                        smem_u32(tmem_slot)),
-                   "n"(kTmemCols)
+                   "n"(L::TMEM_COLS)
                    : "memory");
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
     tmem_fence_before();
-    bar_sync(6, L::MCTA);
+    bar_sync(6, L::NLT);
     tmem_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     uint32_t rot[8];
 #pragma unroll
     for (int s = 0; s < 8; ++s) rot[s] = (uint32_t)(((lane + s) & 7) * 16);
+    // row block rb of this warp: lanes 32 (warp & 3).., columns 64 (warp >> 2) + 256 rb
     const uint32_t taddr = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
-    uint32_t sw[8][4];
+    uint32_t sw[RPT][8][4];
+    int32_t nneg[RPT];
+    uint32_t iwa[RPT][4];
 #pragma unroll
-    for (int s = 0; s < 8; ++s)
+    for (int rb = 0; rb < RPT; ++rb) {
+      nneg[rb] = 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) sw[s][q] = 0;
-    int32_t nneg = 0;
+      for (int s = 0; s < 8; ++s)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sw[rb][s][q] = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) iwa[rb][q] = 0u;
+    }
     bool first = true;
     int since_flush = warp % kFlushTiles;
-    uint32_t iwa[4] = {0u, 0u, 0u, 0u};
     SkIter cur;
     cur.init(u0, u1, KT);
-    const int r = tid;  // this thread's row within the tile
 #pragma unroll 1
     for (int t = 0; t < nunits; ++t) {
 #pragma unroll
@@ -448,22 +465,30 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
         const int u = t * C::SUBS + sub;
         mbar_wait(mbar + mb_full(u % C::NBUF), (u / C::NBUF) & 1);
         if (sub == 0) {
-          const uint4 iw = lds128(idx_s + (t % kStageBufs) * L::IDX_BYTES + tid * 16);
-          iwa[0] = iw.x; iwa[1] = iw.y; iwa[2] = iw.z; iwa[3] = iw.w;
+#pragma unroll
+          for (int rb = 0; rb < RPT; ++rb) {
+            const uint4 iw = lds128(idx_s + (t % kStageBufs) * L::IDX_BYTES + (tid + rb * L::NLT) * 16);
+            iwa[rb][0] = iw.x; iwa[rb][1] = iw.y; iwa[rb][2] = iw.z; iwa[rb][3] = iw.w;
+          }
         }
-        lookup_sub<G, kLookupGP<WARPS>>(sub, tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES), iwa, rot, sw,
-                                        nneg);
+#pragma unroll
+        for (int rb = 0; rb < RPT; ++rb)
+          lookup_sub<G, GP>(sub, tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES), iwa[rb], rot, sw[rb],
+                            nneg[rb]);
         __syncwarp();
         if (lane == 0) mbar_arrive(mbar + mb_empty(u % C::NBUF));
       }
       const bool seg_end = (cur.kt + 1 == cur.seg.kb);
       if (++since_flush >= kFlushTiles || seg_end) {
         since_flush = 0;
-        flush_tmem<G, kLookupGP<WARPS> == 1>(sw, nneg, taddr, first);
+#pragma unroll
+        for (int rb = 0; rb < RPT; ++rb)
+          flush_tmem<G, GP == 1>(sw[rb], nneg[rb], taddr + 256u * (uint32_t)rb, first);
         first = false;
       }
       if (seg_end) {
-        sk_epilogue<G, WARPS, ACC_ONLY>(p, sk, cur.seg, KT, cta, NCTA, tid, lane, taddr, tab_s, smem);
+        sk_epilogue<G, WARPS, RPT, ACC_ONLY>(p, sk, cur.seg, KT, cta, NCTA, tid, lane, taddr, tab_s,
+                                             smem);
         first = true;  // the next segment re-initialises TMEM
       }
       cur.next();
@@ -471,11 +496,11 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
     pdl_wait();
     // TMEM release: every lookup warp is done with it
     tmem_fence_before();
-    bar_sync(6, L::MCTA);
+    bar_sync(6, L::NLT);
     if (warp == 0) {
       tmem_fence_after();
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
-                   "n"(kTmemCols)
+                   "n"(L::TMEM_COLS)
                    : "memory");
     }
   }

@@ -64,9 +64,9 @@ def test_quantize_bit_exact(v, K, N):
 
 def test_quantize_half_boundaries(v):
     """Values whose quotient x / s sits on, or a few ulps around, a k + 1/2
-    rounding boundary for every k in [-127, 126] and several scales: the
-    kernel's reciprocal fast path must hand all of these to the IEEE
-    division (round half away from zero of fl(x / s), as the oracle)."""
+    rounding boundary for every k in [-127, 126] and several scales: codes
+    must be round-half-away of the IEEE quotient fl(x / s), as the oracle's
+    (any shortcut through a reciprocal would differ on some of these)."""
     rng = synth.rng(77)
     N = 24
     amax = np.float32(rng.uniform(0.01, 50.0, N)).astype(np.float32)
@@ -336,12 +336,13 @@ def test_mpgemm_feature_major_output_and_linear(v, M, K, N):
 
 # ------------------------------------------------------------------ stream-K schedule
 @pytest.mark.parametrize("M,K,N,g", SHAPES + [(6912, 2560, 256, 4), (2560, 2560, 2048, 4)])
-@pytest.mark.parametrize("warps", [8, 12, 16])
-def test_streamk_acc_bit_exact(v, M, K, N, g, warps):
+@pytest.mark.parametrize("warps,rpt", [(8, 1), (12, 1), (16, 1), (12, 2)])
+def test_streamk_acc_bit_exact(v, M, K, N, g, warps, rpt):
+    # rpt = output rows per lookup thread (m_cta = 32 * warps * rpt)
     W = synth.ternary_weights(M, K, seed=5 * M + K)
     A = synth.int8_activations(K, N, seed=N + 3)
     pw = v.pack_weights_device(to_dev(W), g)
-    acc = v.mpgemm_acc_ws(pw, to_dev(A), plan=v.LaunchPlan(warps, 1, streamk=1))
+    acc = v.mpgemm_acc_ws(pw, to_dev(A), plan=v.LaunchPlan(warps, 1, m_cta=32 * warps * rpt, streamk=1))
     torch.cuda.synchronize()
     if M * N * K > 2e9:  # large case: sampled rows
         pick = np.unique(synth.rng(1).integers(0, M, size=24))
@@ -358,10 +359,12 @@ def test_streamk_fp32_and_planner_identity(v, M, K, N, g):
     pw = v.pack_weights_device(to_dev(W), g)
     qd, sd = to_dev(q), to_dev(s)
     o_sk = v.mpgemm_ws(pw, qd, sd, synth.W_SCALE, plan=v.LaunchPlan(12, 1, streamk=1))
+    o_sk2 = v.mpgemm_ws(pw, qd, sd, synth.W_SCALE, plan=v.LaunchPlan(12, 1, m_cta=768, streamk=1))
     o_auto = v.mpgemm_ws(pw, qd, sd, synth.W_SCALE)
     o_cl = v.mpgemm(pw, qd, sd, synth.W_SCALE)
     torch.cuda.synchronize()
     assert torch.equal(o_sk.view(torch.int32), o_cl.view(torch.int32))
+    assert torch.equal(o_sk2.view(torch.int32), o_cl.view(torch.int32))
     assert torch.equal(o_auto.view(torch.int32), o_cl.view(torch.int32))
     pick = np.unique(np.concatenate([[0, M - 1], synth.rng(2).integers(0, M, size=16)]))
     check_fp32(o_sk.cpu().numpy()[pick], oracle.gemm_i32(W[pick], q), s, synth.W_SCALE)
@@ -369,7 +372,7 @@ def test_streamk_fp32_and_planner_identity(v, M, K, N, g):
 
 # ------------------------------------------------------------------ fused re-quantization (f1)
 FUSED_PLANS = {"cluster": None, "auto_ws": "ws", "sk16": (16, 1, 1), "sk12": (12, 1, 1),
-               "sk8": (8, 1, 1), "cl12x3": (12, 3, 0)}
+               "sk8": (8, 1, 1), "cl12x3": (12, 3, 0), "sk12r2": (12, 1, 1, 768)}
 
 
 @pytest.mark.parametrize("M,K,N,rows", [(6912, 2560, 256, 6912), (3840, 2560, 200, 2560),
@@ -383,7 +386,8 @@ def test_mpgemm_fused_mul_and_amax(v, M, K, N, rows, how):
     pw = v.pack_weights(W, 4, device=dev())
     amax = torch.zeros((N,), dtype=torch.int32, device=dev())
     h = FUSED_PLANS[how]
-    plan = v.LaunchPlan(h[0], h[1], streamk=h[2]) if isinstance(h, tuple) else None
+    plan = (v.LaunchPlan(h[0], h[1], m_cta=h[3] if len(h) > 3 else 0, streamk=h[2])
+            if isinstance(h, tuple) else None)
     ws = v.workspace(dev()) if h is not None else None
     out = v.mpgemm_fused(pw, to_dev(q), to_dev(s), synth.W_SCALE, mul_in=to_dev(g), amax=amax,
                          amax_rows=rows, plan=plan, ws=ws)
