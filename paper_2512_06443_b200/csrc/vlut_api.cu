@@ -142,7 +142,10 @@ vlut_status encode_a_map(CUtensorMap* map, const int8_t* A, int K, int N, int g)
 
 // ------------------------------------------------------------ planner
 int smem_bytes_for(int g, int warps, int rpt = 1) {
-  if (rpt == 2) return g == 4 ? vlut::Layout<4, 12, 2>::SMEM : vlut::Layout<5, 12, 2>::SMEM;
+  if (rpt == 2) {
+    if (warps == 8) return g == 4 ? vlut::Layout<4, 8, 2>::SMEM : vlut::Layout<5, 8, 2>::SMEM;
+    return g == 4 ? vlut::Layout<4, 12, 2>::SMEM : vlut::Layout<5, 12, 2>::SMEM;
+  }
   if (g == 4) {
     if (warps == 8) return vlut::Layout<4, 8>::SMEM;
     if (warps == 12) return vlut::Layout<4, 12>::SMEM;
@@ -238,9 +241,9 @@ double plan_sk(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
   const int half_rows = (pow3i(g) + 1) / 2;
   double best_cost = 1e300;
   // (warps, rows per lookup thread): 12 warps x 2 rows = 768 rows share each table
-  const int warps_opts[4] = {16, 12, 8, 12};
-  const int rpt_opts[4] = {1, 1, 1, 2};
-  for (int wi = 0; wi < 4; ++wi) {
+  const int warps_opts[5] = {16, 12, 8, 12, 8};
+  const int rpt_opts[5] = {1, 1, 1, 2, 2};
+  for (int wi = 0; wi < 5; ++wi) {
     const int warps = warps_opts[wi];
     const int rpt = rpt_opts[wi];
     if (rpt == 2 && getenv("VLUT_NO_RPT2")) continue;
@@ -249,10 +252,12 @@ double plan_sk(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
     const long long U = MT * NT * kgt;
     const long long grid = U < sms ? U : sms;
     const double units = (double)((U + grid - 1) / grid);
-    // two rows per thread: 12 warps with one group per load batch keep the
-    // pipe a little less busy than 16 warps (measured: ~5 % per lookup row at
-    // g = 4, ~1 % at g = 5, where the halved table-build share dominates)
-    const double row_cost = rpt == 2 ? (g == 4 ? 1.05 : 1.01) : 1.0;
+    // two rows per thread, relative cost per lookup row (measured against 16
+    // warps x 1 row, scripts/rpt_ab.py): 12 warps with one group per load
+    // batch keep the pipe ~5 % less busy at g = 4 (~1 % at g = 5); 8 warps
+    // with two groups per batch ~8 % less at g = 4 and ~1 % more at g = 5
+    const double row_cost =
+        rpt == 2 ? (warps == 8 ? (g == 4 ? 1.08 : 0.99) : (g == 4 ? 1.05 : 1.01)) : 1.0;
     double cost = units * VLUT_KG_TILE * ((double)mcta * row_cost + half_rows);
     cost += 6000.0;                             // start + last epilogue
     cost += (double)mcta * 256.0 * 3.0 / 64.0;  // partial write + read + output
@@ -503,7 +508,9 @@ vlut_status dispatch_sk(int g, int warps, int rpt, const vlut::Params& p, const 
   if (rpt == 2) {
     if (warps == 12) return g == 4 ? launch_sk<4, 12, ACC, 2>(p, sk, grid, st)
                                    : launch_sk<5, 12, ACC, 2>(p, sk, grid, st);
-    return fail(VLUT_ERR_UNSUPPORTED, "two rows per thread: 12 warps only");
+    if (warps == 8) return g == 4 ? launch_sk<4, 8, ACC, 2>(p, sk, grid, st)
+                                  : launch_sk<5, 8, ACC, 2>(p, sk, grid, st);
+    return fail(VLUT_ERR_UNSUPPORTED, "two rows per thread: 8 or 12 warps");
   }
   if (g == 4) {
     if (warps == 8) return launch_sk<4, 8, ACC>(p, sk, grid, st);
@@ -630,10 +637,10 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
     if (plan.streamk && (!ws || acc_in || out_t))
       return fail(VLUT_ERR_INVALID_ARGUMENT, "stream-K plan needs a workspace and [M][N] output");
     // m_cta selects the rows per lookup thread: 0 or 32 * warps -> 1; 64 * warps
-    // -> 2 (stream-K with 12 warps only)
+    // -> 2 (stream-K with 8 or 12 warps)
     if (plan.m_cta && plan.m_cta != 32 * plan.warps &&
-        !(plan.m_cta == 64 * plan.warps && plan.warps == 12 && plan.streamk))
-      return fail(VLUT_ERR_UNSUPPORTED, "m_cta=%d: 32*warps, or 768 with 12 warps stream-K",
+        !(plan.m_cta == 64 * plan.warps && plan.warps <= 12 && plan.streamk))
+      return fail(VLUT_ERR_UNSUPPORTED, "m_cta=%d: 32*warps, or 64*warps (8/12 warps) stream-K",
                   plan.m_cta);
   } else {
     double c_best = plan_for(M, K, N, W->g, d.sms, &plan);

@@ -472,10 +472,11 @@ __device__ __forceinline__ void build_tables(uint32_t tab_s, uint32_t a_s, int g
 // ---------------------------------------------------------------- lookups (a4)
 template <int WARPS>
 constexpr int kLookupGP = (WARPS >= 16) ? 1 : 2;
-// two rows per thread: one group per load batch (the second row's
-// accumulators take the registers of the second batch)
+// two rows per thread: with 12 warps one group per load batch (the second
+// row's accumulators take the registers of the second batch); 8 warps have
+// 170 registers per thread and keep two
 template <int WARPS, int RPT>
-constexpr int kLookupGP2 = (RPT > 1) ? 1 : kLookupGP<WARPS>;
+constexpr int kLookupGP2 = (RPT > 1) ? (WARPS <= 8 ? 2 : 1) : kLookupGP<WARPS>;
 
 // Groups [SUB*GS, SUB*GS+GS) of the K-tile whose index vector is iwa.
 // GP = groups per load batch: 2 (16 LDS.128 in flight, half the negations on

@@ -23,7 +23,8 @@ for (M, K, N, g) in shapes:
     res = {}
     for name, plan in (("auto", None), ("w16r1", v.LaunchPlan(16, 1, streamk=1)),
                        ("w12r1", v.LaunchPlan(12, 1, streamk=1)),
-                       ("w12r2", v.LaunchPlan(12, 1, m_cta=768, streamk=1))):
+                       ("w12r2", v.LaunchPlan(12, 1, m_cta=768, streamk=1)),
+                       ("w8r2", v.LaunchPlan(8, 1, m_cta=512, streamk=1))):
         run = lambda: v.mpgemm_ws(pw, A, s, 0.02, out=out, plan=plan, ws=ws)
         for _ in range(2):
             run()

@@ -336,7 +336,7 @@ def test_mpgemm_feature_major_output_and_linear(v, M, K, N):
 
 # ------------------------------------------------------------------ stream-K schedule
 @pytest.mark.parametrize("M,K,N,g", SHAPES + [(6912, 2560, 256, 4), (2560, 2560, 2048, 4)])
-@pytest.mark.parametrize("warps,rpt", [(8, 1), (12, 1), (16, 1), (12, 2)])
+@pytest.mark.parametrize("warps,rpt", [(8, 1), (12, 1), (16, 1), (12, 2), (8, 2)])
 def test_streamk_acc_bit_exact(v, M, K, N, g, warps, rpt):
     # rpt = output rows per lookup thread (m_cta = 32 * warps * rpt)
     W = synth.ternary_weights(M, K, seed=5 * M + K)
@@ -372,7 +372,7 @@ def test_streamk_fp32_and_planner_identity(v, M, K, N, g):
 
 # ------------------------------------------------------------------ fused re-quantization (f1)
 FUSED_PLANS = {"cluster": None, "auto_ws": "ws", "sk16": (16, 1, 1), "sk12": (12, 1, 1),
-               "sk8": (8, 1, 1), "cl12x3": (12, 3, 0), "sk12r2": (12, 1, 1, 768)}
+               "sk8": (8, 1, 1), "cl12x3": (12, 3, 0), "sk12r2": (12, 1, 1, 768), "sk8r2": (8, 1, 1, 512)}
 
 
 @pytest.mark.parametrize("M,K,N,rows", [(6912, 2560, 256, 6912), (3840, 2560, 200, 2560),
