@@ -735,6 +735,14 @@ def sweep(v, dev, stream, flush, reps=10):
         res.append({"config": 3, "linear": lin.name + " (mixed g5/g4)", "M": lin.M, "K": lin.K,
                     "N": 1024, "k5": k5, "k4": k4, "bpw": 8.0 * (k5 / 5 + k4 / 4) / lin.K,
                     "us": t * 1e6, "frac_smem_roofline": lk / R_LU / t})
+        # the same K with g = 5 and a zero-padded last group (VLUT_PACK_PAD_K):
+        # same bytes per row, one launch
+        p5 = v.pack_weights(W, 5, device=dev, pad_k=True)
+        t5 = timeit(p5, A, sc, out)
+        lk5 = lin.M * (-(-lin.K // 5)) * 1024
+        res.append({"config": 3, "linear": lin.name + " (g5, padded K)", "M": lin.M, "K": lin.K,
+                    "N": 1024, "bpw": 8.0 * (-(-lin.K // 5)) / lin.K, "us": t5 * 1e6,
+                    "frac_smem_roofline": lk5 / R_LU / t5})
     return res
 
 

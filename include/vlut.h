@@ -67,7 +67,9 @@ typedef enum {
  *     covers features k*g .. k*g+g-1 (reading c4) and
  *     index = sum_{r<g} (W[m][k*g+r] + 1) * 3^r  (Alg. 1 GetSign, P:382;
  *     least-significant trit first, reading c1).
- *   Rows m >= M and groups k >= K/g hold the all-zero index (3^g-1)/2
+ *   With VLUT_PACK_PAD_K, K need not be a multiple of g: the last group
+ *   reads zero trits for its features >= K (they contribute exactly 0).
+ *   Rows m >= M and groups k >= ceil(K/g) hold the all-zero index (3^g-1)/2
  *   (40 for g=4, 121 for g=5) and contribute exactly 0.
  * The K-tile index is outermost, matching the K->M loop order of Alg. 1
  * (P:441); within a tile the 16 index bytes of one row are contiguous so one
@@ -79,9 +81,9 @@ typedef struct {
   uint32_t version;        /* VLUT_VERSION                                */
   int32_t M, K, g;         /* logical shape; g in {4,5}                   */
   int32_t m_pad;           /* M rounded up to VLUT_M_TILE                 */
-  int32_t kg_tiles;        /* ceil((K/g) / VLUT_KG_TILE)                  */
+  int32_t kg_tiles;        /* ceil(ceil(K/g) / VLUT_KG_TILE)              */
   int32_t m_tile, kg_tile; /* VLUT_M_TILE, VLUT_KG_TILE                   */
-  int32_t reserved;
+  int32_t flags;           /* 0, or VLUT_PACK_PAD_K                        */
   int64_t payload_bytes;   /* kg_tiles * m_pad * 16                        */
   const void* payload;     /* device pointer (caller-owned)               */
 } vlut_packed_weights;
@@ -112,6 +114,23 @@ typedef struct {
  * (kg_tiles * m_pad * 16).  Returns 0 if the arguments are invalid (M<=0,
  * K<=0, g not in {4,5}, g does not divide K) or the size overflows. */
 size_t vlut_packed_bytes(int M, int K, int g);
+
+/* Packing flag: K need not be a multiple of g; the last group of every row is
+ * completed with zero trits (features >= K; the kernels read those activation
+ * rows as 0).  The same ceil(K/5) bytes per row as the paper's mixed g=5/g=4
+ * schedule -- never more -- but one g for the whole K range, so
+ * one launch.  A B200 alternative to the mixed schedule. */
+#define VLUT_PACK_PAD_K 1
+
+/* vlut_packed_bytes / vlut_pack_weights / vlut_pack_weights_device with
+ * packing flags (0 = the plain functions). */
+size_t vlut_packed_bytes_ex(int M, int K, int g, int flags);
+vlut_status vlut_pack_weights_ex(const int8_t* w_trits_host, int M, int K, int g, int flags,
+                                 void* payload_dev, size_t payload_bytes,
+                                 vlut_packed_weights* desc_out, void* stream);
+vlut_status vlut_pack_weights_device_ex(const int8_t* w_trits_dev, int M, int K, int g, int flags,
+                                        void* payload_dev, size_t payload_bytes,
+                                        vlut_packed_weights* desc_out, void* stream);
 
 /*
  * Pack ternary weights (a1, offline).

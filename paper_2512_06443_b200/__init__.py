@@ -54,7 +54,7 @@ class _Desc(ctypes.Structure):
         ("M", ctypes.c_int32), ("K", ctypes.c_int32), ("g", ctypes.c_int32),
         ("m_pad", ctypes.c_int32), ("kg_tiles", ctypes.c_int32),
         ("m_tile", ctypes.c_int32), ("kg_tile", ctypes.c_int32),
-        ("reserved", ctypes.c_int32), ("payload_bytes", ctypes.c_int64),
+        ("flags", ctypes.c_int32), ("payload_bytes", ctypes.c_int64),
         ("payload", ctypes.c_void_p),
     ]
 
@@ -76,6 +76,14 @@ EXPORTS = {
     "vlut_pack_weights_device": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                   ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(_Desc),
                                   ctypes.c_void_p], ctypes.c_int),
+    "vlut_packed_bytes_ex": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int],
+                             ctypes.c_size_t),
+    "vlut_pack_weights_ex": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                              ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
+                              ctypes.POINTER(_Desc), ctypes.c_void_p], ctypes.c_int),
+    "vlut_pack_weights_device_ex": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
+                                     ctypes.POINTER(_Desc), ctypes.c_void_p], ctypes.c_int),
     "vlut_unpack_weights_host": ([ctypes.POINTER(_Desc), ctypes.c_void_p, ctypes.c_void_p],
                                  ctypes.c_int),
     "vlut_plan": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
@@ -237,39 +245,47 @@ class PackedWeights:
         return int(self.desc.payload_bytes)
 
 
-def packed_bytes(M: int, K: int, g: int) -> int:
-    return int(lib().vlut_packed_bytes(M, K, g))
+PACK_PAD_K = 1  # VLUT_PACK_PAD_K: K need not be a multiple of g (zero-trit padding)
 
 
-def pack_weights(w_trits: np.ndarray, g: int, device=None, stream=None) -> PackedWeights:
-    """Host trits int8 [M][K] -> device packed weights (validated on host)."""
+def packed_bytes(M: int, K: int, g: int, flags: int = 0) -> int:
+    return int(lib().vlut_packed_bytes_ex(M, K, g, flags))
+
+
+def pack_weights(w_trits: np.ndarray, g: int, device=None, stream=None,
+                 pad_k: bool = False) -> PackedWeights:
+    """Host trits int8 [M][K] -> device packed weights (validated on host).
+    pad_k: allow K % g != 0 (the last group is completed with zero trits)."""
     import torch
     w = np.ascontiguousarray(w_trits, dtype=np.int8)
     M, K = w.shape
-    nb = packed_bytes(M, K, g)
+    flags = PACK_PAD_K if pad_k else 0
+    nb = packed_bytes(M, K, g, flags)
     if nb == 0:
         raise VlutError(3, f"cannot pack M={M} K={K} g={g}")
     payload = torch.empty(nb, dtype=torch.uint8, device=device or "cuda")
     d = _Desc()
     with torch.cuda.device(payload.device):
-        _check(lib().vlut_pack_weights(ctypes.c_void_p(w.ctypes.data), M, K, g,
-                                       _dev_ptr(payload), nb, ctypes.byref(d),
-                                       _stream_ptr(stream)))
+        _check(lib().vlut_pack_weights_ex(ctypes.c_void_p(w.ctypes.data), M, K, g, flags,
+                                          _dev_ptr(payload), nb, ctypes.byref(d),
+                                          _stream_ptr(stream)))
     return PackedWeights(payload, d)
 
 
-def pack_weights_device(w_trits, g: int, stream=None) -> PackedWeights:
+def pack_weights_device(w_trits, g: int, stream=None, pad_k: bool = False) -> PackedWeights:
     """Device trits (torch int8 CUDA [M][K]) -> packed weights, on the GPU."""
     import torch
     M, K = w_trits.shape
-    nb = packed_bytes(M, K, g)
+    flags = PACK_PAD_K if pad_k else 0
+    nb = packed_bytes(M, K, g, flags)
     if nb == 0:
         raise VlutError(3, f"cannot pack M={M} K={K} g={g}")
     payload = torch.empty(nb, dtype=torch.uint8, device=w_trits.device)
     d = _Desc()
     with torch.cuda.device(payload.device):
-        _check(lib().vlut_pack_weights_device(_dev_ptr(w_trits), M, K, g, _dev_ptr(payload), nb,
-                                              ctypes.byref(d), _stream_ptr(stream)))
+        _check(lib().vlut_pack_weights_device_ex(_dev_ptr(w_trits), M, K, g, flags,
+                                                 _dev_ptr(payload), nb, ctypes.byref(d),
+                                                 _stream_ptr(stream)))
     return PackedWeights(payload, d)
 
 

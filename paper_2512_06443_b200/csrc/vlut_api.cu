@@ -82,10 +82,11 @@ inline bool valid_g(int g) { return g == 4 || g == 5; }
 
 inline int pow3i(int g) { return g == 4 ? 81 : 243; }
 
-bool layout_of(int M, int K, int g, int* m_pad, int* kg_tiles, size_t* bytes) {
-  if (M <= 0 || K <= 0 || !valid_g(g) || K % g) return false;
+bool layout_of(int M, int K, int g, int flags, int* m_pad, int* kg_tiles, size_t* bytes) {
+  if (M <= 0 || K <= 0 || !valid_g(g) || (flags & ~VLUT_PACK_PAD_K)) return false;
+  if (K % g && !(flags & VLUT_PACK_PAD_K)) return false;
   const long long mp = ((long long)M + VLUT_M_TILE - 1) / VLUT_M_TILE * VLUT_M_TILE;
-  const long long kgt = ((long long)(K / g) + VLUT_KG_TILE - 1) / VLUT_KG_TILE;
+  const long long kgt = ((long long)((K + g - 1) / g) + VLUT_KG_TILE - 1) / VLUT_KG_TILE;
   const long long b = kgt * mp * 16;
   if (mp > (1LL << 30) || kgt > (1LL << 30) || b <= 0) return false;
   *m_pad = (int)mp;
@@ -100,7 +101,7 @@ vlut_status check_desc(const vlut_packed_weights* W, int M, int K) {
     return fail(VLUT_ERR_CORRUPT_DESCRIPTOR, "bad descriptor magic/version");
   int mp = 0, kgt = 0;
   size_t bytes = 0;
-  if (!layout_of(W->M, W->K, W->g, &mp, &kgt, &bytes) || W->m_pad != mp ||
+  if (!layout_of(W->M, W->K, W->g, W->flags, &mp, &kgt, &bytes) || W->m_pad != mp ||
       W->kg_tiles != kgt || W->payload_bytes != (int64_t)bytes || W->m_tile != VLUT_M_TILE ||
       W->kg_tile != VLUT_KG_TILE || !W->payload)
     return fail(VLUT_ERR_CORRUPT_DESCRIPTOR, "descriptor fields inconsistent");
@@ -235,7 +236,7 @@ size_t sk_workspace_bytes(int sms) { return slot_acc_off(sms) + kSlotAccBytes; }
 // Best stream-K plan (persistent, grid = #SMs): every CTA gets ceil(U / sms)
 // K-tile units; cost in the same SMEM-cycle units as plan_for.
 double plan_sk(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
-  const int KG = K / g;
+  const int KG = (K + g - 1) / g;  // padded packing: the last group may be partial
   const int kgt = (KG + VLUT_KG_TILE - 1) / VLUT_KG_TILE;
   const int NT = (N + vlut::kNcta - 1) / vlut::kNcta;
   const int half_rows = (pow3i(g) + 1) / 2;
@@ -287,7 +288,7 @@ double plan_sk(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
 //                (S-1)/S of the m_cta x 256 B int32 tile at ~16 B/clk
 //   total        waves x per-CTA, waves = ceil(CTAs / (active clusters x S))
 double plan_for(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
-  const int KG = K / g;
+  const int KG = (K + g - 1) / g;  // padded packing: the last group may be partial
   const int kgt = (KG + VLUT_KG_TILE - 1) / VLUT_KG_TILE;
   const int NT = (N + vlut::kNcta - 1) / vlut::kNcta;
   const int half_rows = (pow3i(g) + 1) / 2;
@@ -354,7 +355,7 @@ int slot_default_nw(int g, int N, int tpw) {
 // split-K adds the red.global traffic of the partial tile.
 double plan_slot(int M, int K, int N, int g, int sms, int tpw, int nw_force, int S_force,
                  bool have_ws, vlut_launch_plan* out) {
-  const int KG = K / g;
+  const int KG = (K + g - 1) / g;  // padded packing: the last group may be partial
   const int kgt = (KG + VLUT_KG_TILE - 1) / VLUT_KG_TILE;
   const int nw = nw_force > 0 ? nw_force : slot_default_nw(g, N, tpw);
   if (!slot_variant_ok(g, nw, tpw)) return 1e300;
@@ -795,21 +796,26 @@ int vlut_active_clusters(int g, int warps, int splits) {
   return active_clusters_for(g, warps, splits);
 }
 
-size_t vlut_packed_bytes(int M, int K, int g) {
+size_t vlut_packed_bytes_ex(int M, int K, int g, int flags) {
   int mp = 0, kgt = 0;
   size_t b = 0;
-  if (!layout_of(M, K, g, &mp, &kgt, &b)) return 0;
+  if (!layout_of(M, K, g, flags, &mp, &kgt, &b)) return 0;
   return b;
 }
 
-static vlut_status fill_desc(int M, int K, int g, void* payload_dev, size_t payload_bytes,
-                             vlut_packed_weights* desc_out, int* m_pad, int* kgt) {
+size_t vlut_packed_bytes(int M, int K, int g) { return vlut_packed_bytes_ex(M, K, g, 0); }
+
+static vlut_status fill_desc(int M, int K, int g, int flags, void* payload_dev,
+                             size_t payload_bytes, vlut_packed_weights* desc_out, int* m_pad,
+                             int* kgt) {
   if (!desc_out || !payload_dev) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL argument");
   if (!valid_g(g)) return fail(VLUT_ERR_INVALID_ARGUMENT, "g must be 4 or 5 (got %d)", g);
   if (M <= 0 || K <= 0) return fail(VLUT_ERR_INVALID_ARGUMENT, "M, K must be > 0");
-  if (K % g) return fail(VLUT_ERR_SHAPE, "g=%d does not divide K=%d", g, K);
+  if (flags & ~VLUT_PACK_PAD_K) return fail(VLUT_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
+  if (K % g && !(flags & VLUT_PACK_PAD_K))
+    return fail(VLUT_ERR_SHAPE, "g=%d does not divide K=%d", g, K);
   size_t need = 0;
-  if (!layout_of(M, K, g, m_pad, kgt, &need)) return fail(VLUT_ERR_SHAPE, "size overflow");
+  if (!layout_of(M, K, g, flags, m_pad, kgt, &need)) return fail(VLUT_ERR_SHAPE, "size overflow");
   if (payload_bytes < need)
     return fail(VLUT_ERR_BUFFER_TOO_SMALL, "payload needs %zu bytes, got %zu", need,
                 payload_bytes);
@@ -824,20 +830,21 @@ static vlut_status fill_desc(int M, int K, int g, void* payload_dev, size_t payl
   desc_out->kg_tiles = *kgt;
   desc_out->m_tile = VLUT_M_TILE;
   desc_out->kg_tile = VLUT_KG_TILE;
+  desc_out->flags = flags;
   desc_out->payload_bytes = (int64_t)need;
   desc_out->payload = payload_dev;
   return VLUT_OK;
 }
 
-vlut_status vlut_pack_weights(const int8_t* w, int M, int K, int g, void* payload_dev,
-                              size_t payload_bytes, vlut_packed_weights* desc_out,
-                              void* stream) {
+vlut_status vlut_pack_weights_ex(const int8_t* w, int M, int K, int g, int flags,
+                                 void* payload_dev, size_t payload_bytes,
+                                 vlut_packed_weights* desc_out, void* stream) {
   if (!w) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL weights");
   vlut_packed_weights d;
   int mp = 0, kgt = 0;
-  vlut_status st = fill_desc(M, K, g, payload_dev, payload_bytes, &d, &mp, &kgt);
+  vlut_status st = fill_desc(M, K, g, flags, payload_dev, payload_bytes, &d, &mp, &kgt);
   if (st != VLUT_OK) return st;
-  const int KG = K / g;
+  const int KG = (K + g - 1) / g;  // last group padded with zero trits (VLUT_PACK_PAD_K)
   const uint8_t zero = (uint8_t)((pow3i(g) - 1) / 2);
   std::vector<uint8_t> host((size_t)d.payload_bytes, zero);
   for (int m = 0; m < M; ++m) {
@@ -845,9 +852,10 @@ vlut_status vlut_pack_weights(const int8_t* w, int M, int K, int g, void* payloa
     for (int k = 0; k < KG; ++k) {
       int idx = 0, p3 = 1;
       for (int r = 0; r < g; ++r) {
-        const int t = row[k * g + r];
+        const int f = k * g + r;
+        const int t = f < K ? row[f] : 0;
         if (t < -1 || t > 1)
-          return fail(VLUT_ERR_INVALID_TRIT, "invalid trit %d at (%d,%d)", t, m, k * g + r);
+          return fail(VLUT_ERR_INVALID_TRIT, "invalid trit %d at (%d,%d)", t, m, f);
         idx += (t + 1) * p3;
         p3 *= 3;
       }
@@ -861,13 +869,19 @@ vlut_status vlut_pack_weights(const int8_t* w, int M, int K, int g, void* payloa
   return ok();
 }
 
-vlut_status vlut_pack_weights_device(const int8_t* w_dev, int M, int K, int g,
-                                     void* payload_dev, size_t payload_bytes,
-                                     vlut_packed_weights* desc_out, void* stream) {
+vlut_status vlut_pack_weights(const int8_t* w, int M, int K, int g, void* payload_dev,
+                              size_t payload_bytes, vlut_packed_weights* desc_out,
+                              void* stream) {
+  return vlut_pack_weights_ex(w, M, K, g, 0, payload_dev, payload_bytes, desc_out, stream);
+}
+
+vlut_status vlut_pack_weights_device_ex(const int8_t* w_dev, int M, int K, int g, int flags,
+                                        void* payload_dev, size_t payload_bytes,
+                                        vlut_packed_weights* desc_out, void* stream) {
   if (!w_dev) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL weights");
   vlut_packed_weights d;
   int mp = 0, kgt = 0;
-  vlut_status st = fill_desc(M, K, g, payload_dev, payload_bytes, &d, &mp, &kgt);
+  vlut_status st = fill_desc(M, K, g, flags, payload_dev, payload_bytes, &d, &mp, &kgt);
   if (st != VLUT_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const long long total = d.payload_bytes;
@@ -881,21 +895,29 @@ vlut_status vlut_pack_weights_device(const int8_t* w_dev, int M, int K, int g,
   return ok();
 }
 
+vlut_status vlut_pack_weights_device(const int8_t* w_dev, int M, int K, int g,
+                                     void* payload_dev, size_t payload_bytes,
+                                     vlut_packed_weights* desc_out, void* stream) {
+  return vlut_pack_weights_device_ex(w_dev, M, K, g, 0, payload_dev, payload_bytes, desc_out,
+                                     stream);
+}
+
 vlut_status vlut_unpack_weights_host(const vlut_packed_weights* desc, const uint8_t* payload,
                                      int8_t* w) {
   if (!desc || !payload || !w) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL argument");
   int mp = 0, kgt = 0;
   size_t bytes = 0;
-  if (desc->magic != VLUT_MAGIC || !layout_of(desc->M, desc->K, desc->g, &mp, &kgt, &bytes) ||
+  if (desc->magic != VLUT_MAGIC ||
+      !layout_of(desc->M, desc->K, desc->g, desc->flags, &mp, &kgt, &bytes) ||
       desc->m_pad != mp || desc->kg_tiles != kgt)
     return fail(VLUT_ERR_CORRUPT_DESCRIPTOR, "bad descriptor");
-  const int g = desc->g, K = desc->K, KG = K / g, R = pow3i(g);
+  const int g = desc->g, K = desc->K, KG = (K + g - 1) / g, R = pow3i(g);
   for (int m = 0; m < desc->M; ++m)
     for (int k = 0; k < KG; ++k) {
       int idx = payload[((size_t)(k / VLUT_KG_TILE) * mp + m) * 16 + (k % VLUT_KG_TILE)];
       if (idx >= R) return fail(VLUT_ERR_INVALID_TRIT, "corrupt payload byte %d at (%d,%d)", idx, m, k);
       for (int r = 0; r < g; ++r) {
-        w[(size_t)m * K + k * g + r] = (int8_t)(idx % 3 - 1);
+        if (k * g + r < K) w[(size_t)m * K + k * g + r] = (int8_t)(idx % 3 - 1);
         idx /= 3;
       }
     }
@@ -905,7 +927,6 @@ vlut_status vlut_unpack_weights_host(const vlut_packed_weights* desc, const uint
 vlut_status vlut_plan(int M, int K, int N, int g, vlut_launch_plan* plan) {
   if (!plan) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL plan");
   if (M <= 0 || K <= 0 || N <= 0 || !valid_g(g)) return fail(VLUT_ERR_INVALID_ARGUMENT, "bad sizes");
-  if (K % g) return fail(VLUT_ERR_SHAPE, "g=%d does not divide K=%d", g, K);
   DeviceInfo d;
   vlut_status st = device_info(&d);
   if (st != VLUT_OK) return st;
@@ -1001,7 +1022,6 @@ vlut_status vlut_mpgemm_allgather(const vlut_packed_weights* W, const int8_t* A,
 vlut_status vlut_plan_ws(int M, int K, int N, int g, vlut_launch_plan* plan) {
   if (!plan) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL plan");
   if (M <= 0 || K <= 0 || N <= 0 || !valid_g(g)) return fail(VLUT_ERR_INVALID_ARGUMENT, "bad sizes");
-  if (K % g) return fail(VLUT_ERR_SHAPE, "g=%d does not divide K=%d", g, K);
   DeviceInfo d;
   vlut_status st = device_info(&d);
   if (st != VLUT_OK) return st;

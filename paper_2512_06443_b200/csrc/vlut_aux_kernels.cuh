@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(256)
 __global__ void vlut_pack_kernel(const int8_t* __restrict__ w, int M, int K, int g, int m_pad,
                                  int kg_tiles, uint8_t* __restrict__ payload) {
   const long long total = (long long)kg_tiles * m_pad * 16;
-  const int KG = K / g;
+  const int KG = (K + g - 1) / g;  // a partial last group (padded packing) reads zero trits
   const int zero = (g == 4) ? 40 : 121;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
@@ -352,7 +352,7 @@ __global__ void vlut_pack_kernel(const int8_t* __restrict__ w, int M, int K, int
       idx = 0;
       int p3 = 1;
       for (int r = 0; r < g; ++r) {
-        int t = src[r];
+        int t = (k * g + r < K) ? src[r] : 0;
         t = t < -1 ? -1 : (t > 1 ? 1 : t);
         idx += (t + 1) * p3;
         p3 *= 3;

@@ -40,6 +40,17 @@ def test_exports_every_declared_symbol():
     assert b"sm_100a" in v.lib().vlut_version()
 
 
+def test_packed_bytes_padded():
+    # VLUT_PACK_PAD_K: ceil(K/g) groups; the same bytes per row as the mixed
+    # g=5/g=4 schedule for the configs' K (4096 -> 820 groups, 14336 -> 2868)
+    assert v.packed_bytes(128, 4096, 5) == 0                    # g does not divide K
+    assert v.packed_bytes(128, 4096, 5, v.PACK_PAD_K) == 52 * 128 * 16
+    assert v.packed_bytes(128, 14336, 5, v.PACK_PAD_K) == 180 * 128 * 16
+    assert v.packed_bytes(32, 7, 4, v.PACK_PAD_K) == 1 * 32 * 16
+    assert v.packed_bytes(32, 20, 5, v.PACK_PAD_K) == v.packed_bytes(32, 20, 5)
+    assert v.packed_bytes(32, 20, 5, 2) == 0                    # unknown flag
+
+
 def test_packed_bytes():
     assert v.packed_bytes(256, 512, 4) == 8 * 256 * 16          # 128 groups = 8 K-tiles
     assert v.packed_bytes(6912, 2560, 4) == 40 * 6912 * 16
