@@ -563,3 +563,29 @@ def test_padded_mpgemm_every_schedule(v, M, K, N, g, how):
     acc_ref = oracle.gemm_i32(W, q)
     assert np.array_equal(acc.cpu().numpy(), acc_ref)
     check_fp32(out.cpu().numpy(), acc_ref, s, synth.W_SCALE)
+
+
+def test_output_larger_than_2g_elements(v):
+    """M x N > 2^31 output elements (9.6 GB fp32): every offset into out, the
+    workspace and the epilogues must be 64-bit.  Sampled rows (first, last,
+    random) and the last token column vs the oracle."""
+    M, K, N, g = 40000, 20, 60000, 4
+    W = synth.ternary_weights(M, K, seed=99)
+    A = synth.int8_activations(K, N, seed=98)
+    s = synth.token_scales(N, seed=97)
+    pw = v.pack_weights(W, g, device=dev())
+    Ad, sd = to_dev(A), to_dev(s)
+    rows = np.unique(np.concatenate([[0, 1, M - 2, M - 1], synth.rng(5).integers(0, M, size=12)]))
+    ref = oracle.dequant_f32(oracle.gemm_i32(W[rows], A), s, synth.W_SCALE)
+    for how in ("auto", "cluster", "streamk"):
+        if how == "auto":
+            out = v.mpgemm(pw, Ad, sd, synth.W_SCALE)
+        elif how == "cluster":
+            out = v.mpgemm_ex(pw, Ad, sd, synth.W_SCALE)
+        else:
+            out = v.mpgemm_ws(pw, Ad, sd, synth.W_SCALE, plan=v.LaunchPlan(12, 1, m_cta=768, streamk=1))
+        torch.cuda.synchronize()
+        got = out[torch.from_numpy(rows).to(dev())].cpu().numpy()
+        assert np.array_equal(got.view(np.int32), ref.view(np.int32)), how
+        del out
+        torch.cuda.empty_cache()
