@@ -476,13 +476,29 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
       const int r = q * kLookupThreads + warp * 32 + lane;
       if constexpr (L::NTOK >= 4) {
         if (ld == L::NTOK) {  // 16-byte vector stores
+          constexpr int NCH = L::NTOK / 4;
+          int4 ch[NCH];
 #pragma unroll
-          for (int c = 0; c < L::NTOK / 4; ++c) {
+          for (int c = 0; c < NCH; ++c) {
             const int t0 = 4 * c;
-            *reinterpret_cast<int4*>(tile_s + r * L::NTOK + t0) =
-                make_int4(acc[q][t0 / TPW][t0 % TPW], acc[q][(t0 + 1) / TPW][(t0 + 1) % TPW],
-                          acc[q][(t0 + 2) / TPW][(t0 + 2) % TPW],
-                          acc[q][(t0 + 3) / TPW][(t0 + 3) % TPW]);
+            ch[c] = make_int4(acc[q][t0 / TPW][t0 % TPW], acc[q][(t0 + 1) / TPW][(t0 + 1) % TPW],
+                              acc[q][(t0 + 2) / TPW][(t0 + 2) % TPW],
+                              acc[q][(t0 + 3) / TPW][(t0 + 3) % TPW]);
+          }
+          if constexpr (NCH == 4) {
+            // 64-byte rows: lanes l and l+2 share banks; writing chunk
+            // (c + lane) & 3 in step c halves the conflicts (16- -> 8-way)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const int cc = (c + lane) & 3;
+              const int4 a = (cc & 1) ? ch[1] : ch[0];
+              const int4 b = (cc & 1) ? ch[3] : ch[2];
+              *reinterpret_cast<int4*>(tile_s + r * L::NTOK + 4 * cc) = (cc & 2) ? b : a;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < NCH; ++c)
+              *reinterpret_cast<int4*>(tile_s + r * L::NTOK + 4 * c) = ch[c];
           }
           continue;
         }
