@@ -97,7 +97,8 @@ typedef struct {
 typedef struct {
   int32_t warps;        /* 8, 12 or 16                                      */
   int32_t splits;       /* 1..8 (cluster size along K)                        */
-  int32_t m_cta;        /* 32 * warps                                       */
+  int32_t m_cta;        /* 32 * warps; stream-K only: 64 * warps (8 or 12
+                           warps) = two output rows per lookup thread       */
   int32_t n_cta;        /* 64                                               */
   int32_t grid_ctas;    /* total CTAs launched                              */
   int32_t smem_bytes;   /* dynamic shared memory per CTA                    */
