@@ -152,3 +152,24 @@ def test_allgather_shards_stay_in_their_rows(v, M, K, N, g, shards):
             o = b.t.cpu().numpy()
             assert np.array_equal(o[r0:r1].view(np.int32), ref32[r0:r1].view(np.int32))
             assert not o[:r0].any() and not o[r1:].any()
+
+
+def test_empty_inputs_are_noops(v):
+    """N = 0 (no tokens) through every entry point: status OK, nothing written."""
+    M, K, g = 300, 640, 4
+    W = synth.ternary_weights(M, K, seed=1)
+    pw = v.pack_weights(W, g, device=dev())
+    A = torch.empty((K, 0), dtype=torch.int8, device=dev())
+    s = torch.empty((0,), dtype=torch.float32, device=dev())
+    guard = Guarded((M, 1), torch.float32, fill=7)
+    out = guard.t[:, :0]
+    ws = v.workspace(dev())
+    v.mpgemm(pw, A, s, synth.W_SCALE, out=out)
+    v.mpgemm_ws(pw, A, s, synth.W_SCALE, out=out, ws=ws)
+    v.mpgemm_ex(pw, A, s, synth.W_SCALE, out=out)
+    v.mpgemm_scalar_lut(pw, A, s, synth.W_SCALE, out=out, ws=ws)
+    v.mpgemm_layout(pw, A, s, synth.W_SCALE, out=torch.empty((0, M), device=dev()))
+    q, sc = v.quantize(torch.empty((K, 0), device=dev()))
+    torch.cuda.synchronize()
+    assert guard.intact() and bool((guard.raw[GUARD:GUARD + guard.nbytes] == 7).all())
+    assert q.numel() == 0 and sc.numel() == 0
