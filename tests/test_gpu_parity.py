@@ -589,3 +589,31 @@ def test_output_larger_than_2g_elements(v):
         assert np.array_equal(got.view(np.int32), ref.view(np.int32)), how
         del out
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("a_off,o_off", [(1, 0), (4, 4), (8, 0), (0, 4)])
+@pytest.mark.parametrize("N", [64, 256])
+def test_misaligned_device_pointers(v, a_off, o_off, N):
+    """A and out at byte offsets that break 16-byte alignment: the kernels
+    fall back to 4-/1-byte activation staging (no TMA) and scalar stores;
+    every schedule still bit-exact."""
+    M, K, g = 700, 1280, 4
+    W = synth.ternary_weights(M, K, seed=a_off + N)
+    A = synth.int8_activations(K, N, seed=o_off + N)
+    s = synth.token_scales(N, seed=N)
+    pw = v.pack_weights(W, g, device=dev())
+    abuf = torch.zeros(K * N + 64, dtype=torch.int8, device=dev())
+    Ad = abuf[a_off:a_off + K * N].view(K, N)
+    Ad.copy_(torch.from_numpy(A))
+    obuf = torch.zeros(M * N + 16, dtype=torch.float32, device=dev())
+    out = obuf[o_off // 4:o_off // 4 + M * N].view(M, N)
+    sd = to_dev(s)
+    ref = oracle.gemm_i32(W, A)
+    plans = [None, v.LaunchPlan(12, 2), v.LaunchPlan(16, 1, streamk=1)]
+    if N <= 64:
+        plans.append(v.slot_plan(tpw=2))
+    for plan in plans:
+        out.zero_()
+        v.mpgemm_ws(pw, Ad, sd, 0.5, out=out, plan=plan)
+        torch.cuda.synchronize()
+        check_fp32(out.cpu().numpy(), ref, s, 0.5)
