@@ -335,14 +335,14 @@ double plan_for(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
 inline bool slot_variant_ok(int g, int nw, int tpw) {
   if (!(tpw == 1 || tpw == 2)) return false;
   if (!(nw == 1 || nw == 2 || nw == 4 || nw == 8)) return false;
-  return g == 4 || nw <= 2;
+  return g == 4 || nw <= 2 || (nw == 4 && tpw == 1);  // g = 5: half tables at 4 scalar words
 }
 inline int slot_mcta(int g) { return g == 4 ? 1024 : 2048; }
 int slot_smem(int g, int nw, int tpw);
 
 // The narrowest variant covering N tokens in one N-tile (capped at the widest).
 int slot_default_nw(int g, int N, int tpw) {
-  const int maxnw = g == 4 ? 8 : 2;
+  const int maxnw = g == 4 ? 8 : (tpw == 1 ? 4 : 2);
   int nw = 1;
   while (nw < maxnw && nw * tpw < N) nw *= 2;
   return nw;
@@ -380,7 +380,9 @@ double plan_slot(int M, int K, int N, int g, int sms, int tpw, int nw_force, int
   const long long ctas = tiles * S;
   const long long waves = (ctas + sms - 1) / sms;
   const double kt_per = (double)((kgt + S - 1) / S);
-  const double smem_tile = mcta * 16.0 * nw / 32.0 + (double)nw * pow3i(g) + mcta / 8.0;
+  // table rows: full 3^g, half tables for the scalar LUT from 4 words on
+  const double rows = (nw >= 4 && tpw == 1) ? (pow3i(g) + 1) / 2.0 : (double)pow3i(g);
+  const double smem_tile = mcta * 16.0 * nw / 32.0 + (double)nw * rows + mcta / 8.0;
   const double hbm_tile = mcta * 16.0 / 22.0;
   double per_cta = kt_per * (smem_tile > hbm_tile ? smem_tile : hbm_tile) + 3000.0;
   if (S > 1) per_cta += mcta * (double)ntok / 32.0 * 8.0;
@@ -433,7 +435,7 @@ vlut_status launch_slot(const vlut::slot::SlotParams& p, int S, int NTt, int MT,
 
 #define VLUT_SLOT_VARIANTS(X) \
   X(4, 1, 1) X(4, 2, 1) X(4, 4, 1) X(4, 8, 1) X(4, 1, 2) X(4, 2, 2) X(4, 4, 2) X(4, 8, 2) \
-  X(5, 1, 1) X(5, 2, 1) X(5, 1, 2) X(5, 2, 2)
+  X(5, 1, 1) X(5, 2, 1) X(5, 4, 1) X(5, 1, 2) X(5, 2, 2)
 
 int slot_smem(int g, int nw, int tpw) {
 #define X(G_, NW_, TPW_) \

@@ -82,7 +82,15 @@ struct SL {
   static constexpr int MCTA = 32 * kLW * RPL;     // 1024 (g=4) / 2048 (g=5)
   static constexpr int NTOK = NW * TPW;           // tokens per CTA
   static constexpr int NWP = (NW + 1) / 2;        // 256-B row blocks (word pairs)
-  static constexpr int TAB_BYTES = NWP * R * kRowStride;
+  // Scalar LUT (TPW = 1) with 4+ words per lookup: half tables (anti-symmetry
+  // T[i] = -T[3^g-1-i], positions p = |i - ZERO|, sign applied by a multiply
+  // at lookup) halve the build, whose share grows with NW; the per-index
+  // decode is shared by the NW words (measured: N = 16 53 -> 48 us).  The
+  // SWAR vector words lose more on the lookup path than they save (reverted
+  // there, DESIGN.md §4 K2).
+  static constexpr bool HALF = (NW >= 4 && TPW == 1);
+  static constexpr int ROWS = HALF ? (R + 1) / 2 : R;  // stored table rows
+  static constexpr int TAB_BYTES = NWP * ROWS * kRowStride;
   static constexpr int IDX_BYTES = MCTA * 16;
   static constexpr int ACT_BYTES = kKgTile * G * kActNMax;  // one K-tile of A, N <= 64
   static constexpr int FIXED = 2 * TAB_BYTES + 32 + 16 * kMaxStages + 16;
@@ -211,6 +219,42 @@ __device__ __forceinline__ void build_word(uint8_t* row_addr, const uint32_t (&U
   VLUT_CHAIN(0) VLUT_CHAIN(1) VLUT_CHAIN(2) VLUT_CHAIN(3) VLUT_CHAIN(4)
   VLUT_CHAIN(5) VLUT_CHAIN(6) VLUT_CHAIN(7) VLUT_CHAIN(8)
 #undef VLUT_CHAIN
+}
+
+// Half table of one scalar word (HALF): position 0 = the zero pattern; block
+// Lv = the patterns whose trits above Lv are 0, trit Lv = +1 and lower trits
+// free, at positions [(3^Lv+1)/2, (3^(Lv+1)+1)/2) (position = |i - ZERO|),
+// each walked along the base-3 reflected Gray code from all-lower-trits -1
+// (one add per entry).
+template <int G, int Lv>
+__device__ __forceinline__ void build_half_block(uint8_t* row, uint32_t S, const uint32_t (&P)[8],
+                                                 const uint32_t (&Mn)[8]) {
+  if constexpr (Lv < G) {
+    constexpr int P0 = (pow3(Lv) + 1) / 2;
+    uint32_t T = P[Lv] + S;  // trit Lv = +1, trits below -1 (S = their sum)
+    *reinterpret_cast<uint32_t*>(row + P0 * kRowStride) = T;
+    if constexpr (Lv > 0) {
+      constexpr GrayWalk<Lv> gw{};
+#pragma unroll
+      for (int s = 1; s < pow3(Lv); ++s) {
+        T += (gw.dir[s] > 0) ? P[gw.digit[s]] : Mn[gw.digit[s]];
+        *reinterpret_cast<uint32_t*>(row + (P0 + gw.idx[s]) * kRowStride) = T;
+      }
+    }
+    build_half_block<G, Lv + 1>(row, S + Mn[Lv], P, Mn);
+  }
+}
+
+template <int G>
+__device__ __forceinline__ void build_word_half(uint8_t* row_addr, const uint32_t (&U)[G]) {
+  uint32_t P[8], Mn[8];
+#pragma unroll
+  for (int r = 0; r < G; ++r) {
+    P[r] = U[r];
+    Mn[r] = 0u - U[r];
+  }
+  *reinterpret_cast<uint32_t*>(row_addr) = 0u;  // the zero pattern
+  build_half_block<G, 0>(row_addr, 0u, P, Mn);
 }
 
 // One activation value (token n of feature row k) for the builders: staged
@@ -359,9 +403,10 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
       for (int wi = 0; wi < WPB; ++wi) {
         const int w = (NW == 1) ? 0 : bw + wi * kBW;
         if (w < NW) {
-          uint8_t* row = smem + b * L::TAB_BYTES + (w >> 1) * L::R * kRowStride + (w & 1) * 128 +
+          uint8_t* row = smem + b * L::TAB_BYTES + (w >> 1) * L::ROWS * kRowStride + (w & 1) * 128 +
                          4 * lane;
-          build_word<G, NW, TPW>(row, U[wi], bw, NW == 1);
+          if constexpr (L::HALF) build_word_half<G>(row, U[wi]);
+          else build_word<G, NW, TPW>(row, U[wi], bw, NW == 1);
         }
       }
       __syncwarp();
@@ -381,7 +426,9 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
     const int qk = x >> 2;
     uint32_t selv[4];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) selv[b] = 0x5504u | ((uint32_t)(b ^ (x & 3)) << 4);
+    for (int b = 0; b < 4; ++b)
+      selv[b] = L::HALF ? (0x4440u | (uint32_t)(b ^ (x & 3)))  // index byte -> bits 0..7
+                        : (0x5504u | ((uint32_t)(b ^ (x & 3)) << 4));
     uint32_t sw[L::RPL][NW];
 #pragma unroll
     for (int q = 0; q < L::RPL; ++q)
@@ -422,12 +469,22 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
         for (int s = 0; s < kKgTile; ++s) {
           // byte (s & 3) ^ (x & 3) of Wp[s >> 2] -> bits 8..15, slot offset
           // (4 lane) ^ (4 s) -> bits 0..7: the entry's offset i * 256 + 4 slot
-          const uint32_t off = __byte_perm(Wp[s >> 2], (uint32_t)((4 * lane) ^ (4 * s)), selv[s & 3]);
+          uint32_t off;
+          int32_t sg = 1;
+          if constexpr (L::HALF) {
+            // position |i - ZERO| -> bits 8.., slot -> bits 0..7; sign +-1
+            const int d = (int)__byte_perm(Wp[s >> 2], 0u, selv[s & 3]) - L::ZERO;
+            const int m = d >> 31;
+            sg = m | 1;
+            off = ((uint32_t)((d ^ m) - m) << 8) | (uint32_t)((4 * lane) ^ (4 * s));
+          } else {
+            off = __byte_perm(Wp[s >> 2], (uint32_t)((4 * lane) ^ (4 * s)), selv[s & 3]);
+          }
 #pragma unroll
           for (int w = 0; w < NW; ++w) {
             const uint32_t val = *reinterpret_cast<const uint32_t*>(
-                smem + (B * L::TAB_BYTES + (w >> 1) * L::R * kRowStride + (w & 1) * 128) + off);
-            if constexpr (TPW == 1) acc[q][w][0] += (int32_t)val;
+                smem + (B * L::TAB_BYTES + (w >> 1) * L::ROWS * kRowStride + (w & 1) * 128) + off);
+            if constexpr (TPW == 1) acc[q][w][0] += L::HALF ? (int32_t)val * sg : (int32_t)val;
             else sw[q][w] += val;
           }
         }

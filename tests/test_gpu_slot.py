@@ -49,7 +49,7 @@ def check_fp32(got, acc_ref, a_scale, w_scale):
 
 
 VARIANTS = [(4, nw, tpw) for tpw in (1, 2) for nw in (1, 2, 4, 8)] + \
-           [(5, nw, tpw) for tpw in (1, 2) for nw in (1, 2)]
+           [(5, nw, tpw) for tpw in (1, 2) for nw in (1, 2)] + [(5, 4, 1)]
 
 # (M, K, N): ragged M (not a multiple of 32 / of m_cta), K-tiles with a
 # ragged last tile, N not a multiple of the CTA's token count
