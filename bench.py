@@ -11,6 +11,10 @@ once, offline (a1), before timing.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
+With --gpus N > 1 and no WORLD_SIZE in the environment, bench.py re-launches
+itself under torch.distributed.run with N ranks (one per GPU, 127.0.0.1
+rendezvous); n_gpus reports the ranks that joined the process group.
+
 Prints ONE JSON line on rank 0.  Timing: CUDA events on the launching stream
 around each step's kernels; the L2 is flushed (256 MiB memset) between steps
 outside those windows; the sum of per-step durations is the timed total, max
@@ -125,6 +129,118 @@ def workload(args):
                 w_seed=synth.weight_seed(cfg, 0, 0), x_seed=synth.act_seed(cfg, cfg.N[0]))
 
 
+def bench_config(wl, world):
+    """The `config` object of the JSON line -- identical for both arms (the
+    driver compares them); implementation details go to other keys."""
+    return {"workload": "configs[1]: BitNet-2B FFN-up ternary linear", "M": wl["M"],
+            "K": wl["K"], "N": wl["N"], "g": wl["g"],
+            "weights": "iid ternary P(0)=0.4 P(+-1)=0.3, seeded",
+            "activations": "N(0,1) fp32, per-token int8 absmax quantized",
+            "step": "per-token int8 quantize + ternary mpGeMM + fp32 dequant"
+                    + (" + all-gather of output row shards" if world > 1 else ""),
+            "parallelism": f"row-shard M over {world} GPU(s)" if world > 1 else "single GPU",
+            "l2": "flushed between steps (256 MiB memset outside each step's event window)"}
+
+
+def free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def maybe_spawn(args):
+    """--gpus N > 1 without a torch.distributed launcher: re-run this script
+    under torch.distributed.run with N ranks and return its exit code (rank 0
+    prints the JSON line).  None when no spawn is needed."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def comm_check(dist, dev):
+    """The communicator every rank joined: its size and one all-reduce over
+    it (sum of ones == world); logged to stderr and put in the JSON line."""
+    import torch
+    world = dist.get_world_size()
+    t = torch.ones(1, device=dev)
+    dist.all_reduce(t)
+    ok = int(t.item()) == world
+    print(f"[rank {dist.get_rank()}] {dist.get_backend()} communicator: nranks={world} "
+          f"all_reduce_ok={ok}", file=sys.stderr, flush=True)
+    return {"backend": dist.get_backend(), "nranks": world, "all_reduce_ok": ok}
+
+
+def plumbing_main(args):
+    """CPU check of the multi-rank bench plumbing (-m "not gpu" tests): the
+    spawn, process-group join, row sharding with padding, the all-gather and
+    the max-over-ranks timing, over gloo.  The per-shard compute, quantizer
+    and reference are injected from a TEST module (args.plumbing, a file
+    under tests/): bench.py itself computes nothing here, and the line says
+    it is a plumbing check, not a measurement."""
+    import importlib.util
+    import torch
+    import torch.distributed as dist
+    from paper_2512_06443_b200.sharded import RowShardedLinear
+    path = os.path.abspath(args.plumbing)
+    if os.path.basename(os.path.dirname(path)) != "tests":
+        raise SystemExit("--plumbing takes a module under tests/")
+    spec = importlib.util.spec_from_file_location("bench_plumbing_hooks", path)
+    hooks = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(hooks)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        dist.init_process_group("gloo")
+        world = dist.get_world_size()
+    rank = dist.get_rank() if world > 1 else 0
+    comm = comm_check(dist, torch.device("cpu")) if world > 1 else None
+    M, K, N, g = 1001, 256, 32, 4  # M odd: the last shard is padded
+    W = synth.ternary_weights(M, K, 2000, 0.4)
+    x = synth.activations_f32(K, N, 2100)
+    q, s = hooks.quantize(x)
+    lin = RowShardedLinear(W, g, synth.W_SCALE, compute=hooks.compute(synth.W_SCALE),
+                           pack=lambda w, g_: w)
+    for _ in range(args.warmup):
+        out = lin(q, s)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        out = lin(q, s)
+    el = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([el], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t[0])
+    exact = bool(np.array_equal(out.numpy().view(np.int32),
+                                hooks.reference(W, q, s, synth.W_SCALE).view(np.int32)))
+    if world > 1:
+        e = torch.tensor([1 if exact else 0])
+        dist.all_reduce(e, op=dist.ReduceOp.MIN)
+        exact = bool(e.item())
+    if rank == 0:
+        print(json.dumps({"impl": "plumbing-test", "metric": "plumbing check (not a measurement)",
+                          "value": None, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "comm": comm,
+                          "shard_rows": [list(map(int, sharded_rows(M, world, r)))
+                                         for r in range(world)],
+                          "gathered_equals_reference": exact,
+                          "seconds_max_over_ranks": el}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0 if exact else 1
+
+
+def sharded_rows(M, world, rank):
+    from paper_2512_06443_b200.sharded import shard_rows
+    return shard_rows(M, world, rank)
+
+
 def algorithmic(M, K, N, g):
     lookups = M * (K // g) * N
     return dict(lookups=lookups, smem_bytes=2 * lookups,
@@ -163,6 +279,7 @@ def cpu_baseline(W, x, N, budget_s=12.0, min_rows=32):
             break
     tok_s = N * (done / M) / el
     return {"value": tok_s, "unit": "tokens/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "omp_num_threads": oracle.omp_threads_env(), "build": " ".join(oracle.FLAGS),
             "sample": f"oracle quantize+int32 dot products+fp32 dequant on rows [0,{rows}) of "
                       f"the {M}-row workload, {reps} pass(es), {el:.1f} s; tokens/s scaled by "
                       f"rows/M", "seconds": el}
@@ -178,12 +295,13 @@ def run_reference(args):
     x = synth.activations_f32(K, N, wl["x_seed"])
     import oracle
     oracle.build()
-    # size each step so the whole run stays within ~2 minutes
+    # each step is the whole workload (all M rows) when the whole run fits
+    # ~2.5 minutes, else a row sample sized to fit (scaled by M / rows)
     t0 = time.perf_counter()
     oracle_pipeline_rows(W, x, 0, 32, synth.W_SCALE)
     per_row = (time.perf_counter() - t0) / 32
     total_steps = args.steps + args.warmup
-    step_budget = min(2.0, 100.0 / max(total_steps, 1))
+    step_budget = 150.0 / max(total_steps, 1)
     rows = int(min(M, max(8, step_budget / max(per_row, 1e-9))))
     for _ in range(args.warmup):
         oracle_pipeline_rows(W, x, 0, rows, synth.W_SCALE)
@@ -193,18 +311,21 @@ def run_reference(args):
     el = time.perf_counter() - t0
     sec_per_full_step = el / args.steps * (M / rows)
     val = N / sec_per_full_step
+    sample = ("each step: the whole workload (all rows)" if rows == M else
+              f"each step: rows [0,{rows}) of {M}, time scaled by M/rows")
     line = {
         "impl": "reference", "metric": "ternary Vec-LUT mpGeMM tokens/s (configs[1])",
         "value": val, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": sec_per_full_step * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "int32", "data": "synthetic",
-        "config": {"workload": "configs[1]: BitNet-2B FFN-up ternary linear", "M": M, "K": K,
-                   "N": N, "g": g},
+        "config": bench_config(wl, args.gpus),
         "cpu_baseline": {"value": val, "unit": "tokens/s", "kind": "oracle",
                          "cores": oracle.num_threads(),
-                         "sample": f"each step: oracle quantize + int32 dot products + fp32 "
-                                   f"dequant on rows [0,{rows}) of {M}; scaled by rows/M"},
+                         "omp_num_threads": oracle.omp_threads_env(),
+                         "build": " ".join(oracle.FLAGS),
+                         "sample": "oracle quantize + int32 dot products + fp32 dequant; "
+                                   + sample},
         "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -237,7 +358,15 @@ def main():
                     help="write SURVEY §8(d)'s per-(config, N, g) CSV (GPU timings, roofline "
                          "fractions, clocks, and the oracle's GOPS on a bounded row sample "
                          "as the cpu baseline of each row) to this path and exit")
+    ap.add_argument("--plumbing", default="",
+                    help="CPU check of the multi-rank plumbing over gloo with compute "
+                         "injected from this tests/ module (not a measurement)")
     args = ap.parse_args()
+    rc = maybe_spawn(args)
+    if rc is not None:
+        return rc
+    if args.plumbing:
+        return plumbing_main(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.table:
@@ -249,14 +378,17 @@ def main():
     import torch.distributed as dist
     import paper_2512_06443_b200 as v
 
+    from paper_2512_06443_b200.sharded import shard_rows
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+    comm = None
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        comm = comm_check(dist, dev)
+        world = dist.get_world_size()  # the ranks that joined
+    rank = dist.get_rank() if world > 1 else 0
     stream = torch.cuda.current_stream()
 
     peaks, peaks_src = load_peaks()
@@ -266,16 +398,19 @@ def main():
 
     # ---- offline: weights (row shard of this rank) packed on device (a1)
     W = synth.ternary_weights(M, K, wl["w_seed"], wl["p_zero"])
-    assert M % world == 0
-    Ms = M // world
-    W_r = W[rank * Ms:(rank + 1) * Ms]
+    # rank's contiguous rows [r0, r1); shards padded to Mp rows for the gather
+    r0, r1, Mp = shard_rows(M, world, rank)
+    Ms = r1 - r0
+    W_r = W[r0:r1]
     pw = v.pack_weights_device(torch.from_numpy(np.ascontiguousarray(W_r)).to(dev), g)
     x_host = synth.activations_f32(K, N, wl["x_seed"])
     x = torch.from_numpy(x_host).to(dev)
     q = torch.empty((K, N), dtype=torch.int8, device=dev)
     s = torch.empty((N,), dtype=torch.float32, device=dev)
-    out_r = torch.empty((Ms, N), dtype=torch.float32, device=dev)
-    out_full = torch.empty((M, N), dtype=torch.float32, device=dev) if world > 1 else out_r
+    out_loc = torch.zeros((Mp, N), dtype=torch.float32, device=dev)  # pad rows stay 0
+    out_r = out_loc[:Ms]
+    gathered = torch.empty((Mp * world, N), dtype=torch.float32, device=dev) if world > 1 else None
+    out_full = gathered[:M] if world > 1 else out_r
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
     ws = v.workspace(dev)
@@ -292,14 +427,14 @@ def main():
             peer = PeerOutputs()
             v.quantize(x, q=q, scale=s, stream=stream)
             v.mpgemm_ws(pw, q, s, synth.W_SCALE, out=out_r, ws=ws, stream=stream)
-            dist.all_gather_into_tensor(out_full, out_r)
+            dist.all_gather_into_tensor(gathered, out_loc)
             def validate(pe):
                 for _ in range(2):  # both alternating buffers
                     buf, target, peers, barrier = pe.get(M, N, dev)
                     buf.fill_(float("nan"))
                     torch.cuda.synchronize()
                     dist.barrier()
-                    v.mpgemm_allgather(pw, q, s, synth.W_SCALE, target, rank * Ms, peers,
+                    v.mpgemm_allgather(pw, q, s, synth.W_SCALE, target, r0, peers,
                                        stream=stream)
                     barrier()
                     torch.cuda.synchronize()
@@ -324,12 +459,12 @@ def main():
         v.quantize(x, q=q, scale=s, stream=stream)
         if peer is not None:
             buf, target, peers, barrier = peer.get(M, N, dev)
-            v.mpgemm_allgather(pw, q, s, synth.W_SCALE, target, rank * Ms, peers, stream=stream)
+            v.mpgemm_allgather(pw, q, s, synth.W_SCALE, target, r0, peers, stream=stream)
             barrier()
             return
         v.mpgemm_ws(pw, q, s, synth.W_SCALE, out=out_r, ws=ws, stream=stream)
         if world > 1:
-            dist.all_gather_into_tensor(out_full, out_r)
+            dist.all_gather_into_tensor(gathered, out_loc)
 
     # ---- warm-up: W steps, plus >= 0.3 s of work so clocks leave idle
     for _ in range(args.warmup):
@@ -410,10 +545,13 @@ def main():
         o_pins = [torch.empty((Ms, N), dtype=torch.float32).pin_memory() for _ in range(depth)]
         post = None
         if world > 1:
-            fulls = [torch.empty((M, N), dtype=torch.float32, device=dev) for _ in range(depth)]
+            locs = [torch.zeros((Mp, N), dtype=torch.float32, device=dev) for _ in range(depth)]
+            fulls = [torch.empty((Mp * world, N), dtype=torch.float32, device=dev)
+                     for _ in range(depth)]
 
             def post(res, st, slot):
-                dist.all_gather_into_tensor(fulls[slot], res)
+                locs[slot][:Ms].copy_(res)
+                dist.all_gather_into_tensor(fulls[slot], locs[slot])
                 return res  # each rank downloads its own row shard
         pipe = HostPipeline(pw, synth.W_SCALE, K, N, dev, depth=depth, ws=ws, post=post)
         e2e_steps = max(6, min(args.steps, 100))
@@ -458,16 +596,21 @@ def main():
     sm_max = float(peaks.get("sm_max_mhz", SM_MAX_MHZ_FALLBACK))
     smem_peak_gbs = SM_COUNT * SMEM_BYTES_PER_CLK_SM * sm_max * 1e6 / 1e9
     achieved = a_shard["smem_bytes"] / (k1_mean * 1e-3) / 1e9
-    traffic = None
+    # traffic: dram__bytes_read.sum + dram__bytes_write.sum of one K1 launch
+    # from an ncu --set full capture (ncu cannot run inside this timed
+    # process); the file names the capture and the build it was taken of
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "k1_dram_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+            tj = json.load(open(tpath))
+            traffic = tj.get("dram_bytes_per_launch")
+            traffic_src = f"profiles/k1_dram_traffic.json <- {tj.get('source', '?')}"
         except Exception:
             traffic = None
     roofline = {
         "bound": "smem", "achieved": achieved, "peak": smem_peak_gbs, "unit": "GB/s",
-        "frac": achieved / smem_peak_gbs, "traffic": traffic,
+        "frac": achieved / smem_peak_gbs, "traffic": traffic, "traffic_source": traffic_src,
         "kernel": "vlut_mpgemm_kernel (K1)",
         "algorithmic_bytes_per_launch": a_shard["smem_bytes"],
         "per_unit": "2 B of shared-memory table read per int16 lookup-add; lookups = M*(K/g)*N",
@@ -489,17 +632,14 @@ def main():
         "dtype_detail": "int8 activations x ternary (base-3 packed) weights; int16 LUT "
                         "lookup-adds, int32 accumulation, fp32 dequant",
         "data": "synthetic",
-        "config": {"workload": "configs[1]: BitNet-2B FFN-up ternary linear", "M": M, "K": K,
-                   "N": N, "g": g, "weights": "iid ternary P(0)=0.4 P(+-1)=0.3, seeded",
-                   "activations": "N(0,1) fp32, per-token int8 absmax quantized on GPU",
-                   "step": "quantize (K3) + fused Vec-LUT mpGeMM + fp32 dequant (K1)"
-                           + ((" with the all-gather of row shards fused into the epilogue "
-                               "(NVLink peer stores + cross-GPU barrier)" if peer is not None
-                               else " + NCCL all-gather of row shards") if world > 1 else ""),
-                   "gather": gather,
-                   "parallelism": f"row-shard M over {world} GPU(s)" if world > 1 else "single GPU",
-                   "plan": plan.__dict__,
-                   "l2": "flushed between steps (256 MiB memset outside each step's event window)"},
+        "config": bench_config(wl, world),
+        "kernels": "K3 quantize + fused Vec-LUT mpGeMM with fp32 dequant (K1)"
+                   + ((" with the all-gather of row shards fused into the epilogue "
+                       "(NVLink peer stores + cross-GPU barrier)" if peer is not None
+                       else " + NCCL all-gather of row shards") if world > 1 else ""),
+        "gather": gather,
+        "plan": plan.__dict__,
+        "comm": comm,
         "gops": alg["dense_ops"] * args.steps / (total_ms * 1e-3) / 1e9,
         "gpu_launches": args.steps * vlut_launches_per_step(v, plan),
         "roofline": roofline,

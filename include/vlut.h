@@ -16,10 +16,24 @@
  *     as void* (0 = legacy default stream).
  *   - The caller owns every buffer.  The library allocates device memory in
  *     one place only: vlut_mpgemm (the north-star signature, which has no
- *     workspace argument) keeps one workspace per (device, stream), allocated
- *     and zeroed on first use and kept for the life of the process.  Other
- *     global state: a thread-local error string and per-device
- *     property/attribute caches.
+ *     workspace argument) keeps a bounded cache of workspaces (~36 MB each on
+ *     B200): at most 4 per device, each bound to one stream by its
+ *     process-unique id (cudaStreamGetId -- a destroyed-then-recycled stream
+ *     handle never aliases an old entry).  Created and zeroed on a stream's
+ *     first call; a fifth stream takes the least recently used entry after a
+ *     device-wide synchronisation.  Never allocated, evicted or used inside a
+ *     stream capture (a captured vlut_mpgemm runs the cluster schedule).
+ *     vlut_release_workspaces() frees them all.  Other global state: a
+ *     thread-local error string and per-device property/attribute caches.
+ *   - Weight payloads are read before the kernels' griddepcontrol.wait
+ *     (programmatic dependent launch overlaps the weight stream with the
+ *     tail of the previous kernel): a payload must NOT be written by the
+ *     kernel launched immediately before an mpGeMM call on the same stream.
+ *     Payloads written by vlut_pack_weights (which synchronises) and
+ *     vlut_pack_weights_device (which ends with an event record on its
+ *     stream, turning the next launch into an ordinary dependent) satisfy
+ *     this.  Activations, scales and accumulators may come from the previous
+ *     kernel.
  *   - Arguments are validated on the host before anything is launched.  On
  *     failure nothing is launched, a status != VLUT_OK is returned and
  *     vlut_last_error() describes it.  Nothing aborts or throws across the ABI.
@@ -208,11 +222,14 @@ vlut_status vlut_mpgemm_ex(const vlut_packed_weights* W, const int8_t* A,
  * cost model (plan == NULL) unless plan->streamk / plan->slot forces one.
  *   workspace : device, >= vlut_workspace_bytes() bytes, 16-B aligned, ZEROED
  *               ONCE before its first use, and used by one stream at a time.
- *               Regions: stream-K partials and epoch flags (flags are
- *               per-launch epochs), K2 split-K arrival counts and int32
+ *               Regions: stream-K partials and partial-ready flags (each
+ *               flag is set by its producer CTA and reset by its consumer in
+ *               the same launch), K2 split-K arrival counts and int32
  *               accumulators (every K2 launch leaves them zero again) and
- *               per-tile generation words (monotonic).  A K2 split-K launch
- *               is cooperative: its CTAs must be co-resident.
+ *               per-tile generation words (monotonic, read on the device).
+ *               No host-side per-launch state: captured CUDA graphs may be
+ *               replayed.  Stream-K and K2 split-K launches are cooperative
+ *               (their CTAs wait for each other, so all are co-resident).
  * vlut_workspace_bytes() returns 0 without a CUDA device (~36 MB on B200).
  */
 size_t vlut_workspace_bytes(void);
@@ -343,6 +360,14 @@ vlut_status vlut_mpgemm_allgather(const vlut_packed_weights* W, const int8_t* A,
  */
 vlut_status vlut_quantize(const float* x, const float* y, int K, int N,
                           int8_t* q, float* scale, void* stream);
+
+/* The library's vlut_mpgemm workspaces (see Conventions): the number
+ * currently cached (all devices), and a release of all of them (synchronises
+ * each device that holds one, then frees; the next vlut_mpgemm call on a
+ * stream re-creates its workspace).  Call release only when no other thread
+ * is inside a libvlut call. */
+int vlut_cached_workspaces(void);
+vlut_status vlut_release_workspaces(void);
 
 /* Number of kernel launches one vlut_mpgemm/vlut_mpgemm_acc call enqueues
  * (1: the whole path, split-K reduction included, is one cluster launch). */

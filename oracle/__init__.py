@@ -28,14 +28,52 @@ _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 
+FLAGS = ["-O3", "-march=native", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
+         "-fPIC", "-shared"]
+_STAMP = _LIB_PATH + ".host"
+
+
+def _host_key() -> str:
+    """Compiler flags + this host's CPU model: -march=native code built on
+    one machine must not run on another (the GPU box is not this container)."""
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith(("model name", "flags")):
+                    model += line.strip() + "\n"
+                    if line.startswith("flags"):
+                        break
+    except OSError:
+        pass
+    return " ".join(FLAGS) + "\n" + model
+
+
 def build(force: bool = False) -> str:
-    """Compile oracle.c with gcc (plain C, OpenMP over rows, IEEE fp)."""
-    if force or not os.path.exists(_LIB_PATH) or (
-            os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC)):
-        cmd = ["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
-               "-fPIC", "-shared", _SRC, "-o", _LIB_PATH, "-lm"]
-        subprocess.check_call(cmd)
+    """Compile oracle.c with gcc -O3 -march=native (plain C, OpenMP over rows,
+    IEEE fp: no FMA contraction, no fast-math -- SURVEY §8(c)/(d)).  Rebuilt
+    when the source is newer or the host CPU / flags differ."""
+    key = _host_key()
+    stale = force or not os.path.exists(_LIB_PATH) or (
+        os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC))
+    if not stale:
+        try:
+            with open(_STAMP) as f:
+                stale = f.read() != key
+        except OSError:
+            stale = True
+    if stale:
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc"] + FLAGS + [_SRC, "-o", tmp, "-lm"])
+        os.replace(tmp, _LIB_PATH)
+        with open(_STAMP, "w") as f:
+            f.write(key)
     return _LIB_PATH
+
+
+def omp_threads_env() -> str:
+    """OMP_NUM_THREADS as seen by the oracle (unset -> all host threads)."""
+    return os.environ.get("OMP_NUM_THREADS", "unset")
 
 
 def _load():

@@ -27,6 +27,7 @@ __all__ = [
     "MixedPackedWeights", "pack_weights_mixed", "mpgemm_mixed", "mpgemm_layout", "quantize_t",
     "linear", "workspace", "plan_ws", "mpgemm_ws", "mpgemm_acc_ws", "mpgemm_fused",
     "quantize_amax", "mpgemm_scalar_lut", "slot_plan", "mpgemm_allgather",
+    "cached_workspaces", "release_workspaces",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -142,6 +143,8 @@ EXPORTS = {
                                ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
                                ctypes.c_int, ctypes.c_void_p], ctypes.c_int),
     "vlut_launches_per_mpgemm": ([], ctypes.c_int),
+    "vlut_cached_workspaces": ([], ctypes.c_int),
+    "vlut_release_workspaces": ([], ctypes.c_int),
     "vlut_active_clusters": ([ctypes.c_int, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "vlut_last_error": ([], ctypes.c_char_p),
     "vlut_version": ([], ctypes.c_char_p),
@@ -176,11 +179,17 @@ def _check(st: int) -> None:
         raise VlutError(st, last_error())
 
 
-def _stream_ptr(stream) -> ctypes.c_void_p:
+def _stream(stream, device=None):
+    """The stream to launch on: ``stream``, else the current stream of
+    ``device`` (the device of the call's tensors), never another GPU's."""
     import torch
     if stream is None:
-        stream = torch.cuda.current_stream()
-    return ctypes.c_void_p(stream.cuda_stream)
+        stream = torch.cuda.current_stream(device)
+    return stream
+
+
+def _stream_ptr(stream, device=None) -> ctypes.c_void_p:
+    return ctypes.c_void_p(_stream(stream, device).cuda_stream)
 
 
 def _dev_ptr(t) -> ctypes.c_void_p:
@@ -191,6 +200,47 @@ def _dev_ptr(t) -> ctypes.c_void_p:
     if not t.is_contiguous():
         raise ValueError("expected a contiguous tensor")
     return ctypes.c_void_p(t.data_ptr())
+
+
+def _arg(t, name: str, dtype, shape=None, device=None, optional: bool = False):
+    """Device pointer of tensor ``t`` after checking what the C entry point
+    will assume about it (dtype, exact shape, device, contiguity): a wrong
+    dtype or a short buffer would otherwise be read or written past its end."""
+    import torch
+    if t is None:
+        if optional:
+            return ctypes.c_void_p(0)
+        raise ValueError(f"{name}: required")
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name}: expected a torch tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name}: expected a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name}: on {t.device}, expected {device}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: expected a contiguous tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _act(A):
+    """(K, N, device) of int8 activations [K][N]."""
+    import torch
+    if not isinstance(A, torch.Tensor) or A.dim() != 2:
+        raise ValueError("A: expected a 2-D int8 CUDA tensor [K][N]")
+    if A.dtype != torch.int8:
+        raise TypeError(f"A: expected torch.int8, got {A.dtype}")
+    return int(A.shape[0]), int(A.shape[1]), A.device
+
+
+def _ws_arg(ws, device):
+    import torch
+    if ws is None:
+        return ctypes.c_void_p(0), 0
+    return _arg(ws, "ws", torch.uint8, device=device), int(ws.numel())
 
 
 @dataclass
@@ -268,13 +318,15 @@ def pack_weights(w_trits: np.ndarray, g: int, device=None, stream=None,
     with torch.cuda.device(payload.device):
         _check(lib().vlut_pack_weights_ex(ctypes.c_void_p(w.ctypes.data), M, K, g, flags,
                                           _dev_ptr(payload), nb, ctypes.byref(d),
-                                          _stream_ptr(stream)))
+                                          _stream_ptr(stream, payload.device)))
     return PackedWeights(payload, d)
 
 
 def pack_weights_device(w_trits, g: int, stream=None, pad_k: bool = False) -> PackedWeights:
     """Device trits (torch int8 CUDA [M][K]) -> packed weights, on the GPU."""
     import torch
+    if w_trits.dim() != 2:
+        raise ValueError("w_trits: expected [M][K]")
     M, K = w_trits.shape
     flags = PACK_PAD_K if pad_k else 0
     nb = packed_bytes(M, K, g, flags)
@@ -283,9 +335,10 @@ def pack_weights_device(w_trits, g: int, stream=None, pad_k: bool = False) -> Pa
     payload = torch.empty(nb, dtype=torch.uint8, device=w_trits.device)
     d = _Desc()
     with torch.cuda.device(payload.device):
-        _check(lib().vlut_pack_weights_device_ex(_dev_ptr(w_trits), M, K, g, flags,
+        _check(lib().vlut_pack_weights_device_ex(_arg(w_trits, "w_trits", torch.int8),
+                                                 M, K, g, flags,
                                                  _dev_ptr(payload), nb, ctypes.byref(d),
-                                                 _stream_ptr(stream)))
+                                                 _stream_ptr(stream, payload.device)))
     return PackedWeights(payload, d)
 
 
@@ -311,18 +364,33 @@ def _plan_ptr(p: Optional[LaunchPlan]):
     return c, ctypes.byref(c)
 
 
+def _weights(W: PackedWeights, K: int, dev):
+    if W.K != K:
+        raise ValueError(f"W has K={W.K}, A has {K} rows")
+    if W.payload.device != dev:
+        raise ValueError(f"W payload on {W.payload.device}, A on {dev}")
+    return ctypes.byref(W.desc)
+
+
+def _out(out, shape, dtype, dev, name="out"):
+    import torch
+    if out is None:
+        out = torch.empty(shape, dtype=dtype, device=dev)
+    return out, _arg(out, name, dtype, shape, dev)
+
+
 def mpgemm_ex(W: PackedWeights, A, a_scale, w_scale: float, out=None,
               plan: Optional[LaunchPlan] = None, stream=None):
     """fp32 out[M][N] = dequant(W x A) (a2-a6).  A: torch int8 CUDA [K][N]."""
     import torch
-    K, N = A.shape
+    K, N, dev = _act(A)
     M = W.M
-    if out is None:
-        out = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    out, op = _out(out, (M, N), torch.float32, dev)
     keep, pp = _plan_ptr(plan)
-    _check(lib().vlut_mpgemm_ex(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(a_scale),
-                                float(w_scale), _dev_ptr(out), M, K, N, pp,
-                                _stream_ptr(stream)))
+    with torch.cuda.device(dev):
+        _check(lib().vlut_mpgemm_ex(_weights(W, K, dev), _dev_ptr(A),
+                                    _arg(a_scale, "a_scale", torch.float32, (N,), dev),
+                                    float(w_scale), op, M, K, N, pp, _stream_ptr(stream, dev)))
     return out
 
 
@@ -330,38 +398,42 @@ def mpgemm(W: PackedWeights, A, a_scale, w_scale: float, out=None, stream=None):
     """The north-star entry point vlut_mpgemm(W_packed, A_int8, a_scale,
     w_scale, out, M, K, N, stream)."""
     import torch
-    K, N = A.shape
+    K, N, dev = _act(A)
     M = W.M
-    if out is None:
-        out = torch.empty((M, N), dtype=torch.float32, device=A.device)
-    _check(lib().vlut_mpgemm(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(a_scale),
-                             float(w_scale), _dev_ptr(out), M, K, N, _stream_ptr(stream)))
+    out, op = _out(out, (M, N), torch.float32, dev)
+    with torch.cuda.device(dev):
+        _check(lib().vlut_mpgemm(_weights(W, K, dev), _dev_ptr(A),
+                                 _arg(a_scale, "a_scale", torch.float32, (N,), dev),
+                                 float(w_scale), op, M, K, N, _stream_ptr(stream, dev)))
     return out
 
 
 def mpgemm_acc(W: PackedWeights, A, out=None, plan: Optional[LaunchPlan] = None, stream=None):
     """Raw int32 accumulators [M][N] (bit-exact test hook)."""
     import torch
-    K, N = A.shape
+    K, N, dev = _act(A)
     M = W.M
-    if out is None:
-        out = torch.empty((M, N), dtype=torch.int32, device=A.device)
+    out, op = _out(out, (M, N), torch.int32, dev)
     keep, pp = _plan_ptr(plan)
-    _check(lib().vlut_mpgemm_acc(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(out), M, K, N,
-                                 pp, _stream_ptr(stream)))
+    with torch.cuda.device(dev):
+        _check(lib().vlut_mpgemm_acc(_weights(W, K, dev), _dev_ptr(A), op, M, K, N, pp,
+                                     _stream_ptr(stream, dev)))
     return out
 
 
 def quantize(x, y=None, q=None, scale=None, stream=None):
     """Per-token absmax int8 quantizer of fp32 [K][N] (x * y if y given)."""
     import torch
+    if x.dim() != 2:
+        raise ValueError("x: expected fp32 [K][N]")
     K, N = x.shape
-    if q is None:
-        q = torch.empty((K, N), dtype=torch.int8, device=x.device)
-    if scale is None:
-        scale = torch.empty((N,), dtype=torch.float32, device=x.device)
-    _check(lib().vlut_quantize(_dev_ptr(x), _dev_ptr(y), K, N, _dev_ptr(q), _dev_ptr(scale),
-                               _stream_ptr(stream)))
+    dev = x.device
+    q, qp = _out(q, (K, N), torch.int8, dev, "q")
+    scale, sp = _out(scale, (N,), torch.float32, dev, "scale")
+    with torch.cuda.device(dev):
+        _check(lib().vlut_quantize(_arg(x, "x", torch.float32, device=dev),
+                                   _arg(y, "y", torch.float32, (K, N), dev, optional=True),
+                                   K, N, qp, sp, _stream_ptr(stream, dev)))
     return q, scale
 
 
@@ -398,14 +470,18 @@ def pack_weights_mixed(w_trits: np.ndarray, device=None, stream=None) -> MixedPa
 def mpgemm_mixed(W: MixedPackedWeights, A, a_scale, w_scale: float, out=None, ws=None,
                  stream=None):
     import torch
-    K, N = A.shape
-    if out is None:
-        out = torch.empty((W.M, N), dtype=torch.float32, device=A.device)
+    K, N, dev = _act(A)
+    if W.K != K:
+        raise ValueError(f"W has K={W.K}, A has {K} rows")
+    out, op = _out(out, (W.M, N), torch.float32, dev)
     d5 = ctypes.byref(W.w5.desc) if W.w5 is not None else ctypes.POINTER(_Desc)()
     d4 = ctypes.byref(W.w4.desc) if W.w4 is not None else ctypes.POINTER(_Desc)()
-    wsp, wsn = (_dev_ptr(ws), ws.numel()) if ws is not None else (ctypes.c_void_p(0), 0)
-    _check(lib().vlut_mpgemm_mixed_ws(d5, d4, _dev_ptr(A), _dev_ptr(a_scale), float(w_scale),
-                                      _dev_ptr(out), W.M, K, N, wsp, wsn, _stream_ptr(stream)))
+    wsp, wsn = _ws_arg(ws, dev)
+    with torch.cuda.device(dev):
+        _check(lib().vlut_mpgemm_mixed_ws(d5, d4, _dev_ptr(A),
+                                          _arg(a_scale, "a_scale", torch.float32, (N,), dev),
+                                          float(w_scale), op, W.M, K, N, wsp, wsn,
+                                          _stream_ptr(stream, dev)))
     return out
 
 
@@ -417,66 +493,102 @@ def mpgemm_layout(W: PackedWeights, A, a_scale, w_scale: float, out=None, featur
                   stream=None):
     """vlut_mpgemm with the fused output transposition: out [N][M] if feature_major."""
     import torch
-    K, N = A.shape
+    K, N, dev = _act(A)
     M = W.M
-    if out is None:
-        shape = (N, M) if feature_major else (M, N)
-        out = torch.empty(shape, dtype=torch.float32, device=A.device)
-    _check(lib().vlut_mpgemm_layout(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(a_scale),
-                                    float(w_scale), _dev_ptr(out), M, K, N,
-                                    OUT_FEATURE_MAJOR if feature_major else 0,
-                                    _stream_ptr(stream)))
+    out, op = _out(out, (N, M) if feature_major else (M, N), torch.float32, dev)
+    with torch.cuda.device(dev):
+        _check(lib().vlut_mpgemm_layout(_weights(W, K, dev), _dev_ptr(A),
+                                        _arg(a_scale, "a_scale", torch.float32, (N,), dev),
+                                        float(w_scale), op, M, K, N,
+                                        OUT_FEATURE_MAJOR if feature_major else 0,
+                                        _stream_ptr(stream, dev)))
     return out
 
 
 def quantize_t(x_nk, y_nk=None, q=None, scale=None, stream=None):
     """Per-token quantizer of feature-major fp32 [N][K] -> (int8 [K][N], fp32 [N])."""
     import torch
+    if x_nk.dim() != 2:
+        raise ValueError("x_nk: expected fp32 [N][K]")
     N, K = x_nk.shape
-    if q is None:
-        q = torch.empty((K, N), dtype=torch.int8, device=x_nk.device)
-    if scale is None:
-        scale = torch.empty((N,), dtype=torch.float32, device=x_nk.device)
-    _check(lib().vlut_quantize_t(_dev_ptr(x_nk), _dev_ptr(y_nk), K, N, _dev_ptr(q),
-                                 _dev_ptr(scale), _stream_ptr(stream)))
+    dev = x_nk.device
+    q, qp = _out(q, (K, N), torch.int8, dev, "q")
+    scale, sp = _out(scale, (N,), torch.float32, dev, "scale")
+    with torch.cuda.device(dev):
+        _check(lib().vlut_quantize_t(_arg(x_nk, "x_nk", torch.float32, device=dev),
+                                     _arg(y_nk, "y_nk", torch.float32, (N, K), dev, optional=True),
+                                     K, N, qp, sp, _stream_ptr(stream, dev)))
     return q, scale
 
 
 def linear(W: PackedWeights, x_nk, w_scale: float, y=None, q_ws=None, s_ws=None, stream=None):
     """Framework-layout ternary linear: x fp32 [N][K] -> y fp32 [N][M]."""
     import torch
+    if x_nk.dim() != 2:
+        raise ValueError("x_nk: expected fp32 [N][K]")
     N, K = x_nk.shape
     dev = x_nk.device
-    if y is None:
-        y = torch.empty((N, W.M), dtype=torch.float32, device=dev)
-    if q_ws is None:
-        q_ws = torch.empty((K, N), dtype=torch.int8, device=dev)
-    if s_ws is None:
-        s_ws = torch.empty((N,), dtype=torch.float32, device=dev)
-    _check(lib().vlut_linear(ctypes.byref(W.desc), _dev_ptr(x_nk), float(w_scale), _dev_ptr(y),
-                             W.M, K, N, _dev_ptr(q_ws), _dev_ptr(s_ws), _stream_ptr(stream)))
+    y, yp = _out(y, (N, W.M), torch.float32, dev, "y")
+    q_ws, qp = _out(q_ws, (K, N), torch.int8, dev, "q_ws")
+    s_ws, sp = _out(s_ws, (N,), torch.float32, dev, "s_ws")
+    with torch.cuda.device(dev):
+        _check(lib().vlut_linear(_weights(W, K, dev), _arg(x_nk, "x_nk", torch.float32, device=dev),
+                                 float(w_scale), yp, W.M, K, N, qp, sp, _stream_ptr(stream, dev)))
     return y
 
 
-# ---------------------------------------------------------------- stream-K workspace
+# ---------------------------------------------------------------- workspaces
+# One workspace per (device, stream): a workspace is used by one stream at a
+# time (vlut.h), and calls on one stream are ordered.  Bounded: a fifth stream
+# on a device evicts the least recently used entry after synchronising the
+# device (the evicted entry's stream may still be using it).
 _WS = {}
+_WS_CAP = 4
+_ws_tick = 0
 
 
-def workspace(device=None):
-    """The per-device stream-K workspace (zeroed once; one stream at a time)."""
+def workspace(device=None, stream=None):
+    """The zeroed workspace of (device, stream) (stream None: that device's
+    current stream) for the *_ws entry points."""
     import torch
+    global _ws_tick
     dev = torch.device(device or "cuda")
     if dev.index is None:
         dev = torch.device("cuda", torch.cuda.current_device())
-    ws = _WS.get(dev.index)
-    if ws is None:
-        with torch.cuda.device(dev):
-            nb = int(lib().vlut_workspace_bytes())
+    st = _stream(stream, dev)
+    key = (dev.index, int(st.cuda_stream))
+    _ws_tick += 1
+    ent = _WS.get(key)
+    if ent is not None:
+        ent[1] = _ws_tick
+        return ent[0]
+    same = [k for k in _WS if k[0] == dev.index]
+    with torch.cuda.device(dev):
+        if len(same) >= _WS_CAP:
+            torch.cuda.synchronize(dev)
+            del _WS[min(same, key=lambda k: _WS[k][1])]
+        nb = int(lib().vlut_workspace_bytes())
         if nb == 0:
             raise VlutError(7, "no CUDA device for the stream-K workspace")
-        ws = torch.zeros(nb, dtype=torch.uint8, device=dev)
-        _WS[dev.index] = ws
+        with torch.cuda.stream(st):
+            ws = torch.zeros(nb, dtype=torch.uint8, device=dev)
+    _WS[key] = [ws, _ws_tick]
     return ws
+
+
+def cached_workspaces() -> int:
+    """Workspaces the C library keeps for vlut_mpgemm (all devices)."""
+    return int(lib().vlut_cached_workspaces())
+
+
+def release_workspaces() -> None:
+    """Free the C library's vlut_mpgemm workspaces and this module's."""
+    import torch
+    _check(lib().vlut_release_workspaces())
+    if _WS:
+        for d in {k[0] for k in _WS}:
+            torch.cuda.synchronize(d)
+        _WS.clear()
 
 
 def plan_ws(M: int, K: int, N: int, g: int) -> LaunchPlan:
@@ -487,33 +599,39 @@ def plan_ws(M: int, K: int, N: int, g: int) -> LaunchPlan:
 
 def mpgemm_ws(W: PackedWeights, A, a_scale, w_scale: float, out=None,
               plan: Optional[LaunchPlan] = None, ws=None, stream=None):
-    """vlut_mpgemm with a workspace: the planner may pick the stream-K schedule."""
+    """vlut_mpgemm with a workspace: the planner may pick the stream-K schedule.
+    ws None: the workspace of (A's device, the launch stream)."""
     import torch
-    K, N = A.shape
+    K, N, dev = _act(A)
     M = W.M
-    if out is None:
-        out = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    st = _stream(stream, dev)
+    out, op = _out(out, (M, N), torch.float32, dev)
     if ws is None:
-        ws = workspace(A.device)
+        ws = workspace(dev, st)
+    wsp, wsn = _ws_arg(ws, dev)
     keep, pp = _plan_ptr(plan)
-    _check(lib().vlut_mpgemm_ws(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(a_scale),
-                                float(w_scale), _dev_ptr(out), M, K, N, pp, _dev_ptr(ws),
-                                ws.numel(), _stream_ptr(stream)))
+    with torch.cuda.device(dev):
+        _check(lib().vlut_mpgemm_ws(_weights(W, K, dev), _dev_ptr(A),
+                                    _arg(a_scale, "a_scale", torch.float32, (N,), dev),
+                                    float(w_scale), op, M, K, N, pp, wsp, wsn,
+                                    ctypes.c_void_p(st.cuda_stream)))
     return out
 
 
 def mpgemm_acc_ws(W: PackedWeights, A, out=None, plan: Optional[LaunchPlan] = None, ws=None,
                   stream=None):
     import torch
-    K, N = A.shape
+    K, N, dev = _act(A)
     M = W.M
-    if out is None:
-        out = torch.empty((M, N), dtype=torch.int32, device=A.device)
+    st = _stream(stream, dev)
+    out, op = _out(out, (M, N), torch.int32, dev)
     if ws is None:
-        ws = workspace(A.device)
+        ws = workspace(dev, st)
+    wsp, wsn = _ws_arg(ws, dev)
     keep, pp = _plan_ptr(plan)
-    _check(lib().vlut_mpgemm_acc_ws(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(out), M, K, N,
-                                    pp, _dev_ptr(ws), ws.numel(), _stream_ptr(stream)))
+    with torch.cuda.device(dev):
+        _check(lib().vlut_mpgemm_acc_ws(_weights(W, K, dev), _dev_ptr(A), op, M, K, N,
+                                        pp, wsp, wsn, ctypes.c_void_p(st.cuda_stream)))
     return out
 
 
@@ -525,29 +643,36 @@ def mpgemm_fused(W: PackedWeights, A, a_scale, w_scale: float, out=None, mul_in=
     atomically maxes |out| over rows < amax_rows into amax (int32 [N] viewed
     as float bits; zero it first).  Returns out."""
     import torch
-    K, N = A.shape
+    K, N, dev = _act(A)
     M = W.M
-    if out is None:
-        out = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    out, op = _out(out, (M, N), torch.float32, dev)
     rows = M if amax_rows is None else amax_rows
-    wsp, wsn = (_dev_ptr(ws), ws.numel()) if ws is not None else (ctypes.c_void_p(0), 0)
+    wsp, wsn = _ws_arg(ws, dev)
     keep, pp = _plan_ptr(plan)
-    _check(lib().vlut_mpgemm_fused(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(a_scale),
-                                   float(w_scale), _dev_ptr(out), M, K, N, _dev_ptr(mul_in),
-                                   _dev_ptr(amax), int(rows), pp, wsp, wsn, _stream_ptr(stream)))
+    with torch.cuda.device(dev):
+        _check(lib().vlut_mpgemm_fused(_weights(W, K, dev), _dev_ptr(A),
+                                       _arg(a_scale, "a_scale", torch.float32, (N,), dev),
+                                       float(w_scale), op, M, K, N,
+                                       _arg(mul_in, "mul_in", torch.float32, (M, N), dev,
+                                            optional=True),
+                                       _arg(amax, "amax", torch.int32, (N,), dev, optional=True),
+                                       int(rows), pp, wsp, wsn, _stream_ptr(stream, dev)))
     return out
 
 
 def quantize_amax(x, amax, q=None, scale=None, stream=None):
     """Quantize fp32 [K][N] with per-token maxima already known (f1)."""
     import torch
+    if x.dim() != 2:
+        raise ValueError("x: expected fp32 [K][N]")
     K, N = x.shape
-    if q is None:
-        q = torch.empty((K, N), dtype=torch.int8, device=x.device)
-    if scale is None:
-        scale = torch.empty((N,), dtype=torch.float32, device=x.device)
-    _check(lib().vlut_quantize_amax(_dev_ptr(x), _dev_ptr(amax), K, N, _dev_ptr(q),
-                                    _dev_ptr(scale), _stream_ptr(stream)))
+    dev = x.device
+    q, qp = _out(q, (K, N), torch.int8, dev, "q")
+    scale, sp = _out(scale, (N,), torch.float32, dev, "scale")
+    with torch.cuda.device(dev):
+        _check(lib().vlut_quantize_amax(_arg(x, "x", torch.float32, device=dev),
+                                        _arg(amax, "amax", torch.int32, (N,), dev),
+                                        K, N, qp, sp, _stream_ptr(stream, dev)))
     return q, scale
 
 
@@ -558,17 +683,19 @@ def mpgemm_scalar_lut(W: PackedWeights, A, a_scale, w_scale: float, out=None,
     """The scalar-LUT (1->1, one table per token) mpGeMM on the K2 kernel
     (P:84-85); with use_ws the K range is split across CTAs."""
     import torch
-    K, N = A.shape
+    K, N, dev = _act(A)
     M = W.M
-    if out is None:
-        out = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    st = _stream(stream, dev)
+    out, op = _out(out, (M, N), torch.float32, dev)
     if ws is None and use_ws:
-        ws = workspace(A.device)
-    wsp, wsn = (_dev_ptr(ws), ws.numel()) if ws is not None else (ctypes.c_void_p(0), 0)
+        ws = workspace(dev, st)
+    wsp, wsn = _ws_arg(ws, dev)
     keep, pp = _plan_ptr(plan)
-    _check(lib().vlut_mpgemm_scalar_lut(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(a_scale),
-                                        float(w_scale), _dev_ptr(out), M, K, N, pp, wsp, wsn,
-                                        _stream_ptr(stream)))
+    with torch.cuda.device(dev):
+        _check(lib().vlut_mpgemm_scalar_lut(_weights(W, K, dev), _dev_ptr(A),
+                                            _arg(a_scale, "a_scale", torch.float32, (N,), dev),
+                                            float(w_scale), op, M, K, N, pp, wsp, wsn,
+                                            ctypes.c_void_p(st.cuda_stream)))
     return out
 
 
@@ -579,12 +706,20 @@ def mpgemm_allgather(W: PackedWeights, A, a_scale, w_scale: float, out_full, row
     raw device address, e.g. a multicast address), stored there and to every
     peer buffer in ``peer_ptrs`` (device pointers mapped into this process)
     by the K1 epilogue.  Returns out_full."""
-    K, N = A.shape
+    import torch
+    K, N, dev = _act(A)
     arr = (ctypes.c_void_p * max(1, len(peer_ptrs)))(*[ctypes.c_void_p(int(x)) for x in peer_ptrs])
     # out_full: a tensor, or a raw device address (e.g. a multicast address)
-    out_p = ctypes.c_void_p(int(out_full)) if isinstance(out_full, int) else _dev_ptr(out_full)
-    _check(lib().vlut_mpgemm_allgather(ctypes.byref(W.desc), _dev_ptr(A), _dev_ptr(a_scale),
-                                       float(w_scale), out_p, W.M, K, N, int(row0),
-                                       ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p)),
-                                       len(peer_ptrs), _stream_ptr(stream)))
+    if isinstance(out_full, int):
+        out_p = ctypes.c_void_p(int(out_full))
+    else:
+        if out_full.dim() != 2 or out_full.shape[1] != N or out_full.shape[0] < row0 + W.M:
+            raise ValueError("out_full: expected fp32 [>= row0 + M][N]")
+        out_p = _arg(out_full, "out_full", torch.float32, device=dev)
+    with torch.cuda.device(dev):
+        _check(lib().vlut_mpgemm_allgather(_weights(W, K, dev), _dev_ptr(A),
+                                           _arg(a_scale, "a_scale", torch.float32, (N,), dev),
+                                           float(w_scale), out_p, W.M, K, N, int(row0),
+                                           ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p)),
+                                           len(peer_ptrs), _stream_ptr(stream, dev)))
     return out_full

@@ -224,7 +224,7 @@ inline bool valid_split(int warps, int S) { return warps > 0 && S >= 1 && S <= 8
 
 // Workspace layout (caller-provided, zeroed once):
 //   [0, SK)             stream-K int32 partials [sms][768 x 64] (m_cta <= 768)
-//   [SK, SK + 4096)     stream-K epoch flags
+//   [SK, SK + 4096)     stream-K partial-ready flags (0 between launches)
 //   [.., + 64 KB)       K2 split-K arrival counters (kept zero between launches)
 //   [.., + 16 MB)       K2 split-K int32 accumulators [M][N] (kept zero)
 size_t sk_part_bytes(int sms) { return (size_t)sms * 768 * 64 * 4; }  // max m_cta 768
@@ -496,11 +496,16 @@ vlut_status launch_sk(const vlut::Params& p, const vlut::SkParams& sk, int grid,
   cfg.blockDim = dim3(L::THREADS, 1, 1);
   cfg.dynamicSmemBytes = L::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  // owners spin on their producers' flags: every CTA must be co-resident
+  // (grid <= #SMs, one CTA per SM), which a cooperative launch guarantees
+  // whatever else holds SMs (NCCL kernels, other streams)
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   VLUT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p, sk));
   return VLUT_OK;
 }
@@ -711,16 +716,13 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
   if (NT > 65535 || MT > 65535) return fail(VLUT_ERR_SHAPE, "grid too large");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (plan.streamk) {
-    static std::atomic<unsigned> epoch{0};
     vlut::SkParams sk;
     sk.NT = (int)NT;
     sk.MT = (int)MT;
     sk.U = MT * NT * (long long)W->kg_tiles;
     sk.ws = static_cast<int32_t*>(ws);
     sk.flags = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + sk_part_bytes(d.sms));
-    unsigned e = ++epoch;
-    if (e == 0) e = ++epoch;
-    sk.epoch = e;
+    sk.epoch = 1u;  // flags are reset by their consumers: graph-replay safe
     const int grid = (int)(sk.U < d.sms ? sk.U : d.sms);
     st = acc_only ? dispatch_sk<true>(W->g, plan.warps, rpt, p, sk, grid, s)
                   : dispatch_sk<false>(W->g, plan.warps, rpt, p, sk, grid, s);
@@ -735,45 +737,85 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
 
 }  // namespace
 
-// Library-owned workspaces of vlut_mpgemm, one per (device, stream): calls on
-// one stream are ordered, so they may share it; allocated with cudaMalloc and
-// zeroed (stream-ordered) on first use, kept for the life of the process.
-bool internal_workspace(void* stream, void** ws, size_t* bytes) {
-  static std::mutex mu;
-  static std::vector<std::tuple<int, void*, void*, size_t>> cache;  // (device, stream, ptr, bytes)
+// Library-owned workspaces of vlut_mpgemm (the north-star signature has no
+// workspace argument).  At most kWsCap per device, each bound to one stream
+// by its process-unique id (cudaStreamGetId: ids are never reused, so a
+// recycled stream handle cannot alias a workspace with work still in flight,
+// and cudaStreamPerThread / the legacy stream resolve to their own streams).
+// Calls on one stream are ordered, so they share that stream's workspace.  A
+// new stream beyond the cap takes the least recently used entry after a
+// device-wide synchronisation (its previous stream may still be using it) and
+// re-zeroes it on the new stream.  g_ws_mu is held from the lookup through
+// the launch, so an eviction can never rebind a workspace between the lookup
+// and the launch that uses it.  Never allocates or evicts inside a stream
+// capture: the call then runs without a workspace (cluster schedules only).
+struct WsEntry {
+  int dev;
+  unsigned long long sid;
+  void* ptr;
+  size_t bytes;
+  unsigned long long last;
+};
+constexpr int kWsCap = 4;
+std::mutex g_ws_mu;
+std::vector<WsEntry> g_ws;
+unsigned long long g_ws_tick = 0;
+
+bool internal_workspace_locked(void* stream, void** ws, size_t* bytes) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return false;
   DeviceInfo d;
   if (device_info(&d) != VLUT_OK) return false;
-  std::lock_guard<std::mutex> lk(mu);
-  for (auto& e : cache)
-    if (std::get<0>(e) == dev && std::get<1>(e) == stream) {
-      *ws = std::get<2>(e);
-      *bytes = std::get<3>(e);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return false;
+  }
+  unsigned long long sid = 0;
+  if (cudaStreamGetId(st, &sid) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  int n_dev = 0;
+  WsEntry* lru = nullptr;
+  for (auto& e : g_ws) {
+    if (e.dev != dev) continue;
+    if (e.sid == sid) {
+      e.last = ++g_ws_tick;
+      *ws = e.ptr;
+      *bytes = e.bytes;
       return true;
     }
-  // never allocate inside a stream capture (cudaMalloc would invalidate it):
-  // the call then runs without a workspace (cluster schedules only)
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(static_cast<cudaStream_t>(stream), &cap) != cudaSuccess ||
-      cap != cudaStreamCaptureStatusNone) {
-    cudaGetLastError();
-    return false;
+    ++n_dev;
+    if (!lru || e.last < lru->last) lru = &e;
   }
   const size_t need = sk_workspace_bytes(d.sms);
-  void* p = nullptr;
-  if (cudaMalloc(&p, need) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
+  WsEntry* slot = nullptr;
+  if (n_dev >= kWsCap && lru) {
+    // the LRU entry's stream may still run work that uses it
+    if (cudaDeviceSynchronize() != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    slot = lru;
+  } else {
+    void* p = nullptr;
+    if (cudaMalloc(&p, need) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    g_ws.push_back({dev, 0ull, p, need, 0ull});
+    slot = &g_ws.back();
   }
-  if (cudaMemsetAsync(p, 0, need, static_cast<cudaStream_t>(stream)) != cudaSuccess) {
+  if (cudaMemsetAsync(slot->ptr, 0, slot->bytes, st) != cudaSuccess) {
     cudaGetLastError();
-    cudaFree(p);
-    return false;
+    return false;  // the entry stays cached (still unbound to this stream)
   }
-  cache.emplace_back(dev, stream, p, need);
-  *ws = p;
-  *bytes = need;
+  slot->sid = sid;
+  slot->last = ++g_ws_tick;
+  *ws = slot->ptr;
+  *bytes = slot->bytes;
   return true;
 }
 
@@ -893,6 +935,20 @@ vlut_status vlut_pack_weights_device_ex(const int8_t* w_dev, int M, int K, int g
   vlut::vlut_pack_kernel<<<(unsigned)blocks, threads, 0, s>>>(
       w_dev, M, K, g, mp, kgt, static_cast<uint8_t*>(payload_dev));
   VLUT_CUDA_TRY(cudaGetLastError());
+  // The mpGeMM kernels stage weight tiles BEFORE griddepcontrol.wait (the
+  // payload is not an output of the previous kernel -- see vlut.h).  An
+  // event record after the packing kernel makes the next launch on this
+  // stream an ordinary (not programmatic) dependent: it starts only after
+  // the packing kernel has completed and its stores are visible.
+  {
+    static std::mutex mu;
+    static cudaEvent_t ev[64] = {};
+    int dev = 0;
+    VLUT_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (!ev[dev & 63]) VLUT_CUDA_TRY(cudaEventCreateWithFlags(&ev[dev & 63], cudaEventDisableTiming));
+    VLUT_CUDA_TRY(cudaEventRecord(ev[dev & 63], s));
+  }
   *desc_out = d;
   return ok();
 }
@@ -944,9 +1000,36 @@ vlut_status vlut_mpgemm(const vlut_packed_weights* W, const int8_t* A, const flo
   // is available; without one, only the cluster schedules
   void* ws = nullptr;
   size_t ws_bytes = 0;
-  if (M > 0 && N > 0) internal_workspace(stream, &ws, &ws_bytes);
+  std::lock_guard<std::mutex> lk(g_ws_mu);  // held through the launch (see above)
+  if (M > 0 && N > 0) internal_workspace_locked(stream, &ws, &ws_bytes);
   return run_mpgemm(W, A, a_scale, w_scale, out, M, K, N, nullptr, stream, false, nullptr, 0, ws,
                     ws_bytes);
+}
+
+int vlut_cached_workspaces(void) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  return (int)g_ws.size();
+}
+
+vlut_status vlut_release_workspaces(void) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  int cur = 0;
+  VLUT_CUDA_TRY(cudaGetDevice(&cur));
+  vlut_status st = VLUT_OK;
+  while (!g_ws.empty()) {
+    WsEntry e = g_ws.back();
+    cudaError_t err = cudaSetDevice(e.dev);
+    if (err == cudaSuccess) err = cudaDeviceSynchronize();  // its stream may still use it
+    if (err == cudaSuccess) err = cudaFree(e.ptr);
+    if (err != cudaSuccess) {
+      st = fail(VLUT_ERR_CUDA, "releasing a workspace on device %d: %s", e.dev,
+                cudaGetErrorString(err));
+      break;
+    }
+    g_ws.pop_back();
+  }
+  cudaSetDevice(cur);
+  return st == VLUT_OK ? ok() : st;
 }
 
 vlut_status vlut_mpgemm_ex(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,

@@ -10,9 +10,15 @@
 //   * full      [0, KT)        -> epilogue straight from TMEM
 //   * producer  [ka, kb < KT)  -> the tile continues in the next CTA(s): the
 //                                 int32 partial goes to workspace slot c, then
-//                                 flags[c] = epoch (release)
+//                                 flags[c] = 1 (release)
 //   * owner     [ka > 0, KT)   -> waits (acquire) for the producers of the
-//                                 tile's head, adds their partials, epilogue
+//                                 tile's head, resets their flags to 0, adds
+//                                 their partials, epilogue
+// Every producer has exactly one owner, so every flag a launch sets is reset
+// by the same launch: all flags are 0 between launches and the handshake
+// needs no host-side state -- a captured CUDA graph can be replayed (the
+// next launch's producers store only after its griddepcontrol.wait, i.e.
+// after this launch's resets are performed).
 // Execution order inside a CTA: middle full tiles, its last segment, its
 // first segment -- producers never wait, owners wait last, so the dependency
 // graph is acyclic and all G <= #SMs CTAs are co-resident: no deadlock.
@@ -29,8 +35,8 @@ struct SkParams {
   int NT, MT;           // N-tiles, M-tiles
   long long U;          // units = NT * MT * KT
   int32_t* ws;          // [G][MCTA * 64] int32 partials
-  unsigned* flags;      // [G] epoch stamps
-  unsigned epoch;       // unique per launch (never 0)
+  unsigned* flags;      // [G] partial-ready flags: 0 between launches
+  unsigned epoch;       // the 'ready' value (1)
 };
 
 struct SkSeg {
@@ -86,6 +92,9 @@ struct SkIter {
 
 __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   unsigned v;
@@ -159,6 +168,9 @@ __device__ __forceinline__ void sk_epilogue(const Params& p, const SkParams& sk,
             __nanosleep(64);
             if (++spins > (1u << 26)) __trap();
           }
+          // consumed: back to 0 for the next launch (this launch sets it
+          // only once, so no later store can race with the reset)
+          st_relaxed_gpu(sk.flags + c2, 0u);
         }
       }
       bar_sync(6, NLT);

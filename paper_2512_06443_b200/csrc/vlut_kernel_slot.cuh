@@ -71,7 +71,12 @@ constexpr int kFlushTiles = 3;                    // TPW = 2: widen every 48 gro
 constexpr int kMaxCounters = 8192;                // split-K tiles (2 counters each) in the workspace
 constexpr int kActNMax = 64;                      // activations staged by TMA when N <= 64
 constexpr int kMaxStages = 8;                     // staging ring depth (bytes in flight at N = 1)
-constexpr int kRampStages = 2;                    // stages issued before the first tile lands
+#ifndef VLUT_SLOT_RAMP
+#define VLUT_SLOT_RAMP 0
+#endif
+// stages issued before the first tile lands (0: no gate, every ring stage's
+// index rows are requested up front, before griddepcontrol.wait)
+constexpr int kRampStages = VLUT_SLOT_RAMP;
 constexpr int kLastOnlyBytes = 8192;              // split-K tiles up to this size: the last CTA finishes them
 
 template <int G, int NW, int TPW>
@@ -309,20 +314,44 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
     // =========================== producer: index + activation tiles -> ring (a2)
     if (lane == 0 && ntiles > 0) {
       const int rows = min(L::MCTA, p.m_pad - m0);
+      // (1) the packed weights are not an output of the previous kernel
+      // (vlut.h): the index rows of the first ring-full of tiles are
+      // requested before griddepcontrol.wait, so at decode (HBM-bound) the
+      // weight stream overlaps the previous kernel's tail
+      const int pre = min(ntiles, kRampStages > 0 ? min(kRampStages, L::STAGES) : L::STAGES);
 #pragma unroll 1
-      for (int t = 0; t < ntiles; ++t) {
+      for (int t = 0; t < pre; ++t) {
+        const int kt = kt0 + t;
+        const int ab = p.act_tma ? act_tile_bytes(p, kt, G) : 0;
+        const uint32_t stg = mbar + 32 + 8 * t;
+        mbar_expect_tx(stg, (uint32_t)(rows * 16 + ab));
+        bulk_g2s(idx_s + (uint32_t)(t * L::IDX_BYTES), p.payload + ((size_t)kt * p.m_pad + m0) * 16,
+                 (uint32_t)(rows * 16), stg);
+      }
+      // (2) activations come from the previous kernel (quantizer)
+      pdl_wait();
+#pragma unroll 1
+      for (int t = 0; t < pre; ++t) {
+        const int kt = kt0 + t;
+        const int ab = p.act_tma ? act_tile_bytes(p, kt, G) : 0;
+        if (ab > 0)
+          bulk_g2s(act_s + (uint32_t)(t * L::ACT_BYTES), p.A + (size_t)kt * kKgTile * G * p.N,
+                   (uint32_t)ab, mbar + 32 + 8 * t);
+      }
+      // (3) the rest through the ring as stages free up
+#pragma unroll 1
+      for (int t = pre; t < ntiles; ++t) {
         const int st = t % L::STAGES, use = t / L::STAGES;
         const int kt = kt0 + t;
         if (use > 0) mbar_wait(mbar + IFREE0 + 8 * st, (use - 1) & 1);
-        // ramp: all CTAs start their streams together, so the first tile
-        // lands sooner when only two stages per CTA are in flight until it does
-        if (t == kRampStages) mbar_wait(mbar + 32, 0);
+        // ramp (kRampStages > 0): only that many stages per CTA in flight
+        // until the first tile lands
+        if (kRampStages > 0 && t == kRampStages) mbar_wait(mbar + 32, 0);
         const int ab = p.act_tma ? act_tile_bytes(p, kt, G) : 0;
         const uint32_t stg = mbar + 32 + 8 * st;
         mbar_expect_tx(stg, (uint32_t)(rows * 16 + ab));
         bulk_g2s(idx_s + (uint32_t)(st * L::IDX_BYTES), p.payload + ((size_t)kt * p.m_pad + m0) * 16,
                  (uint32_t)(rows * 16), stg);
-        if (t == 0) pdl_wait();  // A is produced by the previous kernel (quantizer)
         if (ab > 0)
           bulk_g2s(act_s + (uint32_t)(st * L::ACT_BYTES), p.A + (size_t)kt * kKgTile * G * p.N,
                    (uint32_t)ab, stg);

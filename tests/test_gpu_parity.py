@@ -258,27 +258,110 @@ def test_config3_linears_sampled(v, j):
 
 
 # ------------------------------------------------------------------ config 5 chain (a7 + a2-a6)
-def test_config5_chain_two_layers_sampled_tokens(v):
-    """Full BitNet-2B-shaped layer weights, N = 2048 tokens on the GPU; the
-    oracle re-runs the chain on sampled token columns (per-token quantization
-    makes columns independent) -- codes and scales bit-exact after each layer."""
+def test_config5_chain_30_layers_sampled_tokens(v):
+    """BASELINE.md's parity bar for config 5: bit-exact int8 re-quantization
+    along the whole 30-layer chain.  Full BitNet-2B-shaped layer weights and
+    N = 2048 tokens on the GPU, through BOTH the plain chain (LayerChain) and
+    the fused re-quantization chain (LayerChain(fused=True), f1); the oracle
+    re-runs the chain (oracle.config5_layer, reading c14) on 16 sampled token
+    columns -- per-token quantization makes columns independent -- and codes
+    and scales must be bit-identical after every one of the 30 layers.
+    Layers are built one at a time (weights generated, packed, checked, freed)."""
     from paper_2512_06443_b200.sharded import LayerChain, RowShardedLinear
     cfg = synth.CONFIGS[5]
-    N, n_layers = 2048, 2
-    layers_w = [[w for _, w in synth.config_weights(cfg, l)] for l in range(n_layers)]
-    layers = [[RowShardedLinear(w, 4, synth.W_SCALE, device=dev()) for w in lw]
-              for lw in layers_w]
-    chain = LayerChain(layers)
+    N, n_layers = 2048, cfg.layers
+    assert n_layers == 30
     x = synth.activations_f32(2560, N, synth.act_seed(cfg, N))
     xq, xs = v.quantize(to_dev(x))
+    fq, fs = xq, xs
     cols = np.unique(np.concatenate([[0, N - 1], synth.rng(5).integers(0, N, size=14)]))
     q_ref, s_ref = oracle.quantize(np.ascontiguousarray(x[:, cols]))
     for l in range(n_layers):
-        xq, xs = chain.layer(l, xq, xs)
-        q_ref, s_ref = oracle.config5_layer(layers_w[l], synth.W_SCALE, q_ref, s_ref, q_rows=2560)
+        lw = [w for _, w in synth.config_weights(cfg, l)]
+        lay = [RowShardedLinear(w, 4, synth.W_SCALE, device=dev(), device_pack=True) for w in lw]
+        xq, xs = LayerChain([lay]).layer(0, xq, xs)
+        fq, fs = LayerChain([lay], fused=True).layer(0, fq, fs)
+        q_ref, s_ref = oracle.config5_layer(lw, synth.W_SCALE, q_ref, s_ref, q_rows=2560)
         torch.cuda.synchronize()
-        assert np.array_equal(xs.cpu().numpy()[cols], s_ref)
-        assert np.array_equal(xq.cpu().numpy()[:, cols], q_ref)
+        assert np.array_equal(xs.cpu().numpy()[cols].view(np.int32), s_ref.view(np.int32)), l
+        assert np.array_equal(xq.cpu().numpy()[:, cols], q_ref), l
+        assert np.array_equal(fs.cpu().numpy()[cols].view(np.int32), s_ref.view(np.int32)), l
+        assert np.array_equal(fq.cpu().numpy()[:, cols], q_ref), l
+        # the two chains agree on every token, not only the sampled ones
+        assert torch.equal(xq, fq) and torch.equal(xs.view(torch.int32), fs.view(torch.int32)), l
+        del lay, lw
+
+
+def test_bench_workload_full_matrix_exact_plan(v):
+    """The launch bench.py times (BASELINE.json configs[1], 6912 x 2560,
+    N = 256, g = 4, P(0) = 0.4 weights; the plan vlut_plan_ws picks, plain
+    epilogue, the library-chosen schedule of vlut_mpgemm too), checked on the
+    WHOLE 6912 x 256 output against the oracle: int32 accumulators bit-exact
+    and fp32 outputs bit-identical to the fixed-order fp32 dequant (and within
+    1e-6 of fp64)."""
+    cfg = synth.CONFIGS[2]
+    lin = cfg.linears[0]
+    M, K, N, g = lin.M, lin.K, cfg.N[0], cfg.g[0]
+    W = synth.ternary_weights(M, K, synth.weight_seed(cfg, 0, 0), cfg.p_zero)
+    x = synth.activations_f32(K, N, synth.act_seed(cfg, N))
+    xd = to_dev(x)
+    q, s = v.quantize(xd)
+    pw = v.pack_weights_device(to_dev(W), g)
+    plan = v.plan_ws(M, K, N, g)
+    out = v.mpgemm_ws(pw, q, s, synth.W_SCALE, plan=plan, ws=v.workspace(dev()))
+    out_ns = v.mpgemm(pw, q, s, synth.W_SCALE)
+    acc = v.mpgemm_acc_ws(pw, q, plan=plan, ws=v.workspace(dev()))
+    torch.cuda.synchronize()
+    q_ref, s_ref = oracle.quantize(x)
+    assert np.array_equal(q.cpu().numpy(), q_ref)
+    assert np.array_equal(s.cpu().numpy().view(np.int32), s_ref.view(np.int32))
+    acc_ref = oracle.gemm_i32(W, q_ref)
+    assert np.array_equal(acc.cpu().numpy(), acc_ref)
+    check_fp32(out.cpu().numpy(), acc_ref, s_ref, synth.W_SCALE)
+    check_fp32(out_ns.cpu().numpy(), acc_ref, s_ref, synth.W_SCALE)
+
+
+def test_parity_harness_detects_single_trit_corruption(v):
+    """an injected single-trit corruption in the payload must be
+    reported.  One payload byte of a real (row, group) is changed ON THE
+    DEVICE to another valid index (one trit flipped); the oracle comparison
+    must then fail exactly on that output row, and restoring the byte must
+    make it pass again.  Proves the parity checks above can fail."""
+    M, K, N, g = 300, 640, 96, 4
+    W = synth.ternary_weights(M, K, seed=481)
+    x = synth.activations_f32(K, N, seed=482)
+    q, s = oracle.quantize(x)
+    qd, sd = to_dev(q), to_dev(s)
+    pw = v.pack_weights(W, g, device=dev())
+    ref = oracle.dequant_f32(oracle.gemm_i32(W, q), s, synth.W_SCALE)
+    ok = v.mpgemm(pw, qd, sd, synth.W_SCALE)
+    torch.cuda.synchronize()
+    assert np.array_equal(ok.cpu().numpy().view(np.int32), ref.view(np.int32))
+    m, k = 123, 37                       # row 123, group 37 (features 148..151)
+    kt, j = divmod(k, 16)
+    off = (kt * pw.desc.m_pad + m) * 16 + j
+    old = int(pw.payload[off].item())
+    assert old == oracle.pack_group(W[m, k * g:(k + 1) * g])
+    trits = oracle.unpack_index(old, g).copy()
+    trits[0] = 1 if trits[0] != 1 else -1     # flip one trit
+    pw.payload[off] = oracle.pack_group(trits)
+    # vlut.h: the payload must not be written by the kernel launched just
+    # before the mpGeMM (weights are staged before griddepcontrol.wait)
+    torch.cuda.synchronize()
+    bad = v.mpgemm(pw, qd, sd, synth.W_SCALE)
+    torch.cuda.synchronize()
+    diff_rows = np.unique(np.nonzero(bad.cpu().numpy().view(np.int32) != ref.view(np.int32))[0])
+    assert diff_rows.tolist() == [m]     # reported, and only where corrupted
+    pw.payload[off] = old
+    torch.cuda.synchronize()
+    again = v.mpgemm(pw, qd, sd, synth.W_SCALE)
+    torch.cuda.synchronize()
+    assert np.array_equal(again.cpu().numpy().view(np.int32), ref.view(np.int32))
+    # a byte outside [0, 3^g) is a corrupt payload for the host unpacker (S:164)
+    pw.payload[off] = 81
+    with pytest.raises(v.VlutError) as e:
+        v.unpack_weights_host(pw)
+    assert e.value.name == "VLUT_ERR_INVALID_TRIT"
 
 
 # ------------------------------------------------------------------ mixed g=5/g=4 schedule (f2)
@@ -401,20 +484,6 @@ def test_mpgemm_fused_mul_and_amax(v, M, K, N, rows, how):
     qr, sr = oracle.quantize(np.ascontiguousarray(ref[:rows]))
     torch.cuda.synchronize()
     assert np.array_equal(ss.cpu().numpy(), sr) and np.array_equal(qq.cpu().numpy(), qr)
-
-
-def test_config5_chain_fused_equals_unfused(v):
-    from paper_2512_06443_b200.sharded import LayerChain, RowShardedLinear
-    cfg = synth.CONFIGS[5]
-    N, n_layers = 2048, 2
-    layers = [[RowShardedLinear(w, 4, synth.W_SCALE, device=dev(), device_pack=True)
-               for _, w in synth.config_weights(cfg, l)] for l in range(n_layers)]
-    x = synth.activations_f32(2560, N, synth.act_seed(cfg, N))
-    xq, xs = v.quantize(to_dev(x))
-    a_q, a_s = LayerChain(layers)(xq, xs)
-    b_q, b_s = LayerChain(layers, fused=True)(xq, xs)
-    torch.cuda.synchronize()
-    assert torch.equal(a_q, b_q) and torch.equal(a_s.view(torch.int32), b_s.view(torch.int32))
 
 
 # ------------------------------------------------------------------ host pipeline (e2e path)
