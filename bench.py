@@ -711,6 +711,23 @@ def chain_bench(v, dev, world, rank, args, reps=3, peer=None):
         torch.cuda.synchronize()
         tf.append(a.elapsed_time(b))
     t_f = float(np.median(tf))
+    # f1 overlapped with compute: 4 token chunks; each linear's per-chunk
+    # MAX all-reduce + quantize + int8 all-gather on a side stream while the
+    # next chunk computes
+    kchain = LayerChain(layers, fused=True, chunks=4)
+    kchain(xq, xs)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    tk = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        kchain(xq, xs)
+        b.record()
+        torch.cuda.synchronize()
+        tk.append(a.elapsed_time(b))
+    t_k = float(np.median(tk))
     # N > 1: every linear's all-gather fused into its K1 epilogue (peer stores)
     t_p = float("nan")
     if world > 1 and peer is not None:
@@ -733,9 +750,9 @@ def chain_bench(v, dev, world, rank, args, reps=3, peer=None):
             for lin in lay:
                 lin.peers = None
     if world > 1:
-        tt = torch.tensor([t, t_f, t_p], device=dev)
+        tt = torch.tensor([t, t_f, t_p, t_k], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t, t_f, t_p = float(tt[0]), float(tt[1]), float(tt[2])
+        t, t_f, t_p, t_k = float(tt[0]), float(tt[1]), float(tt[2]), float(tt[3])
     lookups = L * N * sum(lin.M * lin.K // 4 for lin in cfg.linears)
     R_LU = SM_COUNT * 64 * SM_MAX_MHZ_FALLBACK * 1e6
     return {"config": 5, "layers": L, "N": N, "n_gpus": world, "ms_per_forward": t,
@@ -743,6 +760,10 @@ def chain_bench(v, dev, world, rank, args, reps=3, peer=None):
             "frac_smem_roofline": lookups / (R_LU * world) / (t * 1e-3),
             "fused_requant": {"ms_per_forward": t_f, "tokens_s": N / (t_f * 1e-3),
                               "frac_smem_roofline": lookups / (R_LU * world) / (t_f * 1e-3)},
+            "fused_requant_overlapped": {"ms_per_forward": t_k, "tokens_s": N / (t_k * 1e-3),
+                                         "chunks": 4,
+                                         "frac_smem_roofline": lookups / (R_LU * world)
+                                         / (t_k * 1e-3)},
             "fused_allgather": ({"ms_per_forward": t_p, "tokens_s": N / (t_p * 1e-3),
                                  "frac_smem_roofline": lookups / (R_LU * world) / (t_p * 1e-3)}
                                 if t_p == t_p else None),

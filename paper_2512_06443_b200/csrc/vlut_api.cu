@@ -1,7 +1,9 @@
 // vlut_api.cu -- host side of libvlut.so: argument validation, the weight
 // packer (a1), the launch planner and the launches.  See include/vlut.h for
 // the contract of every entry point.
+#include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -1270,6 +1272,40 @@ vlut_status vlut_quantize(const float* x, const float* y, int K, int N, int8_t* 
   if (K == 0 || N == 0) return ok();
   if (!x || !q || !scale) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // decode shapes (N in {1,2,4,8,16}, flat float4 access possible, fits the
+  // register cache of one cluster): K3f, one cluster over the flat array
+  {
+    const long long total4 = (long long)K * N / 4;
+    const bool pow2n = N == 1 || N == 2 || N == 4 || N == 8 || N == 16;
+    const bool flat_ok = pow2n && ((long long)K * N) % 4 == 0 &&
+                         ((((uintptr_t)x) | ((uintptr_t)(y ? y : x))) & 15) == 0 &&
+                         (((uintptr_t)q) & 3) == 0 &&
+                         total4 <= (long long)vlut::kQfMaxCL * vlut::kQfThreads * vlut::kQfCache;
+    if (flat_ok && !getenv("VLUT_NO_QFLAT")) {
+      // CTAs: ~2 float4 per thread in flight, at most one cluster of 8
+      long long CLl = (total4 + 2LL * vlut::kQfThreads - 1) / (2LL * vlut::kQfThreads);
+      while (CLl < vlut::kQfMaxCL && total4 > CLl * vlut::kQfThreads * vlut::kQfCache) ++CLl;
+      const int CLf = (int)std::max(1LL, std::min<long long>(vlut::kQfMaxCL, CLl));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)CLf, 1, 1);
+      cfg.blockDim = dim3(vlut::kQfThreads, 1, 1);
+      cfg.stream = s;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = (unsigned)CLf;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 2;
+      if (y)
+        VLUT_CUDA_TRY(cudaLaunchKernelEx(&cfg, vlut::vlut_quantize_flat_kernel<true>, x, y, K, N, q, scale));
+      else
+        VLUT_CUDA_TRY(cudaLaunchKernelEx(&cfg, vlut::vlut_quantize_flat_kernel<false>, x, y, K, N, q, scale));
+      return ok();
+    }
+  }
   // cluster size along K: enough CTAs that every row fits the register cache
   // when possible (<= 8, portable), and >= ~2 waves of CTAs over the GPU.
   const long long tok_blocks = (N + vlut::kQTok - 1) / vlut::kQTok;

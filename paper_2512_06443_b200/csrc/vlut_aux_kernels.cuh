@@ -185,6 +185,110 @@ __global__ void __launch_bounds__(kQThreads)
   VLUT_STAMP(6);
 }
 
+// ---------------------------------------------------------------- K3f: small-N (decode) quantizer
+// K3 gives each cluster 16 tokens and each thread 4 tokens of a row: at
+// decode (N = 1) three quarters of its threads idle and one cluster of 8
+// CTAs walks K rows in many serial passes (K = 23040: ~15 us).  K3f treats
+// [K][N] fp32 (token axis contiguous) as ONE flat array of K*N/4 float4s:
+// lane i of the float4 at flat element e = 4f + i is token e mod N; every
+// thread strides by a multiple of N/4 float4s, so its four lanes keep fixed
+// tokens (4 tid + i) mod N (N in {1, 2, 4, 8, 16}).  One cluster of CL CTAs
+// splits the flat array, every load is issued before any use (one DRAM round
+// trip), maxima are reduced warp -> CTA (shared atomicMax on float bits:
+// |x| >= 0 orders like unsigned) -> cluster (DSMEM push, as K3), and codes
+// are written from registers: int8 [K][N] has the same flat order, so four
+// codes are one 4-byte store.  Same IEEE ops as K3: identical codes/scales.
+constexpr int kQfThreads = 512;
+constexpr int kQfCache = 8;  // float4 per thread: <= 8 CTAs x 512 x 8 x 16 B = 512 KiB of x
+constexpr int kQfMaxCL = 8;
+
+template <bool HAS_Y>
+__global__ void __launch_bounds__(kQfThreads)
+    vlut_quantize_flat_kernel(const float* __restrict__ x, const float* __restrict__ y, int K,
+                              int N, int8_t* __restrict__ q, float* __restrict__ scale) {
+  __shared__ unsigned red[16];
+  __shared__ float all_max[kQfMaxCL][16];  // [cluster rank][token]
+  __shared__ float s_scale[16];
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CL = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31;
+  const long long total4 = (long long)K * N / 4;
+  // CTA slice [f0, f1) of float4s, f0 a multiple of kQfThreads (a multiple
+  // of N/4), so a thread's token pattern does not depend on its CTA
+  const long long per =
+      ((total4 + CL - 1) / CL + kQfThreads - 1) / kQfThreads * kQfThreads;
+  const long long f0 = (long long)rank * per;
+  const long long f1 = min(total4, f0 + per);
+  if (tid < 16) red[tid] = 0u;
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  float4 c[kQfCache];
+#pragma unroll
+  for (int j = 0; j < kQfCache; ++j) {
+    const long long f = f0 + tid + (long long)j * kQfThreads;
+    c[j] = (f < f1) ? __ldg(x4 + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if constexpr (HAS_Y) {
+    const float4* y4 = reinterpret_cast<const float4*>(y);
+    float4 yc[kQfCache];
+#pragma unroll
+    for (int j = 0; j < kQfCache; ++j) {
+      const long long f = f0 + tid + (long long)j * kQfThreads;
+      yc[j] = (f < f1) ? __ldg(y4 + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < kQfCache; ++j) c[j] = fmul4(c[j], yc[j]);
+  }
+  float m[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int j = 0; j < kQfCache; ++j) {
+    m[0] = fmaxf(m[0], fabsf(c[j].x)); m[1] = fmaxf(m[1], fabsf(c[j].y));
+    m[2] = fmaxf(m[2], fabsf(c[j].z)); m[3] = fmaxf(m[3], fabsf(c[j].w));
+  }
+  // lanes l and l ^ d (d >= N/4) hold the same tokens
+  const int pat = N >= 4 ? N / 4 : 1;  // distinct lane patterns
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    for (int d = pat; d < 32; d <<= 1) m[i] = fmaxf(m[i], __shfl_xor_sync(0xffffffffu, m[i], d));
+  __syncthreads();  // red[] initialised
+  if (lane < pat) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) atomicMax(red + (4 * lane + i) % N, __float_as_uint(m[i]));
+  }
+  __syncthreads();
+  if (tid < N) {
+    const float a = __uint_as_float(red[tid]);
+    for (int r = 0; r < CL; ++r) cluster.map_shared_rank(&all_max[0][0], r)[rank * 16 + tid] = a;
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  if (tid < N) {
+    float a = 0.f;
+    for (int r = 0; r < CL; ++r) a = fmaxf(a, all_max[r][tid]);
+    const float sc = (a == 0.f) ? 1.f : __fdiv_rn(a, 127.f);
+    s_scale[tid] = sc;
+    if (rank == 0) scale[tid] = sc;
+  }
+  __syncthreads();
+  float s[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) s[i] = s_scale[(4 * tid + i) % N];
+#pragma unroll
+  for (int j = 0; j < kQfCache; ++j) {
+    const long long f = f0 + tid + (long long)j * kQfThreads;
+    if (f < f1) {
+      const uint32_t packed = (uint32_t)(uint8_t)q_code(c[j].x, s[0]) |
+                              ((uint32_t)(uint8_t)q_code(c[j].y, s[1]) << 8) |
+                              ((uint32_t)(uint8_t)q_code(c[j].z, s[2]) << 16) |
+                              ((uint32_t)(uint8_t)q_code(c[j].w, s[3]) << 24);
+      reinterpret_cast<uint32_t*>(q)[f] = packed;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- K3t: fused transposition (f3)
 // Feature-major input (frameworks hold activations [N][K]; the
 // transposition to the token-contiguous [K][N] int8 layout is fused into the

@@ -72,11 +72,28 @@ constexpr int kMaxCounters = 8192;                // split-K tiles (2 counters e
 constexpr int kActNMax = 64;                      // activations staged by TMA when N <= 64
 constexpr int kMaxStages = 8;                     // staging ring depth (bytes in flight at N = 1)
 #ifndef VLUT_SLOT_RAMP
-#define VLUT_SLOT_RAMP 0
+#define VLUT_SLOT_RAMP 2
 #endif
 // stages issued before the first tile lands (0: no gate, every ring stage's
 // index rows are requested up front, before griddepcontrol.wait)
 constexpr int kRampStages = VLUT_SLOT_RAMP;
+#ifndef VLUT_SLOT_PIECES
+#define VLUT_SLOT_PIECES 1
+#endif
+constexpr int kIdxPieces = VLUT_SLOT_PIECES;  // bulk copies per staged index tile
+
+// The index rows of one K-tile (one contiguous block of the payload) as
+// kIdxPieces bulk copies completing on the stage's mbarrier.
+__device__ __forceinline__ void stage_idx(uint32_t dst, const uint8_t* src, int bytes,
+                                          uint32_t mbar) {
+  if (kIdxPieces <= 1) {
+    bulk_g2s(dst, src, (uint32_t)bytes, mbar);
+    return;
+  }
+  const int piece = ((bytes + kIdxPieces - 1) / kIdxPieces + 15) & ~15;
+  for (int o = 0; o < bytes; o += piece)
+    bulk_g2s(dst + o, src + o, (uint32_t)min(piece, bytes - o), mbar);
+}
 constexpr int kLastOnlyBytes = 8192;              // split-K tiles up to this size: the last CTA finishes them
 
 template <int G, int NW, int TPW>
@@ -325,8 +342,8 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
         const int ab = p.act_tma ? act_tile_bytes(p, kt, G) : 0;
         const uint32_t stg = mbar + 32 + 8 * t;
         mbar_expect_tx(stg, (uint32_t)(rows * 16 + ab));
-        bulk_g2s(idx_s + (uint32_t)(t * L::IDX_BYTES), p.payload + ((size_t)kt * p.m_pad + m0) * 16,
-                 (uint32_t)(rows * 16), stg);
+        stage_idx(idx_s + (uint32_t)(t * L::IDX_BYTES), p.payload + ((size_t)kt * p.m_pad + m0) * 16,
+                  rows * 16, stg);
       }
       // (2) activations come from the previous kernel (quantizer)
       pdl_wait();
@@ -350,8 +367,8 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
         const int ab = p.act_tma ? act_tile_bytes(p, kt, G) : 0;
         const uint32_t stg = mbar + 32 + 8 * st;
         mbar_expect_tx(stg, (uint32_t)(rows * 16 + ab));
-        bulk_g2s(idx_s + (uint32_t)(st * L::IDX_BYTES), p.payload + ((size_t)kt * p.m_pad + m0) * 16,
-                 (uint32_t)(rows * 16), stg);
+        stage_idx(idx_s + (uint32_t)(st * L::IDX_BYTES), p.payload + ((size_t)kt * p.m_pad + m0) * 16,
+                  rows * 16, stg);
         if (ab > 0)
           bulk_g2s(act_s + (uint32_t)(st * L::ACT_BYTES), p.A + (size_t)kt * kKgTile * G * p.N,
                    (uint32_t)ab, stg);

@@ -19,7 +19,8 @@ from typing import Callable, List, Optional, Sequence, Tuple
 
 import numpy as np
 
-__all__ = ["shard_rows", "RowShardedLinear", "LayerChain", "CHAIN_Q_ROWS", "PeerOutputs"]
+__all__ = ["shard_rows", "RowShardedLinear", "LayerChain", "CHAIN_Q_ROWS", "PeerOutputs",
+           "Chunk", "split_tokens", "join_tokens"]
 
 
 def shard_rows(M: int, world: int, rank: int) -> Tuple[int, int, int]:
@@ -178,6 +179,12 @@ class RowShardedLinear:
         bytes than fp32) are all-gathered.  Returns (q [q_rows][N] int8,
         scale [N] fp32) on every rank -- bit-identical to quantizing the
         gathered fp32 output."""
+        local, amax = self._fused_local(A, a_scale, q_rows, mul_in)
+        return self._finish_quantized(local, amax, A.shape[1], q_rows)
+
+    def _fused_local(self, A, a_scale, q_rows, mul_in):
+        """This rank's fp32 rows (epilogue: * mul_in) and the per-token maxima
+        of its rows below q_rows (int32 [N], float bits)."""
         import torch
         N = A.shape[1]
         dev = A.device
@@ -187,6 +194,14 @@ class RowShardedLinear:
         arows = max(0, min(self.rows, q_rows - self.r0))
         if self.rows:
             self._fused(self.shard, A, a_scale, local, mul_in, amax, arows)
+        return local, amax
+
+    def _finish_quantized(self, local, amax, N, q_rows):
+        """MAX all-reduce of the maxima, quantize this rank's rows with them,
+        all-gather the int8 shards: (q [q_rows][N], scale [N])."""
+        import torch
+        dev = local.device
+        q_rows = self.M if q_rows is None else q_rows
         d = _dist()
         if d is not None and self.world > 1:
             d.all_reduce(amax, op=d.ReduceOp.MAX)
@@ -204,6 +219,45 @@ class RowShardedLinear:
         full = torch.empty((self.Mp * self.world, N), dtype=torch.int8, device=dev)
         d.all_gather_into_tensor(full, q_loc)
         return full[:q_rows], scale
+
+    def forward_quantized_chunks(self, chunks, q_rows: Optional[int] = None, mul_ins=None,
+                                 comm=None):
+        """f1 overlapped with compute: the tokens are split into chunks
+        (per-token quantization makes them independent) and, per chunk, the
+        fused mpGeMM runs on the compute (current) stream while the previous
+        chunks' MAX all-reduce, quantization and int8 all-gather run on the
+        `comm` stream -- the exchange of chunk i overlaps the compute of chunk
+        i+1 (and of the next linear's earlier chunks).
+
+        chunks: list of Chunk; mul_ins: per-chunk local rows [rows][Nc] or
+        None.  Returns a list of Chunk (q [q_rows][Nc], scale [Nc], ready
+        event on `comm`).  comm None (CPU / gloo): sequential, same values."""
+        out = []
+        for c, ch in enumerate(chunks):
+            A, s = ch.wait()
+            local, amax = self._fused_local(A, s, q_rows, None if mul_ins is None else mul_ins[c])
+            if comm is None:
+                q, sc = self._finish_quantized(local, amax, A.shape[1], q_rows)
+                out.append(Chunk(q, sc))
+                continue
+            import torch
+            cur = torch.cuda.current_stream(A.device)
+            done = torch.cuda.Event()
+            done.record(cur)
+            with torch.cuda.stream(comm):
+                comm.wait_event(done)
+                # produced on `cur`, consumed on `comm`: keep the blocks alive
+                local.record_stream(comm)
+                amax.record_stream(comm)
+                q, sc = self._finish_quantized(local, amax, A.shape[1], q_rows)
+                ready = torch.cuda.Event()
+                ready.record(comm)
+            out.append(Chunk(q, sc, ready))
+        return out
+
+    def local_chunks(self, chunks):
+        """This rank's fp32 rows per chunk (no gather; config 5's gate rows)."""
+        return [self.local(*ch.wait()) for ch in chunks]
 
     def _cuda_compute(self, shard, A, a_scale, out):
         # workspace path: the planner may pick the stream-K schedule
@@ -248,6 +302,41 @@ class RowShardedLinear:
         return res
 
 
+class Chunk:
+    """A token chunk of the chain's int8 activations: q [K][Nc], scale [Nc]
+    and, when produced on a side stream, the event that marks them ready."""
+
+    __slots__ = ("q", "scale", "ready")
+
+    def __init__(self, q, scale, ready=None):
+        self.q, self.scale, self.ready = q, scale, ready
+
+    def wait(self):
+        """(q, scale), with the current stream ordered after their producer."""
+        if self.ready is not None:
+            import torch
+            cur = torch.cuda.current_stream(self.q.device)
+            cur.wait_event(self.ready)
+            self.q.record_stream(cur)
+            self.scale.record_stream(cur)
+        return self.q, self.scale
+
+
+def split_tokens(q, scale, n_chunks: int):
+    """Split [K][N] int8 activations (+ scale [N]) into contiguous token chunks."""
+    N = q.shape[1]
+    bounds = [N * i // n_chunks for i in range(n_chunks + 1)]
+    return [Chunk(q[:, a:b].contiguous(), scale[a:b].contiguous())
+            for a, b in zip(bounds, bounds[1:]) if b > a]
+
+
+def join_tokens(chunks):
+    """Concatenate chunks back into ([K][N] int8, [N] fp32)."""
+    import torch
+    pairs = [ch.wait() for ch in chunks]
+    return torch.cat([p[0] for p in pairs], 1), torch.cat([p[1] for p in pairs])
+
+
 # Config 5 glue (DESIGN.md reading c14): per layer
 #   qkv = L_qkv(x); o = L_o(Q(qkv[0:2560])); u = Q(o);
 #   h = L_gate(u) * L_up(u); x' = Q(L_down(Q(h)))
@@ -262,8 +351,15 @@ class LayerChain:
     """
 
     def __init__(self, layers: Sequence[Sequence[RowShardedLinear]], q_rows: int = CHAIN_Q_ROWS,
-                 quantize: Optional[Callable] = None, fused: bool = False):
+                 quantize: Optional[Callable] = None, fused: bool = False, chunks: int = 1,
+                 comm_stream=None):
+        """chunks > 1 (with fused): the f1 chain overlapped with compute --
+        tokens split into `chunks` groups, each linear's exchange of chunk i
+        on `comm_stream` while chunk i+1 computes (comm_stream None on a GPU:
+        a new side stream; on CPU: sequential)."""
         self.fused = fused
+        self.chunks = chunks
+        self.comm = comm_stream
         self.layers = [tuple(l) for l in layers]
         self.q_rows = q_rows
         if quantize is None:
@@ -282,6 +378,15 @@ class LayerChain:
         hq, hs = L_up.forward_quantized(u, su, mul_in=gate)
         return L_down.forward_quantized(hq, hs)
 
+    def layer_chunked(self, l, chunks):
+        """layer_fused over token chunks, exchange overlapped with compute."""
+        L_qkv, L_o, L_gate, L_up, L_down = self.layers[l]
+        c1 = L_qkv.forward_quantized_chunks(chunks, q_rows=self.q_rows, comm=self.comm)
+        c2 = L_o.forward_quantized_chunks(c1, comm=self.comm)
+        gates = L_gate.local_chunks(c2)
+        c3 = L_up.forward_quantized_chunks(c2, mul_ins=gates, comm=self.comm)
+        return L_down.forward_quantized_chunks(c3, comm=self.comm)
+
     def layer(self, l, xq, xs):
         if self.fused:
             return self.layer_fused(l, xq, xs)
@@ -298,6 +403,14 @@ class LayerChain:
 
     def __call__(self, xq, xs, n_layers: Optional[int] = None):
         n = len(self.layers) if n_layers is None else n_layers
+        if self.fused and self.chunks > 1:
+            if self.comm is None and xq.is_cuda:
+                import torch
+                self.comm = torch.cuda.Stream(xq.device)
+            ch = split_tokens(xq, xs, self.chunks)
+            for l in range(n):
+                ch = self.layer_chunked(l, ch)
+            return join_tokens(ch)
         for l in range(n):
             xq, xs = self.layer(l, xq, xs)
         return xq, xs

@@ -1,5 +1,1 @@
-set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -25 > gpurun_out/r2_gputest1.log
-timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/r2_bench1.json 2> gpurun_out/r2_bench1.err
-tail -c 3000 gpurun_out/r2_bench1.err
+timeout 900 python scripts/decode_bench.py "" abtmp/libvlut_p4.so abtmp/libvlut_p16.so abtmp/libvlut_p4r8.so abtmp/libvlut_p16r8.so > gpurun_out/r2_decode3.txt 2>&1

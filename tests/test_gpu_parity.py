@@ -62,6 +62,25 @@ def test_quantize_bit_exact(v, K, N):
     assert np.array_equal(q.cpu().numpy(), qr)
 
 
+@pytest.mark.parametrize("K,N", [(2560, 1), (23040, 1), (6912, 2), (1000, 4), (4096, 8),
+                                 (8192, 16), (12, 16), (4, 1), (65536, 2)])
+@pytest.mark.parametrize("with_y", [False, True])
+def test_quantize_small_n_flat_path(v, K, N, with_y):
+    """Decode shapes (N in {1,2,4,8,16}: the flat K3f kernel), plain and
+    x * y (config 5's gate (.) up glue): codes and scales bit-exact; a zero
+    token column gets scale 1 and zero codes."""
+    x = synth.activations_f32(K, N, seed=K + 7 * N)
+    y = synth.activations_f32(K, N, seed=K + 9 * N) if with_y else None
+    if N > 1:
+        x[:, N - 1] = 0.0
+    q, s = v.quantize(to_dev(x), None if y is None else to_dev(y))
+    xr = x if y is None else (x * y).astype(np.float32)
+    qr, sr = oracle.quantize(np.ascontiguousarray(xr))
+    torch.cuda.synchronize()
+    assert np.array_equal(s.cpu().numpy().view(np.int32), sr.view(np.int32))
+    assert np.array_equal(q.cpu().numpy(), qr)
+
+
 def test_quantize_half_boundaries(v):
     """Values whose quotient x / s sits on, or a few ulps around, a k + 1/2
     rounding boundary for every k in [-127, 126] and several scales: codes
@@ -265,7 +284,9 @@ def test_config5_chain_30_layers_sampled_tokens(v):
     the fused re-quantization chain (LayerChain(fused=True), f1); the oracle
     re-runs the chain (oracle.config5_layer, reading c14) on 16 sampled token
     columns -- per-token quantization makes columns independent -- and codes
-    and scales must be bit-identical after every one of the 30 layers.
+    and scales must be bit-identical after every one of the 30 layers.  The
+    overlapped f1 chain (4 token chunks, exchange on a side stream) must
+    equal both on every token.
     Layers are built one at a time (weights generated, packed, checked, freed)."""
     from paper_2512_06443_b200.sharded import LayerChain, RowShardedLinear
     cfg = synth.CONFIGS[5]
@@ -274,6 +295,7 @@ def test_config5_chain_30_layers_sampled_tokens(v):
     x = synth.activations_f32(2560, N, synth.act_seed(cfg, N))
     xq, xs = v.quantize(to_dev(x))
     fq, fs = xq, xs
+    kq, ks = xq, xs
     cols = np.unique(np.concatenate([[0, N - 1], synth.rng(5).integers(0, N, size=14)]))
     q_ref, s_ref = oracle.quantize(np.ascontiguousarray(x[:, cols]))
     for l in range(n_layers):
@@ -281,6 +303,8 @@ def test_config5_chain_30_layers_sampled_tokens(v):
         lay = [RowShardedLinear(w, 4, synth.W_SCALE, device=dev(), device_pack=True) for w in lw]
         xq, xs = LayerChain([lay]).layer(0, xq, xs)
         fq, fs = LayerChain([lay], fused=True).layer(0, fq, fs)
+        # f1 overlapped: 4 token chunks, exchange/quantize on a side stream
+        kq, ks = LayerChain([lay], fused=True, chunks=4)(kq, ks)
         q_ref, s_ref = oracle.config5_layer(lw, synth.W_SCALE, q_ref, s_ref, q_rows=2560)
         torch.cuda.synchronize()
         assert np.array_equal(xs.cpu().numpy()[cols].view(np.int32), s_ref.view(np.int32)), l
@@ -289,6 +313,7 @@ def test_config5_chain_30_layers_sampled_tokens(v):
         assert np.array_equal(fq.cpu().numpy()[:, cols], q_ref), l
         # the two chains agree on every token, not only the sampled ones
         assert torch.equal(xq, fq) and torch.equal(xs.view(torch.int32), fs.view(torch.int32)), l
+        assert torch.equal(xq, kq) and torch.equal(xs.view(torch.int32), ks.view(torch.int32)), l
         del lay, lw
 
 

@@ -97,9 +97,14 @@ def _worker(rank, world, port, M, K, N, g, result_path):
         # int8 all-gather, gate (.) up fused into the up projection
         fchain = LayerChain([layer, layer], q_rows=Kc, quantize=oracle_quantize, fused=True)
         fq, fs = fchain(torch.from_numpy(xq), torch.from_numpy(xs))
+        # f1 overlapped: tokens in 3 chunks, per chunk MAX all-reduce + int8
+        # gather (sequential on CPU; on a GPU on a side stream)
+        kchain = LayerChain([layer, layer], q_rows=Kc, quantize=oracle_quantize, fused=True,
+                            chunks=3)
+        kq, ks = kchain(torch.from_numpy(xq), torch.from_numpy(xs))
         if rank == 0:
             np.savez(result_path, out=out.numpy(), cq=cq.numpy(), cs=cs.numpy(),
-                     fq=fq.numpy(), fs=fs.numpy())
+                     fq=fq.numpy(), fs=fs.numpy(), kq=kq.numpy(), ks=ks.numpy())
     finally:
         dist.destroy_process_group()
 
@@ -124,3 +129,4 @@ def test_gloo_row_sharded_equals_single(tmp_path, world, M):
         xq, xs = oracle.config5_layer(Ws, synth.W_SCALE, xq, xs, q_rows=Kc)
     assert np.array_equal(res["cq"], xq) and np.array_equal(res["cs"], xs)
     assert np.array_equal(res["fq"], xq) and np.array_equal(res["fs"], xs)
+    assert np.array_equal(res["kq"], xq) and np.array_equal(res["ks"], xs)
