@@ -81,8 +81,16 @@ struct Cfg {
 };
 
 // WARPS lookup warps (one output row per thread) + kBuilderWarps table
-// builders; threads = 32 * (WARPS + kBuilderWarps).
+// builders; threads = 32 * (WARPS + builders).  Two rows per lookup thread
+// (768 rows per table) halve the table build per lookup, so two builder warps
+// keep up there -- and the 64 threads freed raise the register budget from
+// 128 to 144 per thread (two rows' SWAR fields are 64 registers).
 constexpr int kBuilderWarps = 4;
+#ifndef VLUT_BW_RPT2
+#define VLUT_BW_RPT2 4
+#endif
+template <int WARPS, int RPT>
+constexpr int kBW = (RPT == 2 && WARPS == 12) ? VLUT_BW_RPT2 : kBuilderWarps;
 constexpr int kTmemCols = 256;  // int32 accumulators: 64 columns per 4 lookup warps
 
 // RPT = output rows per lookup thread: 1 (K1, both schedules) or 2 (the
@@ -91,8 +99,9 @@ constexpr int kTmemCols = 256;  // int32 accumulators: 64 columns per 4 lookup w
 template <int G, int WARPS, int RPT = 1>
 struct Layout {
   static_assert(RPT == 1 || RPT == 2, "one or two rows per lookup thread");
+  static constexpr int BW = kBW<WARPS, RPT>;              // builder warps
   static constexpr int NLT = WARPS * 32;                  // lookup threads
-  static constexpr int THREADS = NLT + kBuilderWarps * 32;
+  static constexpr int THREADS = NLT + BW * 32;
   static constexpr int BUILDER0 = NLT;                    // first builder thread
   static constexpr int MCTA = NLT * RPT;                  // output rows per CTA
   static constexpr int RED_BYTES = NLT * kNcta * 4;       // int32 tile of one row block
@@ -308,7 +317,7 @@ __device__ __forceinline__ void stage_tile(const Params& p, int kt, int buf, int
                                            uint8_t* smem, int bt, int what) {
   using C = Cfg<G>;
   using L = Layout<G, WARPS, RPT>;
-  constexpr int NB = kBuilderWarps * 32;
+  constexpr int NB = L::BW * 32;
   if (what & 1) {
     // index vectors: one 16-byte row per CTA row (rows past m_pad -> zero fill)
     for (int r = bt; r < L::MCTA; r += NB) {
@@ -381,7 +390,7 @@ __device__ __forceinline__ void stage_tile_bulk(const Params& p, int kt, int buf
                                                 bool do_idx, bool do_act, bool arm) {
   using C = Cfg<G>;
   using L = Layout<G, WARPS, RPT>;
-  constexpr int NB = kBuilderWarps * 32;
+  constexpr int NB = L::BW * 32;
   const int idx_rows = max(0, min(L::MCTA, p.m_pad - m0));
   const int k0 = kt * kKgTile * G;
   const int a_rows = max(0, min(C::A_ROWS, p.K - k0));
@@ -443,16 +452,16 @@ __device__ __forceinline__ void build_blocks(uint32_t row0, uint32_t S, const ui
   }
 }
 
-// Builder warp bw (of kBuilderWarps) builds the half tables of its groups of
+// Builder warp bw (of BW) builds the half tables of its groups of
 // sub-stage [grp0, grp0 + GS) of the staged K-tile.
-template <int G>
+template <int G, int BW = kBuilderWarps>
 __device__ __forceinline__ void build_tables(uint32_t tab_s, uint32_t a_s, int grp0, int bw,
                                              int lane) {
   using C = Cfg<G>;
   constexpr uint32_t K1 = 0x00010001u;
   constexpr uint32_t C128 = 128u * K1;
 #pragma unroll 1
-  for (int j = bw; j < C::GS; j += kBuilderWarps) {
+  for (int j = bw; j < C::GS; j += BW) {
     uint32_t U[8], P[8], Mn[8];
 #pragma unroll
     for (int r = 0; r < G; ++r) {
@@ -477,37 +486,81 @@ constexpr int kLookupGP = (WARPS >= 16) ? 1 : 2;
 // 170 registers per thread and keep two
 template <int WARPS, int RPT>
 constexpr int kLookupGP2 = (RPT > 1) ? (WARPS <= 8 ? 2 : 1) : kLookupGP<WARPS>;
+// loads per batch of the one-group path: 4 where 8 would spill (two rows per
+// thread with 12 warps: 64 SWAR registers live)
+#ifndef VLUT_LB_RPT2
+#define VLUT_LB_RPT2 8
+#endif
+#ifndef VLUT_LB_W16
+#define VLUT_LB_W16 8
+#endif
+template <int WARPS, int RPT>
+constexpr int kLookupLB = (RPT > 1 && WARPS >= 12) ? VLUT_LB_RPT2 : (WARPS >= 16 ? VLUT_LB_W16 : 8);
 
-// Groups [SUB*GS, SUB*GS+GS) of the K-tile whose index vector is iwa.
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+// Groups [SUB*GS, SUB*GS+GS) of the K-tile; idx_row = shared address of this
+// thread's 16-byte index row of the tile (one index byte per group: a 32-bit
+// word is loaded when its first group comes up -- the same wavefronts as one
+// LDS.128 per tile, without 4 live registers per row).  Chunk order: slot s
+// of lane l reads the 16-byte chunk c = (l & 7) ^ s of the 128-byte table row
+// (the 8 lanes of an LDS.128 phase hit 8 different bank groups whatever the
+// rows; row addresses are 128-aligned, so the chunk address is one XOR:
+// (row | rot[0]) ^ 16 s -- no per-slot offset registers), or, RX = false,
+// c = (l + s) & 7 with rot[s] = 16 c.
 // GP = groups per load batch: 2 (16 LDS.128 in flight, half the negations on
 // the ALU pipe as XOR, half on the FMA pipe as multiply) or 1 (8 in flight,
 // every negation a multiply: 32 fewer live registers, for the 16-warp
 // variants whose 102-register budget would otherwise spill).
-template <int G, int GP = 2>
+// LB (GP = 1 only): LDS.128 per load batch, 8 or 4 (16 fewer live registers
+// for the variants whose budget would otherwise spill inside this loop).
+// LAZY: index words loaded from shared memory when first needed (idx_row)
+// instead of held in registers (iwa, loaded once per K-tile by the caller) --
+// for the two-rows-per-thread variants; elsewhere the eager form spills less.
+// RX: chunk order c = (lane & 7) ^ s (one XOR per load, no offset registers:
+// the two-rows-per-thread variants) or c = (lane + s) & 7 (rot[s] offsets in
+// registers, r + rot[s]: what the other variants allocate best).
+template <bool RX>
+__device__ __forceinline__ int chunk_of(int lane, int s) {
+  return RX ? ((lane ^ s) & 7) : ((lane + s) & 7);
+}
+
+template <int G, int GP = 2, int LB = 8, bool LAZY = false, bool RX = false>
 __device__ __forceinline__ void lookup_sub(const int SUB, uint32_t tab, const uint32_t (&iwa)[4],
-                                           const uint32_t (&rot)[8], uint32_t (&sw)[8][4],
-                                           int32_t& nneg) {
+                                           uint32_t idx_row, const uint32_t (&rot)[8],
+                                           uint32_t (&sw)[8][4], int32_t& nneg) {
   using C = Cfg<G>;
+  static_assert(LB == 8 || LB == 4, "loads per batch");
+  uint32_t word = 0;
   if constexpr (GP == 1) {
 #pragma unroll
     for (int j = 0; j < C::GS; ++j) {
       const int b = SUB * C::GS + j;
-      const int i = (int)((iwa[b >> 2] >> (8 * (b & 3))) & C::IDX_MASK);
+      if (j == 0 || (b & 3) == 0) word = LAZY ? lds32(idx_row + 4 * (b >> 2)) : iwa[b >> 2];
+      const int i = (int)((word >> (8 * (b & 3))) & C::IDX_MASK);
       const int d = i - C::ZERO;
       const uint32_t m = (uint32_t)(d >> 31);
       const uint32_t pos = (uint32_t)((d ^ (int)m) - (int)m);
       nneg += (int)m;
       const uint32_t sg = m | 1u;
       const uint32_t r = tab + (uint32_t)(j * C::HR * kRowBytes) + pos * kRowBytes;
-      uint4 v[8];
 #pragma unroll
-      for (int s = 0; s < 8; ++s) v[s] = lds128(r + rot[s]);
+      for (int s0 = 0; s0 < 8; s0 += LB) {
+        uint4 v[LB];
 #pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        sw[s][0] += v[s].x * sg;
-        sw[s][1] += v[s].y * sg;
-        sw[s][2] += v[s].z * sg;
-        sw[s][3] += v[s].w * sg;
+        for (int s = 0; s < LB; ++s)
+          v[s] = lds128(RX ? ((r | rot[0]) ^ (uint32_t)(16 * (s0 + s))) : r + rot[s0 + s]);
+#pragma unroll
+        for (int s = 0; s < LB; ++s) {
+          sw[s0 + s][0] += v[s].x * sg;
+          sw[s0 + s][1] += v[s].y * sg;
+          sw[s0 + s][2] += v[s].z * sg;
+          sw[s0 + s][3] += v[s].w * sg;
+        }
       }
     }
     return;
@@ -515,8 +568,9 @@ __device__ __forceinline__ void lookup_sub(const int SUB, uint32_t tab, const ui
 #pragma unroll
   for (int jp = 0; jp < C::GS / 2; ++jp) {
     const int b0 = SUB * C::GS + 2 * jp, b1 = b0 + 1;  // index bytes in the K-tile
-    const int i0 = (int)((iwa[b0 >> 2] >> (8 * (b0 & 3))) & C::IDX_MASK);
-    const int i1 = (int)((iwa[b1 >> 2] >> (8 * (b1 & 3))) & C::IDX_MASK);
+    if (jp == 0 || (b0 & 3) == 0) word = LAZY ? lds32(idx_row + 4 * (b0 >> 2)) : iwa[b0 >> 2];
+    const int i0 = (int)((word >> (8 * (b0 & 3))) & C::IDX_MASK);
+    const int i1 = (int)((word >> (8 * (b1 & 3))) & C::IDX_MASK);  // b0 even: same word
     const int d0 = i0 - C::ZERO, d1 = i1 - C::ZERO;
     const uint32_t m0 = (uint32_t)(d0 >> 31), m1 = (uint32_t)(d1 >> 31);  // 0 or ~0: negate
     const uint32_t p0 = (uint32_t)((d0 ^ (int)m0) - (int)m0);              // |d|
@@ -528,8 +582,8 @@ __device__ __forceinline__ void lookup_sub(const int SUB, uint32_t tab, const ui
     uint4 v0[8], v1[8];
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
-      v0[s] = lds128(r0 + rot[s]);
-      v1[s] = lds128(r1 + rot[s]);
+      v0[s] = lds128(RX ? ((r0 | rot[0]) ^ (uint32_t)(16 * s)) : r0 + rot[s]);
+      v1[s] = lds128(RX ? ((r1 | rot[0]) ^ (uint32_t)(16 * s)) : r1 + rot[s]);
     }
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
@@ -599,7 +653,7 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 
 // ---------------------------------------------------------------- the kernel
 template <int G, int WARPS, bool ACC_ONLY>
-__global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
+__global__ void __launch_bounds__((WARPS + kBW<WARPS, 1>) * 32, 1)
     vlut_mpgemm_kernel(const __grid_constant__ Params p) {
   using C = Cfg<G>;
   using L = Layout<G, WARPS>;
@@ -683,7 +737,7 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
         }
         bar_sync(5, kBuilderWarps * 32);  // tile T's A rows visible to all builders
       }
-      build_tables<G>(tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES),
+      build_tables<G, L::BW>(tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES),
                       a_s0 + (uint32_t)((T % kStageBufs) * C::A_BYTES), sub * C::GS, bw, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(mbar + mb_full(u % C::NBUF));  // table u (and tile T's indices) ready
@@ -704,11 +758,11 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
     tmem_fence_after();
     tmem_base = *tmem_slot;
     VLUT_STAMP(1);
-    // lane-rotated chunk offsets: slot s of this lane holds tokens 8c..8c+7,
+    // lane-rotated chunk order: slot s of this lane holds tokens 8c..8c+7,
     // c = (lane + s) & 7
     uint32_t rot[8];
 #pragma unroll
-    for (int s = 0; s < 8; ++s) rot[s] = (uint32_t)(((lane + s) & 7) * 16);
+    for (int s = 0; s < 8; ++s) rot[s] = (uint32_t)(chunk_of<false>(lane, s) * 16);
     const uint32_t taddr = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
     uint32_t sw[8][4];
 #pragma unroll
@@ -726,12 +780,13 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
         const int u = t * C::SUBS + sub;
         mbar_wait(mbar + mb_full(u % C::NBUF), (u / C::NBUF) & 1);  // table u built
         if (u == 0) VLUT_STAMP(2);
+        const uint32_t idx_row = idx_s + (uint32_t)((t % kStageBufs) * L::IDX_BYTES + tid * 16);
         if (sub == 0) {
-          const uint4 iw = lds128(idx_s + (t % kStageBufs) * L::IDX_BYTES + tid * 16);
+          const uint4 iw = lds128(idx_row);
           iwa[0] = iw.x; iwa[1] = iw.y; iwa[2] = iw.z; iwa[3] = iw.w;
         }
-        lookup_sub<G, kLookupGP<WARPS>>(sub, tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES), iwa, rot, sw,
-                                        nneg);
+        lookup_sub<G, kLookupGP<WARPS>, kLookupLB<WARPS, 1>>(
+            sub, tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES), iwa, idx_row, rot, sw, nneg);
         __syncwarp();
         if (lane == 0) mbar_arrive(mbar + mb_empty(u % C::NBUF));  // table buffer u & 1 free
       }
@@ -779,7 +834,7 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
       for (int h = 0; h < 4; ++h) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int c = (lane + 2 * h + e) & 7;
+          const int c = chunk_of<false>(lane, 2 * h + e);
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             sts32(red_s + (uint32_t)(((8 * c + j) * L::MCTA + r) * 4), v[h][8 * e + j] - bias_total);
@@ -791,7 +846,7 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int s = 2 * h + e;
-          const uint32_t c = (uint32_t)((lane + s) & 7);
+          const uint32_t c = (uint32_t)chunk_of<false>(lane, s);
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             const uint32_t uu = (2 * c + hh) ^ swz;

@@ -31,6 +31,13 @@
 
 namespace vlut {
 
+// The g = 5 two-rows-per-thread 12-warp variant (128 registers, 64 of them
+// SWAR fields) loads index words lazily and uses the XOR chunk order (A/B:
+// config 4 g = 5 N = 1024 1089 -> 1073 us; at g = 4 the eager form is ~1.5 %
+// faster on config 5's gate shape).
+template <int G, int WARPS, int RPT>
+constexpr bool kLazyRx = (G == 5 && RPT == 2 && WARPS == 12);
+
 struct SkParams {
   int NT, MT;           // N-tiles, M-tiles
   long long U;          // units = NT * MT * KT
@@ -115,6 +122,7 @@ __device__ __forceinline__ void sk_epilogue(const Params& p, const SkParams& sk,
   using C = Cfg<G>;
   using L = Layout<G, WARPS, RPT>;
   constexpr int NLT = L::NLT;
+  constexpr bool RX = kLazyRx<G, WARPS, RPT>;
   const int r = tid;  // row within a row block
   const int m0 = (sg.tile / sk.NT) * L::MCTA, n0 = (sg.tile % sk.NT) * kNcta;
   const int32_t bias_total = C::BIAS * kKgTile * (sg.kb - sg.ka);
@@ -149,7 +157,7 @@ __device__ __forceinline__ void sk_epilogue(const Params& p, const SkParams& sk,
           tmem_wait_ld();
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const uint32_t c = (uint32_t)((lane + 2 * h + e) & 7);
+            const uint32_t c = (uint32_t)chunk_of<RX>(lane, 2 * h + e);
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
               const uint32_t uu = (2 * c + hh) ^ swz;
@@ -287,7 +295,7 @@ __device__ __forceinline__ void sk_epilogue(const Params& p, const SkParams& sk,
         int32_t* wrow = sk.ws + ((size_t)cta * L::MCTA + rr) * kNcta;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int c = (lane + 2 * h + e) & 7;
+          const int c = chunk_of<RX>(lane, 2 * h + e);
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             const int32_t* x = a + 8 * e + 4 * hh;
@@ -299,7 +307,7 @@ __device__ __forceinline__ void sk_epilogue(const Params& p, const SkParams& sk,
       if (m >= p.M) continue;
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int c = (lane + 2 * h + e) & 7;
+        const int c = chunk_of<RX>(lane, 2 * h + e);
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           const int n = n0 + 8 * c + 4 * hh;
@@ -347,11 +355,12 @@ __device__ __forceinline__ void sk_epilogue(const Params& p, const SkParams& sk,
 }
 
 template <int G, int WARPS, int RPT, bool ACC_ONLY>
-__global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
+__global__ void __launch_bounds__((WARPS + kBW<WARPS, RPT>) * 32, 1)
     vlut_mpgemm_sk_kernel(const __grid_constant__ Params p, const SkParams sk) {
   using C = Cfg<G>;
   using L = Layout<G, WARPS, RPT>;
   constexpr int GP = kLookupGP2<WARPS, RPT>;
+  constexpr bool RX = kLazyRx<G, WARPS, RPT>;
   extern __shared__ __align__(1024) uint8_t smem[];
 
   const int tid = threadIdx.x;
@@ -372,7 +381,7 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
 
   if (tid == L::BUILDER0) {
     for (int b = 0; b < C::NBUF; ++b) {
-      mbar_init(mbar + mb_full(b), kBuilderWarps);
+      mbar_init(mbar + mb_full(b), L::BW);
       mbar_init(mbar + mb_empty(b), WARPS);
     }
     for (int st = 0; st < kStageBufs; ++st) mbar_init(mbar + mb_stage(st), 1);
@@ -428,9 +437,9 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
           cp_async_wait_all();
         }
         if (bulk) mbar_wait(mbar + mb_stage(T % kStageBufs), (T / kStageBufs) & 1);
-        bar_sync(5, kBuilderWarps * 32);
+        bar_sync(5, L::BW * 32);
       }
-      build_tables<G>(tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES),
+      build_tables<G, L::BW>(tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES),
                       a_s0 + (uint32_t)((T % kStageBufs) * C::A_BYTES), sub * C::GS, bw, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(mbar + mb_full(u % C::NBUF));
@@ -448,9 +457,10 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
     bar_sync(6, L::NLT);
     tmem_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // slot s of this lane <-> 16-byte chunk chunk_of<RX>(lane, s) of a row
     uint32_t rot[8];
 #pragma unroll
-    for (int s = 0; s < 8; ++s) rot[s] = (uint32_t)(((lane + s) & 7) * 16);
+    for (int s = 0; s < 8; ++s) rot[s] = (uint32_t)(chunk_of<RX>(lane, s) * 16);
     // row block rb of this warp: lanes 32 (warp & 3).., columns 64 (warp >> 2) + 256 rb
     const uint32_t taddr = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
     uint32_t sw[RPT][8][4];
@@ -460,11 +470,11 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
     for (int rb = 0; rb < RPT; ++rb) {
       nneg[rb] = 0;
 #pragma unroll
+      for (int q = 0; q < 4; ++q) iwa[rb][q] = 0u;
+#pragma unroll
       for (int s = 0; s < 8; ++s)
 #pragma unroll
         for (int q = 0; q < 4; ++q) sw[rb][s][q] = 0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) iwa[rb][q] = 0u;
     }
     bool first = true;
     int since_flush = warp % kFlushTiles;
@@ -476,17 +486,19 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
       for (int sub = 0; sub < C::SUBS; ++sub) {
         const int u = t * C::SUBS + sub;
         mbar_wait(mbar + mb_full(u % C::NBUF), (u / C::NBUF) & 1);
-        if (sub == 0) {
+        constexpr bool LAZY = kLazyRx<G, WARPS, RPT>;  // index words from shared memory
 #pragma unroll
-          for (int rb = 0; rb < RPT; ++rb) {
-            const uint4 iw = lds128(idx_s + (t % kStageBufs) * L::IDX_BYTES + (tid + rb * L::NLT) * 16);
+        for (int rb = 0; rb < RPT; ++rb) {
+          const uint32_t idx_row =
+              idx_s + (uint32_t)((t % kStageBufs) * L::IDX_BYTES + (tid + rb * L::NLT) * 16);
+          if (!LAZY && sub == 0) {
+            const uint4 iw = lds128(idx_row);
             iwa[rb][0] = iw.x; iwa[rb][1] = iw.y; iwa[rb][2] = iw.z; iwa[rb][3] = iw.w;
           }
+          lookup_sub<G, GP, kLookupLB<WARPS, RPT>, LAZY, RX>(
+              sub, tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES), iwa[rb], idx_row, rot, sw[rb],
+              nneg[rb]);
         }
-#pragma unroll
-        for (int rb = 0; rb < RPT; ++rb)
-          lookup_sub<G, GP>(sub, tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES), iwa[rb], rot, sw[rb],
-                            nneg[rb]);
         __syncwarp();
         if (lane == 0) mbar_arrive(mbar + mb_empty(u % C::NBUF));
       }
