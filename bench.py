@@ -842,7 +842,7 @@ def sweep(v, dev, stream, flush, reps=10):
                 t = timeit(pw, A, sc, out)
                 timing = "per-launch events, L2 flushed"
             kern = (f"K2 lane-slot tpw={pl.tpw} nw={pl.nw} splits={pl.splits}" if pl.slot else
-                    f"K1 warps={pl.warps} m_cta={pl.m_cta} splits={pl.splits} streamk={pl.streamk}")
+                    f"K1 warps={pl.warps} m_cta={pl.m_cta} n_cta={pl.n_cta} splits={pl.splits} streamk={pl.streamk}")
             e = {"config": 4, "M": lin.M, "K": lin.K, "N": N, "g": g, "us": t * 1e6,
                  "kernel": kern, "timing": timing,
                  "tokens_s": N / t, "gops": 2 * lin.M * lin.K * N / t / 1e9,
@@ -959,7 +959,7 @@ def config_table(path, oracle_budget_s=0.6):
         t_roof = max(hbm_b / hbm, lk / r_lu)
         pl = v.plan_ws(M, K, N, g)
         kern = (f"K2 tpw={pl.tpw} nw={pl.nw} splits={pl.splits}" if pl.slot else
-                f"K1 warps={pl.warps} m_cta={pl.m_cta} splits={pl.splits} streamk={pl.streamk}")
+                f"K1 warps={pl.warps} m_cta={pl.m_cta} n_cta={pl.n_cta} splits={pl.splits} streamk={pl.streamk}")
         call = lambda p_: (lambda: v.mpgemm_ws(p_, A, sc, synth.W_SCALE, out=out, ws=ws))
         with ClockSampler(dev) as clk:
             if N <= 64:

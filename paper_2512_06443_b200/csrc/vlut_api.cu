@@ -14,6 +14,7 @@
 #include "../../include/vlut.h"
 #include "vlut_aux_kernels.cuh"
 #include "vlut_kernel.cuh"
+#include "vlut_kernel32.cuh"
 #include "vlut_kernel_sk.cuh"
 #include "vlut_kernel_slot.cuh"
 #include <atomic>
@@ -121,7 +122,8 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-vlut_status encode_a_map(CUtensorMap* map, const int8_t* A, int K, int N, int g) {
+vlut_status encode_a_map(CUtensorMap* map, const int8_t* A, int K, int N, int g,
+                         int box_n = vlut::kNcta) {
   static EncodeTiledFn fn = nullptr;
   static std::once_flag once;
   static cudaError_t get_err = cudaSuccess;
@@ -134,7 +136,7 @@ vlut_status encode_a_map(CUtensorMap* map, const int8_t* A, int K, int N, int g)
   if (!fn) return fail(VLUT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (%s)", cudaGetErrorString(get_err));
   const cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)K};
   const cuuint64_t strides[1] = {(cuuint64_t)N};
-  const cuuint32_t box[2] = {(cuuint32_t)vlut::kNcta, (cuuint32_t)(vlut::kKgTile * g)};
+  const cuuint32_t box[2] = {(cuuint32_t)box_n, (cuuint32_t)(vlut::kKgTile * g)};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)A, dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -209,6 +211,75 @@ int active_clusters(int S) {
     c = n;
   }
   return c;
+}
+
+// K1-32 (32-token tiles): kernel attribute + co-resident clusters
+template <int G, int WARPS, bool ACC>
+cudaError_t prepare_kernel32() {
+  using L = vlut::Layout32<G, WARPS>;
+  static std::once_flag flags[64];
+  static cudaError_t errs[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::call_once(flags[dev & 63], [&] {
+    errs[dev & 63] = cudaFuncSetAttribute(vlut::vlut_mpgemm32_kernel<G, WARPS, ACC>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+  });
+  return errs[dev & 63];
+}
+
+template <int G, int WARPS>
+int active_clusters32(int S) {
+  using L = vlut::Layout32<G, WARPS>;
+  static std::mutex mu;
+  static int cache[64][9];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || S < 1 || S > 8) return 0;
+  std::lock_guard<std::mutex> lk(mu);
+  int& c = cache[dev & 63][S];
+  if (c == 0) {
+    if (prepare_kernel32<G, WARPS, false>() != cudaSuccess) return 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)S, 1, 1);
+    cfg.blockDim = dim3(L::THREADS, 1, 1);
+    cfg.dynamicSmemBytes = L::SMEM;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)S;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, vlut::vlut_mpgemm32_kernel<G, WARPS, false>, &cfg) !=
+            cudaSuccess ||
+        n <= 0) {
+      cudaGetLastError();
+      n = -1;
+    }
+    c = n;
+  }
+  return c;
+}
+
+int active_clusters32_for(int g, int warps, int S) {
+  if (g == 4) {
+    if (warps == 8) return active_clusters32<4, 8>(S);
+    if (warps == 12) return active_clusters32<4, 12>(S);
+    return active_clusters32<4, 16>(S);
+  }
+  if (warps == 8) return active_clusters32<5, 8>(S);
+  if (warps == 12) return active_clusters32<5, 12>(S);
+  return active_clusters32<5, 16>(S);
+}
+
+int smem_bytes32_for(int g, int warps) {
+  if (g == 4)
+    return warps == 8 ? vlut::Layout32<4, 8>::SMEM
+                      : (warps == 12 ? vlut::Layout32<4, 12>::SMEM : vlut::Layout32<4, 16>::SMEM);
+  return warps == 8 ? vlut::Layout32<5, 8>::SMEM
+                    : (warps == 12 ? vlut::Layout32<5, 12>::SMEM : vlut::Layout32<5, 16>::SMEM);
 }
 
 int active_clusters_for(int g, int warps, int S) {
@@ -325,6 +396,56 @@ double plan_for(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
         best->n_cta = vlut::kNcta;
         best->grid_ctas = (int)ctas;
         best->smem_bytes = smem_bytes_for(g, warps);
+        best->streamk = 0;
+      }
+    }
+  }
+  return best_cost;
+}
+
+// K1-32 (32-token tiles, paired-group tables): the same shared-memory cycle
+// units as plan_for -- a 32-token row is half a 128-byte wavefront -- with
+// the lookup path's extra ALU work (per-lane line selection) charged as a
+// factor, a cheaper epilogue (no DSMEM exchange at splits = 1) and the
+// DSMEM reduction of 128-byte rows when split.
+#ifndef VLUT_K32_FACTOR
+#define VLUT_K32_FACTOR 1.08
+#endif
+double plan_for32(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
+  const int KG = (K + g - 1) / g;
+  const int kgt = (KG + VLUT_KG_TILE - 1) / VLUT_KG_TILE;
+  const int NT = (N + vlut::kN32 - 1) / vlut::kN32;
+  const int half_rows = (pow3i(g) + 1) / 2;
+  double best_cost = 1e300;
+  if (getenv("VLUT_NO_K32")) return best_cost;
+  const int warps_opts[3] = {16, 12, 8};
+  for (int wi = 0; wi < 3; ++wi) {
+    const int warps = warps_opts[wi];
+    const int mcta = 32 * warps;
+    const long long MT = (M + mcta - 1) / mcta;
+    for (int S = 1; S <= 8; ++S) {
+      if (S > kgt) continue;
+      const long long ctas = MT * NT * S;
+      if (ctas > 65535LL * 65535LL) continue;
+      int clusters = active_clusters32_for(g, warps, S);
+      if (clusters < 0) continue;
+      if (clusters == 0) clusters = sms / S;
+      const long long slots = (long long)clusters * S;
+      if (slots <= 0) continue;
+      const long long waves = (ctas + slots - 1) / slots;
+      const double tiles = (double)((kgt + S - 1) / S);
+      double per_cta = tiles * VLUT_KG_TILE * 0.5 * (double)(mcta + half_rows) * VLUT_K32_FACTOR;
+      per_cta += 4000.0;  // start (first tile + table) and epilogue
+      if (S > 1) per_cta += (double)(S - 1) / S * mcta * 128.0 / 16.0 + 1500.0;
+      const double cost = waves * per_cta;
+      if (cost < best_cost * 0.995) {
+        best_cost = cost;
+        best->warps = warps;
+        best->splits = S;
+        best->m_cta = mcta;
+        best->n_cta = vlut::kN32;
+        best->grid_ctas = (int)ctas;
+        best->smem_bytes = smem_bytes32_for(g, warps);
         best->streamk = 0;
       }
     }
@@ -480,6 +601,44 @@ vlut_status launch_k1(const vlut::Params& p, int S, int NT, int MT, cudaStream_t
   return VLUT_OK;
 }
 
+template <int G, int WARPS, bool ACC>
+vlut_status launch_k1_32(const vlut::Params& p, int S, int NT, int MT, cudaStream_t st) {
+  using L = vlut::Layout32<G, WARPS>;
+  auto kern = vlut::vlut_mpgemm32_kernel<G, WARPS, ACC>;
+  VLUT_CUDA_TRY((prepare_kernel32<G, WARPS, ACC>()));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)S, (unsigned)NT, (unsigned)MT);
+  cfg.blockDim = dim3(L::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = L::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  VLUT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
+  return VLUT_OK;
+}
+
+template <bool ACC>
+vlut_status dispatch32(int g, int warps, const vlut::Params& p, int S, int NT, int MT,
+                       cudaStream_t st) {
+  if (g == 4) {
+    if (warps == 8) return launch_k1_32<4, 8, ACC>(p, S, NT, MT, st);
+    if (warps == 12) return launch_k1_32<4, 12, ACC>(p, S, NT, MT, st);
+    if (warps == 16) return launch_k1_32<4, 16, ACC>(p, S, NT, MT, st);
+  } else {
+    if (warps == 8) return launch_k1_32<5, 8, ACC>(p, S, NT, MT, st);
+    if (warps == 12) return launch_k1_32<5, 12, ACC>(p, S, NT, MT, st);
+    if (warps == 16) return launch_k1_32<5, 16, ACC>(p, S, NT, MT, st);
+  }
+  return fail(VLUT_ERR_UNSUPPORTED, "no K1-32 variant for g=%d warps=%d", g, warps);
+}
+
 template <int G, int WARPS, bool ACC, int RPT = 1>
 vlut_status launch_sk(const vlut::Params& p, const vlut::SkParams& sk, int grid,
                       cudaStream_t st) {
@@ -611,6 +770,14 @@ vlut_status run_slot(const vlut_packed_weights* W, const int8_t* A, const float*
   return ok();
 }
 
+// K1-32 preconditions: TMA activation staging (N % 16 == 0, 16-B aligned A),
+// 16-byte output stores, the plain fp32 (or raw int32) epilogue.
+bool k32_ok(const void* A, const void* out, int N, const int32_t* acc_in, int out_t,
+            const float* mul_in, const unsigned* amax_out) {
+  return N % 16 == 0 && ((((uintptr_t)A) | ((uintptr_t)out)) & 15) == 0 && !acc_in && !out_t &&
+         !mul_in && !amax_out && !getenv("VLUT_NO_K32");
+}
+
 vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,
                        float w_scale, void* out, int M, int K, int N,
                        const vlut_launch_plan* plan_in, void* stream, bool acc_only,
@@ -646,6 +813,8 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
                   plan.splits);
     if (plan.streamk && (!ws || acc_in || out_t))
       return fail(VLUT_ERR_INVALID_ARGUMENT, "stream-K plan needs a workspace and [M][N] output");
+    if (plan.n_cta == vlut::kN32 && plan.streamk)
+      return fail(VLUT_ERR_UNSUPPORTED, "32-token tiles: cluster schedule only");
     // m_cta selects the rows per lookup thread: 0 or 32 * warps -> 1; 64 * warps
     // -> 2 (stream-K with 8 or 12 warps)
     if (plan.m_cta && plan.m_cta != 32 * plan.warps &&
@@ -660,6 +829,14 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
       if (c_sk < c_best) {
         plan = sk_plan;
         c_best = c_sk;
+      }
+    }
+    if (k32_ok(A, out, N, acc_in, out_t, mul_in, amax_out)) {
+      vlut_launch_plan p32 = {};
+      const double c32 = plan_for32(M, K, N, W->g, d.sms, &p32);
+      if (c32 < c_best) {
+        plan = p32;
+        c_best = c32;
       }
     }
     if (plain_epilogue && N <= kSlotAutoMaxN) {
@@ -678,6 +855,18 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
                 sk_workspace_bytes(d.sms));
   if (plan.streamk && (((uintptr_t)ws) & 15)) return fail(VLUT_ERR_MISALIGNED, "workspace not 16-B aligned");
   if (plan.splits > W->kg_tiles) plan.splits = 1;
+  const bool n32 = plan.n_cta == vlut::kN32 && !plan.streamk;
+  if (n32) {
+    if (!k32_ok(A, out, N, acc_in, out_t, mul_in, amax_out) || g_peer_tls.n)
+      return fail(VLUT_ERR_UNSUPPORTED,
+                  "32-token tiles: N %% 16 == 0, 16-B aligned A / out, plain epilogue only");
+    if (plan.m_cta && plan.m_cta != 32 * plan.warps)
+      return fail(VLUT_ERR_UNSUPPORTED, "32-token tiles: m_cta = 32 * warps");
+    const int smem32 = smem_bytes32_for(W->g, plan.warps);
+    if (smem32 > d.smem_optin)
+      return fail(VLUT_ERR_UNSUPPORTED, "needs %d B shared memory, device allows %d", smem32,
+                  d.smem_optin);
+  }
   const int rpt = (plan.streamk && plan.m_cta == 64 * plan.warps) ? 2 : 1;
   const int smem = smem_bytes_for(W->g, plan.warps, rpt);
   if (smem > d.smem_optin)
@@ -700,7 +889,7 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
   const uintptr_t ap = (uintptr_t)A;
   p.a_vec = (N % 16 == 0 && (ap & 15) == 0) ? 16 : ((N % 4 == 0 && (ap & 3) == 0) ? 4 : 1);
   if (p.a_vec == 16) {
-    st = encode_a_map(&p.a_map, A, K, N, W->g);
+    st = encode_a_map(&p.a_map, A, K, N, W->g, n32 ? vlut::kN32 : vlut::kNcta);
     if (st != VLUT_OK) return st;
   }
   p.out_t = out_t;
@@ -728,6 +917,14 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
     const int grid = (int)(sk.U < d.sms ? sk.U : d.sms);
     st = acc_only ? dispatch_sk<true>(W->g, plan.warps, rpt, p, sk, grid, s)
                   : dispatch_sk<false>(W->g, plan.warps, rpt, p, sk, grid, s);
+    if (st != VLUT_OK) return st;
+    return ok();
+  }
+  if (n32) {
+    const long long NT32 = (N + vlut::kN32 - 1) / vlut::kN32;
+    if (NT32 > 65535) return fail(VLUT_ERR_SHAPE, "grid too large");
+    st = acc_only ? dispatch32<true>(W->g, plan.warps, p, plan.splits, (int)NT32, (int)MT, s)
+                  : dispatch32<false>(W->g, plan.warps, p, plan.splits, (int)NT32, (int)MT, s);
     if (st != VLUT_OK) return st;
     return ok();
   }
@@ -991,7 +1188,9 @@ vlut_status vlut_plan(int M, int K, int N, int g, vlut_launch_plan* plan) {
   vlut_status st = device_info(&d);
   if (st != VLUT_OK) return st;
   memset(plan, 0, sizeof(*plan));
-  plan_for(M, K, N, g, d.sms, plan);
+  const double c = plan_for(M, K, N, g, d.sms, plan);
+  vlut_launch_plan p32 = {};
+  if (N % 16 == 0 && !getenv("VLUT_NO_K32") && plan_for32(M, K, N, g, d.sms, &p32) < c) *plan = p32;
   return ok();
 }
 
@@ -1119,6 +1318,14 @@ vlut_status vlut_plan_ws(int M, int K, int N, int g, vlut_launch_plan* plan) {
   if (c_sk < c) {
     *plan = skp;
     c = c_sk;
+  }
+  vlut_launch_plan p32 = {};
+  if (N % 16 == 0 && !getenv("VLUT_NO_K32")) {
+    const double c32 = plan_for32(M, K, N, g, d.sms, &p32);
+    if (c32 < c) {
+      *plan = p32;
+      c = c32;
+    }
   }
   if (N <= kSlotAutoMaxN && plan_slot(M, K, N, g, d.sms, N == 1 ? 1 : 2, 0, 0, true, &slp) < c)
     *plan = slp;

@@ -1,0 +1,494 @@
+// vlut_kernel32.cuh -- K1-32: the fused Vec-LUT mpGeMM with 32-token tiles.
+//
+// K1 (vlut_kernel.cuh) stores a table row of 64 tokens = 128 bytes, one full
+// bank line, so a lookup's 8 LDS.128 of one row are conflict-free in the
+// lane-rotated order.  Its 64-token N-tile leaves the headline shape
+// (6912 x 2560, N = 256) with 72 (384-row) tiles for 148 SMs: the K range is
+// split over a cluster pair and the int32 partials (48 KB per CTA) cross
+// distributed shared memory at ~8.5 B/clk each way (~3 us per launch).
+//
+// K1-32 halves the N-tile to 32 tokens (64-byte rows) and keeps every lookup
+// conflict-free by PAIRING groups: line p of pair jp holds row p of group
+// 2jp in bytes [0, 64) and row p of group 2jp+1 in bytes [64, 128) of one
+// 128-byte bank line.  A lookup thread reads, for its output row, row pos0
+// of group 2jp and row pos1 of group 2jp+1 (4 chunks each) in the order
+// chunk v = (lane & 7) ^ s, s = 0..7: v < 4 is a chunk of the first half
+// (group 2jp), v >= 4 of the second half (group 2jp+1), and the 8 lanes of an
+// LDS.128 phase always cover the 8 bank groups whatever rows they read.  For
+// lanes with (lane & 7) < 4 the first four steps read group 2jp; for the
+// others group 2jp+1 -- so steps 0..3 read line LA and steps 4..7 line LB,
+// (LA, LB) = (L0, L1) or (L1, L0) per lane.  Step s and s+4 land in the same
+// SWAR slot k = s & 3 (tokens of chunk (lane ^ k) & 3): 16 accumulator
+// registers instead of 32.  The same 2 bytes of shared memory per
+// lookup-add, the same half-table build share per row, twice the tiles: the
+// headline runs as 144 CTAs without split-K and without a DSMEM exchange.
+//
+// Everything else is K1's: builder warps stage index rows (one bulk copy)
+// and the activation tile (2-D TMA, box 32 x 16g) and build the half tables
+// along base-3 reflected Gray codes; one builder lane computes
+// two tokens of one group's half-table rows, the two halves of a warp the
+// two groups of a pair, so a warp-wide 4-byte store fills one bank line;
+// SWAR fields (T + 128 g) widen into TMEM int32 every 48 groups;
+// optional cluster split-K (DSMEM); fp32 epilogue
+// out = fl((float)acc * fl(a_scale[n] * w_scale)) through a swizzled shared
+// tile for coalesced 16-byte stores.
+#pragma once
+#include "vlut_kernel.cuh"
+
+namespace vlut {
+
+constexpr int kN32 = 32;  // tokens per CTA
+// mbarrier slots of K1-32 (byte offsets): FULL[NB], EMPTY[NB], STAGE[NB + 1]
+template <int NB>
+__device__ __forceinline__ constexpr int m32_full(int b) { return 8 * b; }
+template <int NB>
+__device__ __forceinline__ constexpr int m32_empty(int b) { return 8 * NB + 8 * b; }
+template <int NB>
+__device__ __forceinline__ constexpr int m32_stage(int s) { return 16 * NB + 8 * s; }
+
+template <int G>
+struct Cfg32 {
+  static constexpr int R = pow3(G);
+  static constexpr int ZERO = (R - 1) / 2;
+  static constexpr int HR = (R + 1) / 2;            // stored half-table positions
+#ifndef VLUT_K32_NBUF
+#define VLUT_K32_NBUF 3
+#endif
+  static constexpr int NBUF = (G == 4) ? VLUT_K32_NBUF : 2;  // table buffers
+  static constexpr int GS = (G == 4) ? 16 : 8;      // groups per sub-stage (even)
+  static constexpr int PAIRS = GS / 2;
+  static constexpr int SUBS = kKgTile / GS;
+  static constexpr int BIAS = 128 * G;
+  static constexpr int PAIR_BYTES = HR * 128;       // one bank line per position
+  static constexpr int TAB_BYTES = PAIRS * PAIR_BYTES;
+  static constexpr int A_ROWS = kKgTile * G;
+  static constexpr int A_BYTES = A_ROWS * kN32;     // 16g rows x 32 tokens
+  static constexpr int IDX_MASK = (G == 4) ? 0x7F : 0xFF;
+  // staging buffers: the builders (up to NBUF tables ahead) stage tile T+1
+  // while lookup warps may still be about to read tile T+1-STAGE's index
+  // rows -- STAGE >= NBUF + 1 (one sub-stage per tile at g = 4)
+  static constexpr int STAGE = NBUF + 1;
+  static_assert(STAGE * 8 + 16 * NBUF <= 96, "mbarrier region");
+  static_assert(kFlushTiles * kKgTile * 2 * BIAS <= 65535, "SWAR field overflow");
+};
+
+template <int G, int WARPS>
+struct Layout32 {
+  static constexpr int NLT = WARPS * 32;
+  static constexpr int THREADS = NLT + kBuilderWarps * 32;
+  static constexpr int BUILDER0 = NLT;
+  static constexpr int MCTA = NLT;
+  static constexpr int RED_BYTES = MCTA * kN32 * 4;   // int32 tile [row][32]
+  static constexpr int TMEM_COLS = 32 * ((WARPS + 3) / 4) <= 32 ? 32
+                                   : (32 * ((WARPS + 3) / 4) <= 64 ? 64 : 128);
+  static constexpr int TAB_REGION = Cfg32<G>::NBUF * Cfg32<G>::TAB_BYTES > RED_BYTES
+                                        ? Cfg32<G>::NBUF * Cfg32<G>::TAB_BYTES : RED_BYTES;
+  static constexpr int IDX_OFF = TAB_REGION;
+  static constexpr int IDX_BYTES = MCTA * 16;
+  static constexpr int A_OFF = IDX_OFF + Cfg32<G>::STAGE * IDX_BYTES;
+  static constexpr int MISC_OFF = A_OFF + Cfg32<G>::STAGE * Cfg32<G>::A_BYTES;
+  static constexpr int MBAR_OFF = MISC_OFF + 16;
+  static constexpr int SCALE_OFF = MBAR_OFF + 96;
+  static constexpr int SMEM = SCALE_OFF + kN32 * 4;
+  static constexpr int EPI_UNITS = (MCTA * 8 + THREADS - 1) / THREADS;  // 16-B units / thread
+  static_assert(WARPS <= 16, "TMEM: at most 4 column blocks of 32");
+};
+
+// ---------------------------------------------------------------- staging (a2)
+template <int G, int WARPS>
+__device__ __forceinline__ void stage32(const Params& p, int kt, int buf, int m0, int n0,
+                                        uint8_t* smem, int bt, uint32_t stg_mbar, bool do_idx,
+                                        bool do_act, bool arm) {
+  using C = Cfg32<G>;
+  using L = Layout32<G, WARPS>;
+  constexpr int NB = kBuilderWarps * 32;
+  const int idx_rows = max(0, min(L::MCTA, p.m_pad - m0));
+  const int k0 = kt * kKgTile * G;
+  uint8_t* idx_dst = smem + L::IDX_OFF + buf * L::IDX_BYTES;
+  uint8_t* a_dst = smem + L::A_OFF + buf * C::A_BYTES;
+  if (do_idx)  // rows past m_pad: zero (index 0 rows are never looked up by valid rows)
+    for (int i = idx_rows * 16 + bt * 16; i < L::MCTA * 16; i += NB * 16)
+      *reinterpret_cast<uint4*>(idx_dst + i) = make_uint4(0, 0, 0, 0);
+  if (bt < 32) {
+    if (arm && bt == 0)  // the A box always delivers 16g x 32 bytes (OOB zero-filled)
+      mbar_expect_tx(stg_mbar, (uint32_t)(idx_rows * 16 + C::A_BYTES));
+    __syncwarp();
+    if (do_idx && bt == 0 && idx_rows > 0)
+      bulk_g2s(smem_u32(idx_dst), p.payload + ((size_t)kt * p.m_pad + m0) * 16,
+               (uint32_t)(idx_rows * 16), stg_mbar);
+    if (do_act && bt == 0) tma_load_2d(smem_u32(a_dst), &p.a_map, n0, k0, stg_mbar);
+  }
+}
+
+// ---------------------------------------------------------------- table build (a3)
+// Builder warp bw builds pairs jp = bw, bw + 4, ... of the sub-stage: lanes
+// 0..15 the half table of group 2jp, lanes 16..31 of group 2jp+1, two tokens
+// per lane; position i of both lands in one 128-byte line (one wavefront per
+// warp-wide store).
+template <int G>
+__device__ __forceinline__ void build_tables32(uint32_t tab_s, uint32_t a_s, int grp0, int bw,
+                                               int lane) {
+  using C = Cfg32<G>;
+  constexpr uint32_t K1 = 0x00010001u;
+  constexpr uint32_t C128 = 128u * K1;
+  const int hf = lane >> 4, tl = lane & 15;
+#pragma unroll 1
+  for (int jp = bw; jp < C::PAIRS; jp += kBuilderWarps) {
+    const int jg = 2 * jp + hf;  // group within the sub-stage
+    uint32_t U[8], P[8], Mn[8];
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+      const uint32_t x = lds_u16(a_s + ((grp0 + jg) * G + r) * kN32 + 2 * tl);
+      U[r] = __byte_perm(x ^ 0x8080u, 0u, 0x4140);
+      P[r] = U[r] - C128;
+      Mn[r] = C128 - U[r];
+    }
+    const uint32_t row0 = tab_s + (uint32_t)(jp * C::PAIR_BYTES + hf * 64 + 4 * tl);
+    sts32(row0, (uint32_t)C::BIAS * K1);  // the zero pattern
+    build_blocks<G, 0>(row0, 0u, U, P, Mn);
+  }
+}
+
+// ---------------------------------------------------------------- lookups (a4)
+// Pairs [SUB*PAIRS, ...) of the K-tile.  PB pairs per load batch (8 LDS.128
+// each).  Slots k < NX negate by XOR (ALU pipe), k >= NX by multiply (FMA
+// pipe): the per-lane line selection adds ALU work, so fewer XOR slots than
+// K1 keep the two integer pipes balanced.
+#ifndef VLUT_K32_NX
+#define VLUT_K32_NX 1
+#endif
+constexpr int kNX32 = VLUT_K32_NX;
+template <int G, int PB>
+__device__ __forceinline__ void lookup_sub32(const int SUB, uint32_t tab, const uint32_t (&iwa)[4],
+                                             const uint32_t (&rot)[8], bool lo,
+                                             uint32_t (&sw)[4][4], int32_t& nneg) {
+  using C = Cfg32<G>;
+  static_assert(C::PAIRS % PB == 0, "pairs per batch");
+#pragma unroll
+  for (int jb = 0; jb < C::PAIRS; jb += PB) {
+    uint4 va[PB][4], vb[PB][4];
+    uint32_t ma[PB], mb[PB];
+#pragma unroll
+    for (int q = 0; q < PB; ++q) {
+      const int jp = jb + q;
+      const int b0 = SUB * C::GS + 2 * jp;  // even: b0, b0 + 1 in one index word
+      const uint32_t word = iwa[b0 >> 2];
+      const int i0 = (int)((word >> (8 * (b0 & 3))) & C::IDX_MASK);
+      const int i1 = (int)((word >> (8 * ((b0 + 1) & 3))) & C::IDX_MASK);
+      const int d0 = i0 - C::ZERO, d1 = i1 - C::ZERO;
+      const uint32_t m0 = (uint32_t)(d0 >> 31), m1 = (uint32_t)(d1 >> 31);
+      const uint32_t p0 = (uint32_t)((d0 ^ (int)m0) - (int)m0);
+      const uint32_t p1 = (uint32_t)((d1 ^ (int)m1) - (int)m1);
+      nneg += (int)m0 + (int)m1;
+      const uint32_t base = tab + (uint32_t)(jp * C::PAIR_BYTES);
+      const uint32_t l0 = base + p0 * 128u, l1 = base + p1 * 128u;
+      const uint32_t la = lo ? l0 : l1, lb = lo ? l1 : l0;
+      ma[q] = lo ? m0 : m1;
+      mb[q] = lo ? m1 : m0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {  // lines are 128-aligned: + == |
+        va[q][k] = lds128(la + rot[k]);
+        vb[q][k] = lds128(lb + rot[k + 4]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < PB; ++q) {
+      const uint32_t sa = ma[q] * 2u + 1u, sb = mb[q] * 2u + 1u;  // +1 / -1
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (k < kNX32) {
+          sw[k][0] += (va[q][k].x ^ ma[q]) + (vb[q][k].x ^ mb[q]);
+          sw[k][1] += (va[q][k].y ^ ma[q]) + (vb[q][k].y ^ mb[q]);
+          sw[k][2] += (va[q][k].z ^ ma[q]) + (vb[q][k].z ^ mb[q]);
+          sw[k][3] += (va[q][k].w ^ ma[q]) + (vb[q][k].w ^ mb[q]);
+        } else {
+          sw[k][0] += va[q][k].x * sa + vb[q][k].x * sb;
+          sw[k][1] += va[q][k].y * sa + vb[q][k].y * sb;
+          sw[k][2] += va[q][k].z * sa + vb[q][k].z * sb;
+          sw[k][3] += va[q][k].w * sa + vb[q][k].w * sb;
+        }
+      }
+    }
+  }
+}
+
+// Widen (INT16 -> INT32) the 4 slots into TMEM columns 8k .. 8k + 7.
+template <int G>
+__device__ __forceinline__ void flush32(uint32_t (&sw)[4][4], int32_t& nneg, uint32_t taddr,
+                                        bool first) {
+  constexpr uint32_t K1 = 0x00010001u;
+  const uint32_t cnt = (uint32_t)(-nneg);
+  const uint32_t corr_xor = cnt * (2u * Cfg32<G>::BIAS * K1 + 1u);
+  const uint32_t corr_mul = cnt * (2u * Cfg32<G>::BIAS * K1);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t v[16];
+    if (!first) {
+      tmem_ld16(taddr + 16 * h, v);
+      tmem_wait_ld();
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = 0;
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int k = 2 * h + e;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t w = sw[k][q] + (k < kNX32 ? corr_xor : corr_mul);
+        v[8 * e + 2 * q] += w & 0xFFFFu;
+        v[8 * e + 2 * q + 1] += w >> 16;
+        sw[k][q] = 0;
+      }
+    }
+    tmem_st16(taddr + 16 * h, v);
+  }
+  tmem_wait_st();
+  nneg = 0;
+}
+
+// ---------------------------------------------------------------- the kernel
+template <int G, int WARPS, bool ACC_ONLY>
+__global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
+    vlut_mpgemm32_kernel(const __grid_constant__ Params p) {
+  using C = Cfg32<G>;
+  using L = Layout32<G, WARPS>;
+#ifndef VLUT_K32_PB
+#define VLUT_K32_PB 2
+#endif
+  constexpr int PB = VLUT_K32_PB;  // pairs per load batch: 8 PB LDS.128 in flight
+  extern __shared__ __align__(1024) uint8_t smem[];
+  VLUT_STAMP(0);
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int rank = blockIdx.x;  // split index (== rank in cluster)
+  const int n0 = blockIdx.y * kN32;
+  const int m0 = blockIdx.z * L::MCTA;
+  const int S = p.splits;
+  const int kt_begin = (int)(((long long)rank * p.kg_tiles) / S);
+  const int kt_end = (int)(((long long)(rank + 1) * p.kg_tiles) / S);
+  const int ntiles = kt_end - kt_begin;
+  const int nsub = ntiles * C::SUBS;
+
+  const uint32_t tab_s = smem_u32(smem);
+  const uint32_t idx_s = smem_u32(smem + L::IDX_OFF);
+  const uint32_t a_s0 = smem_u32(smem + L::A_OFF);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::MISC_OFF);
+  float* scale_s = reinterpret_cast<float*>(smem + L::SCALE_OFF);
+  const uint32_t mbar = smem_u32(smem + L::MBAR_OFF);
+
+  if (tid == L::BUILDER0) {
+    for (int b = 0; b < C::NBUF; ++b) {
+      mbar_init(mbar + m32_full<C::NBUF>(b), kBuilderWarps);
+      mbar_init(mbar + m32_empty<C::NBUF>(b), WARPS);
+    }
+    for (int st = 0; st < C::STAGE; ++st) mbar_init(mbar + m32_stage<C::NBUF>(st), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  uint32_t tmem_base = 0;
+  if (warp >= WARPS) {
+    // =========================== builders: staging + table builds
+    const int bt = tid - L::BUILDER0;
+    const int bw = warp - WARPS;
+    if (ntiles > 0) {
+      // weights are not an output of the previous kernel (vlut.h): tile 0's
+      // index rows before griddepcontrol.wait, its activations after
+      stage32<G, WARPS>(p, kt_begin, 0, m0, n0, smem, bt, mbar + m32_stage<C::NBUF>(0), true, false, true);
+      pdl_wait();
+      stage32<G, WARPS>(p, kt_begin, 0, m0, n0, smem, bt, mbar + m32_stage<C::NBUF>(0), false, true, false);
+    } else {
+      pdl_wait();
+    }
+    if (!ACC_ONLY && bt < kN32) {
+      const int n = n0 + bt;
+      scale_s[bt] = (n < p.N) ? __fmul_rn(__ldg(p.a_scale + n), p.w_scale) : 0.f;
+    }
+#pragma unroll 1
+    for (int u = 0; u < nsub + C::NBUF; ++u) {
+      if (u >= C::NBUF) mbar_wait(mbar + m32_empty<C::NBUF>(u % C::NBUF), ((u / C::NBUF) - 1) & 1);
+      if (u >= nsub) continue;
+      const int T = u / C::SUBS, sub = u - T * C::SUBS;
+      if (sub == 0) {
+        if (T + 1 < ntiles) {
+          const int b1 = (T + 1) % C::STAGE;
+          stage32<G, WARPS>(p, kt_begin + T + 1, b1, m0, n0, smem, bt, mbar + m32_stage<C::NBUF>(b1), true,
+                            true, true);
+        }
+        mbar_wait(mbar + m32_stage<C::NBUF>(T % C::STAGE), (T / C::STAGE) & 1);
+        bar_sync(5, kBuilderWarps * 32);  // tile T's rows visible to all builders
+      }
+      build_tables32<G>(tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES),
+                        a_s0 + (uint32_t)((T % C::STAGE) * C::A_BYTES), sub * C::GS, bw, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(mbar + m32_full<C::NBUF>(u % C::NBUF));
+    }
+  } else {
+    // =========================== lookup warps: one output row per thread
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(L::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    tmem_fence_before();
+    bar_sync(6, L::MCTA);
+    tmem_fence_after();
+    tmem_base = *tmem_slot;
+    VLUT_STAMP(1);
+    uint32_t rot[8];  // chunk (lane & 7) ^ s of a 128-byte line
+#pragma unroll
+    for (int s = 0; s < 8; ++s) rot[s] = (uint32_t)((((lane & 7) ^ s) & 7) * 16);
+    const bool lo = (lane & 4) == 0;
+    const uint32_t taddr =
+        tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(32 * (warp >> 2));
+    uint32_t sw[4][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sw[k][q] = 0;
+    int32_t nneg = 0;
+    bool first = true;
+    int since_flush = warp % kFlushTiles;
+    uint32_t iwa[4] = {0u, 0u, 0u, 0u};
+#pragma unroll 1
+    for (int t = 0; t < ntiles; ++t) {
+#pragma unroll
+      for (int sub = 0; sub < C::SUBS; ++sub) {
+        const int u = t * C::SUBS + sub;
+        mbar_wait(mbar + m32_full<C::NBUF>(u % C::NBUF), (u / C::NBUF) & 1);
+        if (u == 0) VLUT_STAMP(2);
+        if (sub == 0) {
+          const uint4 iw = lds128(idx_s + (uint32_t)((t % C::STAGE) * L::IDX_BYTES + tid * 16));
+          iwa[0] = iw.x; iwa[1] = iw.y; iwa[2] = iw.z; iwa[3] = iw.w;
+        }
+        lookup_sub32<G, PB>(sub, tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES), iwa, rot, lo,
+                            sw, nneg);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(mbar + m32_empty<C::NBUF>(u % C::NBUF));
+      }
+      if (++since_flush >= kFlushTiles || t + 1 == ntiles) {
+        since_flush = 0;
+        flush32<G>(sw, nneg, taddr, first);
+        first = false;
+      }
+    }
+    pdl_wait();  // (no-op by now) formally orders the epilogue's a_scale reads
+  }
+  pdl_launch_dependents();
+
+  VLUT_STAMP(3);
+  // ---- int32 tile -> shared (a5): row r = 128 bytes = 8 units of 4 tokens;
+  // unit u of row r stored at position u ^ (r & 7) (conflict-free for the
+  // lane-per-row writes here and the 8-threads-per-row reads below)
+  const int rows_per = ((L::MCTA + S - 1) / S + 3) & ~3;
+  tmem_fence_before();
+  __syncthreads();  // every table read done before the region is reused
+  tmem_fence_after();
+  if (warp < WARPS) {
+    const uint32_t taddr =
+        tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(32 * (warp >> 2));
+    const int32_t bias_total = C::BIAS * kKgTile * ntiles;
+    const int r = tid;
+    uint32_t v[2][16];
+    if (ntiles > 0) {
+      tmem_ld16(taddr, v[0]);
+      tmem_ld16(taddr + 16, v[1]);
+      tmem_wait_ld();
+    } else {
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[h][i] = 0;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int k = 2 * h + e;
+        const uint32_t c = (uint32_t)((lane ^ k) & 3);  // tokens 8c .. 8c+7 (units 2c, 2c+1)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const uint32_t uu = (2 * c + hh) ^ (uint32_t)(r & 7);
+          const uint32_t* x = v[h] + 8 * e + 4 * hh;
+          sts128(tab_s + (uint32_t)(r * 128) + uu * 16, x[0] - bias_total, x[1] - bias_total,
+                 x[2] - bias_total, x[3] - bias_total);
+        }
+      }
+    }
+  }
+  VLUT_STAMP(4);
+  tmem_fence_before();
+  cg::cluster_group cluster = cg::this_cluster();
+  if (S > 1) cluster.sync(); else __syncthreads();
+  VLUT_STAMP(5);
+  if (warp == 0) {
+    tmem_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
+                 "n"(L::TMEM_COLS)
+                 : "memory");
+  }
+
+  // ---- reduce across the cluster + epilogue (a5, a6): unit e = row
+  // r_begin + e / 8, tokens 4 (e % 8) .. + 3; eight consecutive threads store
+  // one row's 128 bytes
+  {
+    const int r_begin = min(L::MCTA, rank * rows_per);
+    const int my_rows = min(rows_per, L::MCTA - r_begin);
+    const int units = my_rows * 8;
+    const int4* red_local = reinterpret_cast<const int4*>(smem);
+    auto tile_off = [&](int e) -> int {
+      const int r = r_begin + (e >> 3);
+      return r * 8 + ((e & 7) ^ (r & 7));
+    };
+    constexpr int CH = L::EPI_UNITS;
+    int4 acc4[CH];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const int e = tid + i * L::THREADS;
+      acc4[i] = make_int4(0, 0, 0, 0);
+      if (e < units) acc4[i] = red_local[tile_off(e)];
+    }
+    for (int q = 1; q < S; ++q) {
+      const int4* rem = cluster.map_shared_rank(red_local, (rank + q) % S);
+      int4 w4[CH];
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {
+        const int e = tid + i * L::THREADS;
+        w4[i] = make_int4(0, 0, 0, 0);
+        if (e < units) w4[i] = rem[tile_off(e)];
+      }
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {
+        acc4[i].x += w4[i].x; acc4[i].y += w4[i].y; acc4[i].z += w4[i].z; acc4[i].w += w4[i].w;
+      }
+    }
+    if (S > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const int e = tid + i * L::THREADS;
+      if (e >= units) continue;
+      const int u = e & 7;
+      const int m = m0 + r_begin + (e >> 3);
+      const int n = n0 + 4 * u;
+      if (m >= p.M || n >= p.N) continue;  // N % 16 == 0: a unit is all-in or all-out
+      if constexpr (ACC_ONLY) {
+        *reinterpret_cast<int4*>(reinterpret_cast<int32_t*>(p.out) + (size_t)m * p.N + n) = acc4[i];
+      } else {
+        const int vv[4] = {acc4[i].x, acc4[i].y, acc4[i].z, acc4[i].w};
+        float f[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) f[k] = __fmul_rn((float)vv[k], scale_s[4 * u + k]);
+        *reinterpret_cast<float4*>(p.out + (size_t)m * p.N + n) = make_float4(f[0], f[1], f[2], f[3]);
+      }
+    }
+  }
+  VLUT_STAMP(7);
+  if (S > 1) asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+}
+
+}  // namespace vlut

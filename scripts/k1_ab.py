@@ -20,12 +20,19 @@ SHAPES = [  # (M, K, N, g, plan-name)
     (6912, 2560, 2048, 4, "auto"), (3840, 2560, 2048, 4, "auto"), (2560, 6912, 2048, 4, "auto"),
 ]
 PLANS = {"auto": None, "c12x2": (12, 2, 0, 0), "w12r2": (12, 1, 768, 1), "w8r2": (8, 1, 512, 1),
-         "w8r3": (8, 1, 768, 1), "w16r1": (16, 1, 0, 1), "w12r1": (12, 1, 0, 1)}
+         "w8r3": (8, 1, 768, 1), "w16r1": (16, 1, 0, 1), "w12r1": (12, 1, 0, 1),
+         "n32w12": (12, 1, 0, 0, 32), "n32w16": (16, 1, 0, 0, 32), "n32w8": (8, 1, 0, 0, 32),
+         "n32w12s2": (12, 2, 0, 0, 32), "n32w16s2": (16, 2, 0, 0, 32), "n32w8s2": (8, 2, 0, 0, 32),
+         "n32w12s4": (12, 4, 0, 0, 32)}
 
 
 def main():
     libs = sys.argv[1:] or [""]
-    if os.environ.get("K1AB_PLANS"):
+    if os.environ.get("K1AB_SHAPES"):
+        # "M,K,N,g,plan;M,K,N,g,plan;..."
+        shapes = [tuple(int(x) for x in t.split(",")[:4]) + (t.split(",")[4],)
+                  for t in os.environ["K1AB_SHAPES"].split(";")]
+    elif os.environ.get("K1AB_PLANS"):
         keep = set(os.environ["K1AB_PLANS"].split(","))
         shapes = [s for s in SHAPES if s[4] in keep]
     else:
@@ -46,7 +53,8 @@ def main():
             v._lib = None
             ws = torch.zeros(int(v.lib().vlut_workspace_bytes()), dtype=torch.uint8, device=dev)
             pl = PLANS[pn]
-            plan = None if pl is None else v.LaunchPlan(pl[0], pl[1], m_cta=pl[2], streamk=pl[3])
+            plan = None if pl is None else v.LaunchPlan(pl[0], pl[1], m_cta=pl[2], streamk=pl[3],
+                                                         n_cta=pl[4] if len(pl) > 4 else 64)
             run = lambda: v.mpgemm_ws(pw, A, s, 0.02, out=out, plan=plan, ws=ws)
             try:
                 for _ in range(3):

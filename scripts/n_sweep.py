@@ -15,7 +15,7 @@ W = torch.from_numpy(synth.ternary_weights(M, K, 2000, 0.4)).to(dev)
 pws = [v.pack_weights_device(W, g) for _ in range(60)]
 ws = v.workspace(dev)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-for N in (1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096):
+for N in (1, 2, 4, 8, 16, 32, 48, 64, 80, 96, 112, 128, 160, 192, 256, 512, 1024, 2048, 4096):
     A = torch.randint(-127, 128, (K, N), dtype=torch.int8, device=dev)
     s = torch.rand(N, device=dev) * 0.01 + 1e-3
     out = torch.empty((M, N), device=dev)
@@ -46,6 +46,6 @@ for N in (1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096):
     roof = max(lk / R_LU, hb / HBM)
     pl = v.plan_ws(M, K, N, g)
     kern = (f"K2 tpw={pl.tpw} nw={pl.nw} S={pl.splits}" if pl.slot else
-            f"K1 w{pl.warps} m{pl.m_cta} S={pl.splits} sk={pl.streamk}")
+            f"K1 w{pl.warps} m{pl.m_cta} n{pl.n_cta} S={pl.splits} sk={pl.streamk}")
     print(f"N={N:5d} {kern:28s} {t * 1e6:9.2f} us  {N / t / 1e6:8.3f} M tok/s  "
           f"frac {roof / t:.3f} ({'hbm' if hb / HBM > lk / R_LU else 'smem'})", flush=True)

@@ -172,6 +172,58 @@ def test_mpgemm_acc_every_plan(v, g, warps, splits):
     assert np.array_equal(acc.cpu().numpy(), oracle.gemm_i32(W, A))
 
 
+# ------------------------------------------------------------------ K1-32 (32-token tiles)
+SHAPES32 = [
+    # (M, K, N, g) -- N % 16 == 0 (TMA staging); 16-token N tails, M / K tails
+    (1, 4, 16, 4), (33, 68, 48, 4), (385, 1024, 144, 4), (520, 1280, 32, 4), (1000, 260, 256, 4),
+    (5, 5, 16, 5), (129, 640, 80, 5), (400, 1280, 112, 5), (777, 2560, 208, 5),
+]
+
+
+@pytest.mark.parametrize("M,K,N,g", SHAPES32)
+@pytest.mark.parametrize("warps,splits", [(12, 1), (16, 1), (8, 1), (12, 2), (16, 3), (8, 5)])
+def test_mpgemm32_acc_and_fp32(v, M, K, N, g, warps, splits):
+    """K1-32 (paired-group tables, 32-token tiles): int32 accumulators
+    bit-exact, fp32 bit-identical to the oracle's fixed-order dequant, for
+    every warp count and cluster split (ragged split ranges included)."""
+    W = synth.ternary_weights(M, K, seed=5 * M + K)
+    A = synth.int8_activations(K, N, seed=N + 29)  # full int8 range incl. -128
+    s = synth.token_scales(N, seed=N)
+    pw = v.pack_weights(W, g, device=dev())
+    plan = v.LaunchPlan(warps, splits, n_cta=32)
+    acc = v.mpgemm_acc(pw, to_dev(A), plan=plan)
+    out = v.mpgemm_ex(pw, to_dev(A), to_dev(s), synth.W_SCALE, plan=plan)
+    torch.cuda.synchronize()
+    ref = oracle.gemm_i32(W, A)
+    assert np.array_equal(acc.cpu().numpy(), ref)
+    check_fp32(out.cpu().numpy(), ref, s, synth.W_SCALE)
+
+
+@pytest.mark.parametrize("g", [4, 5])
+def test_mpgemm32_adversarial_extremes(v, g):
+    M, K, N = 64, 23040, 64
+    W = np.ones((M, K), np.int8)
+    W[1::2] = -1
+    W[2::4] = 0
+    A = np.full((K, N), -128, np.int8)
+    A[:, 1::2] = 127
+    A[:, 2::4] = 0
+    pw = v.pack_weights(W, g, device=dev())
+    acc = v.mpgemm_acc(pw, to_dev(A), plan=v.LaunchPlan(12, 1, n_cta=32)).cpu().numpy()
+    ref = oracle.gemm_i32(W, A)
+    assert np.array_equal(acc, ref)
+
+
+def test_mpgemm32_rejects_unsupported(v):
+    """32-token tiles need N % 16 == 0 and the plain epilogue."""
+    M, K, g = 64, 64, 4
+    pw = v.pack_weights(synth.ternary_weights(M, K, seed=1), g, device=dev())
+    A = to_dev(synth.int8_activations(K, 24, seed=2))
+    with pytest.raises(v.VlutError) as e:
+        v.mpgemm_acc(pw, A, plan=v.LaunchPlan(12, 1, n_cta=32))
+    assert e.value.name == "VLUT_ERR_UNSUPPORTED"
+
+
 @pytest.mark.parametrize("g", [4, 5])
 def test_mpgemm_adversarial_extremes(v, g):
     # |acc| up to 128 * K: all +1 weights against all -128 / +127 activations,
