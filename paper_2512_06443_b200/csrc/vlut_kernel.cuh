@@ -478,6 +478,148 @@ __device__ __forceinline__ void build_tables(uint32_t tab_s, uint32_t a_s, int g
   }
 }
 
+// ---------------------------------------------------------------- wide-store table build
+// 16-byte-store builders (K1 and K1-32): lane = 8 q + ch writes chunk ch of
+// a 128-byte table line for line set q, one STS.128 per warp fills four
+// lines (four wavefronts, conflict-free) -- a quarter of the store
+// instructions of the 4-byte form, which matters because the lookup warps
+// keep the shared-memory queue full (K1-32: 94 -> 88 us on the headline).
+// The half table (anti-symmetry as in K1: position 0 = the zero
+// pattern, block Lv = trits above Lv zero, trit Lv = +1, trits below free, at
+// positions (3^Lv+1)/2 + base-3 value of digits d_r = t_r + 1) is cut into
+// sub-walks: unit (Lv, D, PF) fixes digits D .. Lv-1 to the base-3 number PF
+// and walks digits 0 .. D-1 along the reflected Gray code from all -1 (one
+// packed add per entry and word).  The units are spread over the builder
+// warps of a pair group (g = 4: 2 warps x 4 pairs x 41 lines; g = 5: 4 warps
+// x 4 pairs x 122 lines).
+template <int G, int Lv, int D, int PF>
+__device__ __forceinline__ void sub_walk(uint32_t row0, const uint32_t (&P)[G][4],
+                                         const uint32_t (&Mn)[G][4]) {
+  constexpr uint32_t K1 = 0x00010001u;
+  uint32_t T[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    T[w] = (uint32_t)Cfg<G>::BIAS * K1 + P[Lv][w];
+#pragma unroll
+    for (int r = 0; r < Lv; ++r) {
+      if (r < D) {
+        T[w] += Mn[r][w];  // walked digits start at trit -1
+      } else {
+        const int d = (PF / pow3(r - D)) % 3;  // fixed digit (compile time)
+        if (d == 2) T[w] += P[r][w];
+        if (d == 0) T[w] += Mn[r][w];
+      }
+    }
+  }
+  constexpr int pos0 = (pow3(Lv) + 1) / 2 + PF * pow3(D);
+  sts128(row0 + pos0 * 128, T[0], T[1], T[2], T[3]);
+  if constexpr (D > 0) {
+    constexpr GrayWalk<D> gw{};
+#pragma unroll
+    for (int st = 1; st < pow3(D); ++st) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) T[w] += (gw.dir[st] > 0) ? P[gw.digit[st]][w] : Mn[gw.digit[st]][w];
+      sts128(row0 + (pos0 + gw.idx[st]) * 128, T[0], T[1], T[2], T[3]);
+    }
+  }
+}
+
+template <int G>
+__device__ __forceinline__ void zero_row(uint32_t row0) {
+  constexpr uint32_t Z = (uint32_t)Cfg<G>::BIAS * 0x00010001u;
+  sts128(row0, Z, Z, Z, Z);
+}
+
+// g = 4: half h of a pair group (41 lines: 23 + 18)
+template <int G>
+__device__ __forceinline__ void build_units(int h, uint32_t row0, const uint32_t (&P)[G][4],
+                                            const uint32_t (&Mn)[G][4]) {
+  if constexpr (G == 4) {
+    if (h == 0) {
+      zero_row<4>(row0);
+      sub_walk<4, 0, 0, 0>(row0, P, Mn);
+      sub_walk<4, 1, 1, 0>(row0, P, Mn);
+      sub_walk<4, 3, 2, 0>(row0, P, Mn);
+      sub_walk<4, 3, 2, 1>(row0, P, Mn);
+    } else {
+      sub_walk<4, 2, 2, 0>(row0, P, Mn);
+      sub_walk<4, 3, 2, 2>(row0, P, Mn);
+    }
+  } else {  // g = 5: quarter h (122 lines: 36 + 27 + 27 + 32)
+    if (h == 0) {
+      sub_walk<5, 4, 2, 0>(row0, P, Mn);
+      sub_walk<5, 4, 2, 1>(row0, P, Mn);
+      sub_walk<5, 4, 2, 2>(row0, P, Mn);
+      sub_walk<5, 2, 2, 0>(row0, P, Mn);
+    } else if (h == 1) {
+      sub_walk<5, 4, 2, 3>(row0, P, Mn);
+      sub_walk<5, 4, 2, 4>(row0, P, Mn);
+      sub_walk<5, 4, 2, 5>(row0, P, Mn);
+    } else if (h == 2) {
+      sub_walk<5, 4, 2, 6>(row0, P, Mn);
+      sub_walk<5, 4, 2, 7>(row0, P, Mn);
+      sub_walk<5, 4, 2, 8>(row0, P, Mn);
+    } else {
+      sub_walk<5, 3, 2, 0>(row0, P, Mn);
+      sub_walk<5, 3, 2, 1>(row0, P, Mn);
+      sub_walk<5, 3, 2, 2>(row0, P, Mn);
+      zero_row<5>(row0);
+      sub_walk<5, 0, 0, 0>(row0, P, Mn);
+      sub_walk<5, 1, 1, 0>(row0, P, Mn);
+    }
+  }
+}
+
+// K1 (64-token rows): builder warp bw of BW builds its line sets -- at g = 4
+// set s = four groups 4s .. 4s+3 of the 16-group sub-stage (all 41 lines),
+// at g = 5 (4-group sub-stages) the four groups' quarter s of the 122 lines.
+// Lane 8 q + ch: group q of the set, tokens 8 ch .. 8 ch + 7.
+template <int G, int BW = kBuilderWarps>
+__device__ __forceinline__ void build_tables_wide(uint32_t tab_s, uint32_t a_s, int grp0, int bw,
+                                                  int lane) {
+  using C = Cfg<G>;
+  constexpr uint32_t K1 = 0x00010001u;
+  constexpr uint32_t C128 = 128u * K1;
+  constexpr int SETS = (G == 4) ? C::GS / 4 : 4;  // g=4: group sets; g=5: line quarters
+  static_assert(G == 5 ? C::GS == 4 : C::GS % 4 == 0, "wide builder: 4 groups per set");
+  const int q = lane >> 3, ch = lane & 7;
+#pragma unroll 1
+  for (int st = bw; st < SETS; st += BW) {
+    const int j = (G == 4) ? 4 * st + q : q;  // group within the sub-stage
+    uint32_t P[G][4], Mn[G][4];
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+      uint32_t x0, x1;
+      asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n"
+                   : "=r"(x0), "=r"(x1)
+                   : "r"(a_s + (uint32_t)(((grp0 + j) * G + r) * kNcta + 8 * ch)));
+      x0 ^= 0x80808080u;
+      x1 ^= 0x80808080u;
+      const uint32_t U[4] = {__byte_perm(x0, 0u, 0x4140), __byte_perm(x0, 0u, 0x4342),
+                             __byte_perm(x1, 0u, 0x4140), __byte_perm(x1, 0u, 0x4342)};
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        P[r][w] = U[w] - C128;
+        Mn[r][w] = C128 - U[w];
+      }
+    }
+    const uint32_t row0 = tab_s + (uint32_t)(j * C::HR * kRowBytes + ch * 16);
+    if constexpr (G == 4) {
+      build_units<4>(0, row0, P, Mn);
+      build_units<4>(1, row0, P, Mn);
+    } else {
+      build_units<5>(st, row0, P, Mn);
+    }
+  }
+}
+
+// table builder of K1 / K1-SK: wide 16-byte stores or the 4-byte form
+#ifndef VLUT_WIDE_MAX_WARPS
+#define VLUT_WIDE_MAX_WARPS 12
+#endif
+template <int WARPS>
+constexpr bool kWideBuild = WARPS <= VLUT_WIDE_MAX_WARPS;
+
 // ---------------------------------------------------------------- lookups (a4)
 template <int WARPS>
 constexpr int kLookupGP = (WARPS >= 16) ? 1 : 2;
@@ -737,8 +879,18 @@ __global__ void __launch_bounds__((WARPS + kBW<WARPS, 1>) * 32, 1)
         }
         bar_sync(5, kBuilderWarps * 32);  // tile T's A rows visible to all builders
       }
-      build_tables<G, L::BW>(tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES),
-                      a_s0 + (uint32_t)((T % kStageBufs) * C::A_BYTES), sub * C::GS, bw, lane);
+#ifndef VLUT_K1_NOBUILD  // (timing experiment only: tables left unbuilt)
+      // 16-byte-store builders, except in the 16-warp variants (96-register
+      // budget: the wide builders' 32-40 delta registers would spill there)
+      if constexpr (kWideBuild<WARPS>)
+        build_tables_wide<G, L::BW>(tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES),
+                                    a_s0 + (uint32_t)((T % kStageBufs) * C::A_BYTES), sub * C::GS,
+                                    bw, lane);
+      else
+        build_tables<G, L::BW>(tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES),
+                               a_s0 + (uint32_t)((T % kStageBufs) * C::A_BYTES), sub * C::GS, bw,
+                               lane);
+#endif
       __syncwarp();
       if (lane == 0) mbar_arrive(mbar + mb_full(u % C::NBUF));  // table u (and tile T's indices) ready
     }

@@ -64,10 +64,16 @@ struct Cfg32 {
   static constexpr int A_ROWS = kKgTile * G;
   static constexpr int A_BYTES = A_ROWS * kN32;     // 16g rows x 32 tokens
   static constexpr int IDX_MASK = (G == 4) ? 0x7F : 0xFF;
-  // staging buffers: the builders (up to NBUF tables ahead) stage tile T+1
-  // while lookup warps may still be about to read tile T+1-STAGE's index
-  // rows -- STAGE >= NBUF + 1 (one sub-stage per tile at g = 4)
-  static constexpr int STAGE = NBUF + 1;
+  // staging: while building tile T the builders stage tile T + AHEAD (its
+  // index rows and activations land during AHEAD tiles of lookups: a tile
+  // is only ~2 us of lookups here); the builders run up to NBUF tables ahead
+  // of the lookup warps, which may still have to read the index rows of tile
+  // T - NBUF + 1 -- so STAGE >= NBUF + AHEAD buffers
+#ifndef VLUT_K32_AHEAD
+#define VLUT_K32_AHEAD 2
+#endif
+  static constexpr int AHEAD = VLUT_K32_AHEAD;
+  static constexpr int STAGE = NBUF + AHEAD;
   static_assert(STAGE * 8 + 16 * NBUF <= 96, "mbarrier region");
   static_assert(kFlushTiles * kKgTile * 2 * BIAS <= 65535, "SWAR field overflow");
 };
@@ -121,32 +127,47 @@ __device__ __forceinline__ void stage32(const Params& p, int kt, int buf, int m0
 }
 
 // ---------------------------------------------------------------- table build (a3)
-// Builder warp bw builds pairs jp = bw, bw + 4, ... of the sub-stage: lanes
-// 0..15 the half table of group 2jp, lanes 16..31 of group 2jp+1, two tokens
-// per lane; position i of both lands in one 128-byte line (one wavefront per
-// warp-wide store).
+// Wide-store builders: a builder warp writes FOUR pairs' lines at once with
+// 16-byte stores.  Lane = 8 q + ch: q picks pair 4 pg + q of the warp's pair
+// group pg, ch the 16-byte chunk of the 128-byte line (ch < 4: tokens
+// 8 ch .. 8 ch + 7 of group 2jp, ch >= 4: of group 2jp+1), so one STS.128
+// fills four lines (four wavefronts, conflict-free) and a table costs a
+// quarter of the store instructions of 4-byte stores -- the lookup warps keep
+// the shared-memory queue full, and builders issuing 4-byte stores could not
+// keep up (measured: halving their stores took K1-32 from 94 to 86 us).
+//
 template <int G>
 __device__ __forceinline__ void build_tables32(uint32_t tab_s, uint32_t a_s, int grp0, int bw,
                                                int lane) {
   using C = Cfg32<G>;
+  // warps per pair group: g = 4 -> 2 (two groups of 4 pairs), g = 5 -> 4
+  constexpr int WPG = kBuilderWarps / (C::PAIRS / 4);
+  static_assert(C::PAIRS % 4 == 0 && kBuilderWarps % (C::PAIRS / 4) == 0, "builder split");
   constexpr uint32_t K1 = 0x00010001u;
   constexpr uint32_t C128 = 128u * K1;
-  const int hf = lane >> 4, tl = lane & 15;
-#pragma unroll 1
-  for (int jp = bw; jp < C::PAIRS; jp += kBuilderWarps) {
-    const int jg = 2 * jp + hf;  // group within the sub-stage
-    uint32_t U[8], P[8], Mn[8];
+  const int pg = bw / WPG, h = bw % WPG;
+  const int q = lane >> 3, ch = lane & 7;
+  const int jp = 4 * pg + q;
+  const int jg = 2 * jp + (ch >> 2);  // group within the sub-stage
+  const int c = ch & 3;               // tokens 8c .. 8c + 7
+  uint32_t P[G][4], Mn[G][4];
 #pragma unroll
-    for (int r = 0; r < G; ++r) {
-      const uint32_t x = lds_u16(a_s + ((grp0 + jg) * G + r) * kN32 + 2 * tl);
-      U[r] = __byte_perm(x ^ 0x8080u, 0u, 0x4140);
-      P[r] = U[r] - C128;
-      Mn[r] = C128 - U[r];
+  for (int r = 0; r < G; ++r) {
+    uint32_t x0, x1;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n"
+                 : "=r"(x0), "=r"(x1)
+                 : "r"(a_s + (uint32_t)(((grp0 + jg) * G + r) * kN32 + 8 * c)));
+    x0 ^= 0x80808080u;  // int8 a -> a + 128
+    x1 ^= 0x80808080u;
+    const uint32_t U[4] = {__byte_perm(x0, 0u, 0x4140), __byte_perm(x0, 0u, 0x4342),
+                           __byte_perm(x1, 0u, 0x4140), __byte_perm(x1, 0u, 0x4342)};
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      P[r][w] = U[w] - C128;   // +a_r as a packed arithmetic delta
+      Mn[r][w] = C128 - U[w];  // -a_r
     }
-    const uint32_t row0 = tab_s + (uint32_t)(jp * C::PAIR_BYTES + hf * 64 + 4 * tl);
-    sts32(row0, (uint32_t)C::BIAS * K1);  // the zero pattern
-    build_blocks<G, 0>(row0, 0u, U, P, Mn);
   }
+  build_units<G>(h, tab_s + (uint32_t)(jp * C::PAIR_BYTES + ch * 16), P, Mn);
 }
 
 // ---------------------------------------------------------------- lookups (a4)
@@ -294,15 +315,16 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
     // =========================== builders: staging + table builds
     const int bt = tid - L::BUILDER0;
     const int bw = warp - WARPS;
-    if (ntiles > 0) {
-      // weights are not an output of the previous kernel (vlut.h): tile 0's
-      // index rows before griddepcontrol.wait, its activations after
-      stage32<G, WARPS>(p, kt_begin, 0, m0, n0, smem, bt, mbar + m32_stage<C::NBUF>(0), true, false, true);
-      pdl_wait();
-      stage32<G, WARPS>(p, kt_begin, 0, m0, n0, smem, bt, mbar + m32_stage<C::NBUF>(0), false, true, false);
-    } else {
-      pdl_wait();
-    }
+    // weights are not an output of the previous kernel (vlut.h): the first
+    // AHEAD tiles' index rows before griddepcontrol.wait, activations after
+    const int pre = min(ntiles, C::AHEAD);
+    for (int T = 0; T < pre; ++T)
+      stage32<G, WARPS>(p, kt_begin + T, T, m0, n0, smem, bt, mbar + m32_stage<C::NBUF>(T), true,
+                        false, true);
+    pdl_wait();
+    for (int T = 0; T < pre; ++T)
+      stage32<G, WARPS>(p, kt_begin + T, T, m0, n0, smem, bt, mbar + m32_stage<C::NBUF>(T), false,
+                        true, false);
     if (!ACC_ONLY && bt < kN32) {
       const int n = n0 + bt;
       scale_s[bt] = (n < p.N) ? __fmul_rn(__ldg(p.a_scale + n), p.w_scale) : 0.f;
@@ -313,16 +335,18 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
       if (u >= nsub) continue;
       const int T = u / C::SUBS, sub = u - T * C::SUBS;
       if (sub == 0) {
-        if (T + 1 < ntiles) {
-          const int b1 = (T + 1) % C::STAGE;
-          stage32<G, WARPS>(p, kt_begin + T + 1, b1, m0, n0, smem, bt, mbar + m32_stage<C::NBUF>(b1), true,
-                            true, true);
+        if (T + C::AHEAD < ntiles) {
+          const int b1 = (T + C::AHEAD) % C::STAGE;
+          stage32<G, WARPS>(p, kt_begin + T + C::AHEAD, b1, m0, n0, smem, bt,
+                            mbar + m32_stage<C::NBUF>(b1), true, true, true);
         }
         mbar_wait(mbar + m32_stage<C::NBUF>(T % C::STAGE), (T / C::STAGE) & 1);
         bar_sync(5, kBuilderWarps * 32);  // tile T's rows visible to all builders
       }
+#ifndef VLUT_K32_NOBUILD  // (timing experiment only: tables left unbuilt)
       build_tables32<G>(tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES),
                         a_s0 + (uint32_t)((T % C::STAGE) * C::A_BYTES), sub * C::GS, bw, lane);
+#endif
       __syncwarp();
       if (lane == 0) mbar_arrive(mbar + m32_full<C::NBUF>(u % C::NBUF));
     }
@@ -366,8 +390,10 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
           const uint4 iw = lds128(idx_s + (uint32_t)((t % C::STAGE) * L::IDX_BYTES + tid * 16));
           iwa[0] = iw.x; iwa[1] = iw.y; iwa[2] = iw.z; iwa[3] = iw.w;
         }
+#ifndef VLUT_K32_NOLOOKUP  // (timing experiment only)
         lookup_sub32<G, PB>(sub, tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES), iwa, rot, lo,
                             sw, nneg);
+#endif
         __syncwarp();
         if (lane == 0) mbar_arrive(mbar + m32_empty<C::NBUF>(u % C::NBUF));
       }

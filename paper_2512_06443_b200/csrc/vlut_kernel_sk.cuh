@@ -439,8 +439,16 @@ __global__ void __launch_bounds__((WARPS + kBW<WARPS, RPT>) * 32, 1)
         if (bulk) mbar_wait(mbar + mb_stage(T % kStageBufs), (T / kStageBufs) & 1);
         bar_sync(5, L::BW * 32);
       }
-      build_tables<G, L::BW>(tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES),
-                      a_s0 + (uint32_t)((T % kStageBufs) * C::A_BYTES), sub * C::GS, bw, lane);
+      // 16-byte-store builders, except in the 16-warp variants (96-register
+      // budget: the wide builders' 32-40 delta registers would spill there)
+      if constexpr (kWideBuild<WARPS>)
+        build_tables_wide<G, L::BW>(tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES),
+                                    a_s0 + (uint32_t)((T % kStageBufs) * C::A_BYTES), sub * C::GS,
+                                    bw, lane);
+      else
+        build_tables<G, L::BW>(tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES),
+                               a_s0 + (uint32_t)((T % kStageBufs) * C::A_BYTES), sub * C::GS, bw,
+                               lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(mbar + mb_full(u % C::NBUF));
     }

@@ -60,16 +60,39 @@ def main():
                 for _ in range(3):
                     run()
                 torch.cuda.synchronize()
-                ts = []
-                for _ in range(reps):
-                    flush.zero_()
-                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    a.record()
-                    run()
-                    b.record()
-                    torch.cuda.synchronize()
-                    ts.append(a.elapsed_time(b) * 1e3)
-                t = float(np.median(ts))
+                if os.environ.get("K1AB_EVENTS"):
+                    ts = []
+                    for _ in range(reps):
+                        flush.zero_()
+                        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        a.record()
+                        run()
+                        b.record()
+                        torch.cuda.synchronize()
+                        ts.append(a.elapsed_time(b) * 1e3)
+                    t = float(np.median(ts))
+                else:
+                    # per-launch events resolve ~2 us on B200: time a CUDA graph of
+                    # (L2 flush, launch) x n minus a graph of n flushes alone
+                    def graph_time(with_run, n=12):
+                        gr = torch.cuda.CUDAGraph()
+                        with torch.cuda.graph(gr):
+                            for _ in range(n):
+                                flush.zero_()
+                                if with_run:
+                                    run()
+                        gr.replay()
+                        torch.cuda.synchronize()
+                        best = []
+                        for _ in range(3):
+                            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                            a.record()
+                            gr.replay()
+                            b.record()
+                            torch.cuda.synchronize()
+                            best.append(a.elapsed_time(b) * 1e3 / n)
+                        return float(np.median(best))
+                    t = graph_time(True) - graph_time(False)
                 row += f" | {os.path.basename(lp) or 'tree'}: {t:8.1f} us {lk / R_LU / (t * 1e-6):.3f}"
             except Exception as e:  # plan not supported by this build
                 row += f" | {os.path.basename(lp) or 'tree'}: n/a ({str(e)[:40]})"

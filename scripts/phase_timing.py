@@ -13,6 +13,8 @@ import paper_2512_06443_b200 as v
 v.lib_path = lib
 from paper_2512_06443_b200 import synth
 M, K, N = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
+# optional plan: warps splits n_cta
+plan = v.LaunchPlan(int(sys.argv[4]), int(sys.argv[5]), n_cta=int(sys.argv[6])) if len(sys.argv) > 6 else None
 dev = torch.device("cuda")
 W = torch.from_numpy(synth.ternary_weights(M, K, 1, 0.4)).to(dev)
 pw = v.pack_weights_device(W, 4)
@@ -28,13 +30,14 @@ for it in range(3):
     flush.zero_(); torch.cuda.synchronize()
     buf.zero_()
     torch.cuda.synchronize()
-    v.mpgemm(pw, A, s, 0.02, out=out)
+    v.mpgemm_ex(pw, A, s, 0.02, out=out, plan=plan) if plan else v.mpgemm(pw, A, s, 0.02, out=out)
     torch.cuda.synchronize()
 t = buf.view(-1, 8).cpu().numpy().astype(np.int64)
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 rel = (t - t0) / 1000.0
 names = ["entry", "tmem", "table0", "loop_end", "red_written", "sync1", "reduced", "stored"]
+print("plan", plan)
 print("CTAs", len(t), "rc", rc)
 for i, n in enumerate(names):
     col = rel[:, i]
