@@ -492,9 +492,11 @@ __device__ __forceinline__ void build_tables(uint32_t tab_s, uint32_t a_s, int g
 // packed add per entry and word).  The units are spread over the builder
 // warps of a pair group (g = 4: 2 warps x 4 pairs x 41 lines; g = 5: 4 warps
 // x 4 pairs x 122 lines).
+// P[r][w] = +a_r as packed arithmetic 16-bit deltas (U - 128 per field); the
+// -a_r step is T - P (mod 2^32 the same as adding C128 - U), so no second
+// delta array is held.
 template <int G, int Lv, int D, int PF>
-__device__ __forceinline__ void sub_walk(uint32_t row0, const uint32_t (&P)[G][4],
-                                         const uint32_t (&Mn)[G][4]) {
+__device__ __forceinline__ void sub_walk(uint32_t row0, const uint32_t (&P)[G][4]) {
   constexpr uint32_t K1 = 0x00010001u;
   uint32_t T[4];
 #pragma unroll
@@ -503,11 +505,11 @@ __device__ __forceinline__ void sub_walk(uint32_t row0, const uint32_t (&P)[G][4
 #pragma unroll
     for (int r = 0; r < Lv; ++r) {
       if (r < D) {
-        T[w] += Mn[r][w];  // walked digits start at trit -1
+        T[w] -= P[r][w];  // walked digits start at trit -1
       } else {
         const int d = (PF / pow3(r - D)) % 3;  // fixed digit (compile time)
         if (d == 2) T[w] += P[r][w];
-        if (d == 0) T[w] += Mn[r][w];
+        if (d == 0) T[w] -= P[r][w];
       }
     }
   }
@@ -518,7 +520,10 @@ __device__ __forceinline__ void sub_walk(uint32_t row0, const uint32_t (&P)[G][4
 #pragma unroll
     for (int st = 1; st < pow3(D); ++st) {
 #pragma unroll
-      for (int w = 0; w < 4; ++w) T[w] += (gw.dir[st] > 0) ? P[gw.digit[st]][w] : Mn[gw.digit[st]][w];
+      for (int w = 0; w < 4; ++w) {
+        if (gw.dir[st] > 0) T[w] += P[gw.digit[st]][w];
+        else T[w] -= P[gw.digit[st]][w];
+      }
       sts128(row0 + (pos0 + gw.idx[st]) * 128, T[0], T[1], T[2], T[3]);
     }
   }
@@ -532,40 +537,39 @@ __device__ __forceinline__ void zero_row(uint32_t row0) {
 
 // g = 4: half h of a pair group (41 lines: 23 + 18)
 template <int G>
-__device__ __forceinline__ void build_units(int h, uint32_t row0, const uint32_t (&P)[G][4],
-                                            const uint32_t (&Mn)[G][4]) {
+__device__ __forceinline__ void build_units(int h, uint32_t row0, const uint32_t (&P)[G][4]) {
   if constexpr (G == 4) {
     if (h == 0) {
       zero_row<4>(row0);
-      sub_walk<4, 0, 0, 0>(row0, P, Mn);
-      sub_walk<4, 1, 1, 0>(row0, P, Mn);
-      sub_walk<4, 3, 2, 0>(row0, P, Mn);
-      sub_walk<4, 3, 2, 1>(row0, P, Mn);
+      sub_walk<4, 0, 0, 0>(row0, P);
+      sub_walk<4, 1, 1, 0>(row0, P);
+      sub_walk<4, 3, 2, 0>(row0, P);
+      sub_walk<4, 3, 2, 1>(row0, P);
     } else {
-      sub_walk<4, 2, 2, 0>(row0, P, Mn);
-      sub_walk<4, 3, 2, 2>(row0, P, Mn);
+      sub_walk<4, 2, 2, 0>(row0, P);
+      sub_walk<4, 3, 2, 2>(row0, P);
     }
   } else {  // g = 5: quarter h (122 lines: 36 + 27 + 27 + 32)
     if (h == 0) {
-      sub_walk<5, 4, 2, 0>(row0, P, Mn);
-      sub_walk<5, 4, 2, 1>(row0, P, Mn);
-      sub_walk<5, 4, 2, 2>(row0, P, Mn);
-      sub_walk<5, 2, 2, 0>(row0, P, Mn);
+      sub_walk<5, 4, 2, 0>(row0, P);
+      sub_walk<5, 4, 2, 1>(row0, P);
+      sub_walk<5, 4, 2, 2>(row0, P);
+      sub_walk<5, 2, 2, 0>(row0, P);
     } else if (h == 1) {
-      sub_walk<5, 4, 2, 3>(row0, P, Mn);
-      sub_walk<5, 4, 2, 4>(row0, P, Mn);
-      sub_walk<5, 4, 2, 5>(row0, P, Mn);
+      sub_walk<5, 4, 2, 3>(row0, P);
+      sub_walk<5, 4, 2, 4>(row0, P);
+      sub_walk<5, 4, 2, 5>(row0, P);
     } else if (h == 2) {
-      sub_walk<5, 4, 2, 6>(row0, P, Mn);
-      sub_walk<5, 4, 2, 7>(row0, P, Mn);
-      sub_walk<5, 4, 2, 8>(row0, P, Mn);
+      sub_walk<5, 4, 2, 6>(row0, P);
+      sub_walk<5, 4, 2, 7>(row0, P);
+      sub_walk<5, 4, 2, 8>(row0, P);
     } else {
-      sub_walk<5, 3, 2, 0>(row0, P, Mn);
-      sub_walk<5, 3, 2, 1>(row0, P, Mn);
-      sub_walk<5, 3, 2, 2>(row0, P, Mn);
+      sub_walk<5, 3, 2, 0>(row0, P);
+      sub_walk<5, 3, 2, 1>(row0, P);
+      sub_walk<5, 3, 2, 2>(row0, P);
       zero_row<5>(row0);
-      sub_walk<5, 0, 0, 0>(row0, P, Mn);
-      sub_walk<5, 1, 1, 0>(row0, P, Mn);
+      sub_walk<5, 0, 0, 0>(row0, P);
+      sub_walk<5, 1, 1, 0>(row0, P);
     }
   }
 }
@@ -586,7 +590,7 @@ __device__ __forceinline__ void build_tables_wide(uint32_t tab_s, uint32_t a_s, 
 #pragma unroll 1
   for (int st = bw; st < SETS; st += BW) {
     const int j = (G == 4) ? 4 * st + q : q;  // group within the sub-stage
-    uint32_t P[G][4], Mn[G][4];
+    uint32_t P[G][4];
 #pragma unroll
     for (int r = 0; r < G; ++r) {
       uint32_t x0, x1;
@@ -598,24 +602,21 @@ __device__ __forceinline__ void build_tables_wide(uint32_t tab_s, uint32_t a_s, 
       const uint32_t U[4] = {__byte_perm(x0, 0u, 0x4140), __byte_perm(x0, 0u, 0x4342),
                              __byte_perm(x1, 0u, 0x4140), __byte_perm(x1, 0u, 0x4342)};
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        P[r][w] = U[w] - C128;
-        Mn[r][w] = C128 - U[w];
-      }
+      for (int w = 0; w < 4; ++w) P[r][w] = U[w] - C128;
     }
     const uint32_t row0 = tab_s + (uint32_t)(j * C::HR * kRowBytes + ch * 16);
     if constexpr (G == 4) {
-      build_units<4>(0, row0, P, Mn);
-      build_units<4>(1, row0, P, Mn);
+      build_units<4>(0, row0, P);
+      build_units<4>(1, row0, P);
     } else {
-      build_units<5>(st, row0, P, Mn);
+      build_units<5>(st, row0, P);
     }
   }
 }
 
 // table builder of K1 / K1-SK: wide 16-byte stores or the 4-byte form
 #ifndef VLUT_WIDE_MAX_WARPS
-#define VLUT_WIDE_MAX_WARPS 12
+#define VLUT_WIDE_MAX_WARPS 16
 #endif
 template <int WARPS>
 constexpr bool kWideBuild = WARPS <= VLUT_WIDE_MAX_WARPS;

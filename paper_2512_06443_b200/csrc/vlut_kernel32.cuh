@@ -150,7 +150,7 @@ __device__ __forceinline__ void build_tables32(uint32_t tab_s, uint32_t a_s, int
   const int jp = 4 * pg + q;
   const int jg = 2 * jp + (ch >> 2);  // group within the sub-stage
   const int c = ch & 3;               // tokens 8c .. 8c + 7
-  uint32_t P[G][4], Mn[G][4];
+  uint32_t P[G][4];
 #pragma unroll
   for (int r = 0; r < G; ++r) {
     uint32_t x0, x1;
@@ -162,12 +162,9 @@ __device__ __forceinline__ void build_tables32(uint32_t tab_s, uint32_t a_s, int
     const uint32_t U[4] = {__byte_perm(x0, 0u, 0x4140), __byte_perm(x0, 0u, 0x4342),
                            __byte_perm(x1, 0u, 0x4140), __byte_perm(x1, 0u, 0x4342)};
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      P[r][w] = U[w] - C128;   // +a_r as a packed arithmetic delta
-      Mn[r][w] = C128 - U[w];  // -a_r
-    }
+    for (int w = 0; w < 4; ++w) P[r][w] = U[w] - C128;  // +a_r as a packed arithmetic delta
   }
-  build_units<G>(h, tab_s + (uint32_t)(jp * C::PAIR_BYTES + ch * 16), P, Mn);
+  build_units<G>(h, tab_s + (uint32_t)(jp * C::PAIR_BYTES + ch * 16), P);
 }
 
 // ---------------------------------------------------------------- lookups (a4)
