@@ -664,7 +664,7 @@ def main():
     return 0
 
 
-def chain_bench(v, dev, world, rank, args, reps=3, peer=None):
+def chain_bench(v, dev, world, rank, args, reps=5, peer=None):
     """BASELINE.json configs[4]: 30 BitNet-2B-shaped layers of ternary linears
     (QKV, O, gate, up, down), N = 2048 tokens, every linear row-sharded over
     the N GPUs with an NCCL all-gather (north star), int8 re-quantization
@@ -711,11 +711,12 @@ def chain_bench(v, dev, world, rank, args, reps=3, peer=None):
         torch.cuda.synchronize()
         tf.append(a.elapsed_time(b))
     t_f = float(np.median(tf))
-    # f1 overlapped with compute: 4 token chunks; each linear's per-chunk
+    # f1 overlapped with compute: 2 token chunks; each linear's per-chunk
     # MAX all-reduce + quantize + int8 all-gather on a side stream while the
     # next chunk computes
-    kchain = LayerChain(layers, fused=True, chunks=4)
-    kchain(xq, xs)
+    kchain = LayerChain(layers, fused=True, chunks=2)
+    for _ in range(2):  # allocator steady state across the two streams
+        kchain(xq, xs)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -761,7 +762,7 @@ def chain_bench(v, dev, world, rank, args, reps=3, peer=None):
             "fused_requant": {"ms_per_forward": t_f, "tokens_s": N / (t_f * 1e-3),
                               "frac_smem_roofline": lookups / (R_LU * world) / (t_f * 1e-3)},
             "fused_requant_overlapped": {"ms_per_forward": t_k, "tokens_s": N / (t_k * 1e-3),
-                                         "chunks": 4,
+                                         "chunks": 2,
                                          "frac_smem_roofline": lookups / (R_LU * world)
                                          / (t_k * 1e-3)},
             "fused_allgather": ({"ms_per_forward": t_p, "tokens_s": N / (t_p * 1e-3),
