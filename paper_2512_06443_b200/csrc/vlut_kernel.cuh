@@ -535,7 +535,9 @@ __device__ __forceinline__ void zero_row(uint32_t row0) {
   sts128(row0, Z, Z, Z, Z);
 }
 
-// g = 4: half h of a pair group (41 lines: 23 + 18)
+// The units of one builder warp: g = 4, half h of the 41 lines (20 + 21);
+// g = 5, quarter h of the 122 lines (31 + 31 + 30 + 30).  Balanced, because
+// the slowest builder warp paces the table handshake.
 template <int G>
 __device__ __forceinline__ void build_units(int h, uint32_t row0, const uint32_t (&P)[G][4]) {
   if constexpr (G == 4) {
@@ -544,32 +546,36 @@ __device__ __forceinline__ void build_units(int h, uint32_t row0, const uint32_t
       sub_walk<4, 0, 0, 0>(row0, P);
       sub_walk<4, 1, 1, 0>(row0, P);
       sub_walk<4, 3, 2, 0>(row0, P);
-      sub_walk<4, 3, 2, 1>(row0, P);
+      sub_walk<4, 2, 1, 0>(row0, P);
+      sub_walk<4, 2, 1, 1>(row0, P);
     } else {
-      sub_walk<4, 2, 2, 0>(row0, P);
+      sub_walk<4, 3, 2, 1>(row0, P);
       sub_walk<4, 3, 2, 2>(row0, P);
+      sub_walk<4, 2, 1, 2>(row0, P);
     }
-  } else {  // g = 5: quarter h (122 lines: 36 + 27 + 27 + 32)
+  } else {
     if (h == 0) {
       sub_walk<5, 4, 2, 0>(row0, P);
       sub_walk<5, 4, 2, 1>(row0, P);
       sub_walk<5, 4, 2, 2>(row0, P);
-      sub_walk<5, 2, 2, 0>(row0, P);
+      sub_walk<5, 1, 1, 0>(row0, P);
+      sub_walk<5, 0, 0, 0>(row0, P);
     } else if (h == 1) {
       sub_walk<5, 4, 2, 3>(row0, P);
       sub_walk<5, 4, 2, 4>(row0, P);
       sub_walk<5, 4, 2, 5>(row0, P);
+      sub_walk<5, 2, 1, 0>(row0, P);
+      zero_row<5>(row0);
     } else if (h == 2) {
       sub_walk<5, 4, 2, 6>(row0, P);
       sub_walk<5, 4, 2, 7>(row0, P);
       sub_walk<5, 4, 2, 8>(row0, P);
+      sub_walk<5, 2, 1, 1>(row0, P);
     } else {
       sub_walk<5, 3, 2, 0>(row0, P);
       sub_walk<5, 3, 2, 1>(row0, P);
       sub_walk<5, 3, 2, 2>(row0, P);
-      zero_row<5>(row0);
-      sub_walk<5, 0, 0, 0>(row0, P);
-      sub_walk<5, 1, 1, 0>(row0, P);
+      sub_walk<5, 2, 1, 2>(row0, P);
     }
   }
 }
