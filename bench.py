@@ -611,7 +611,9 @@ def main():
     roofline = {
         "bound": "smem", "achieved": achieved, "peak": smem_peak_gbs, "unit": "GB/s",
         "frac": achieved / smem_peak_gbs, "traffic": traffic, "traffic_source": traffic_src,
-        "kernel": "vlut_mpgemm_kernel (K1)",
+        "kernel": ("vlut_mpgemm32_kernel (K1-32: 32-token tiles, paired-group tables)"
+                   if plan.n_cta == 32 else "vlut_mpgemm_kernel (K1)")
+                  + f" warps={plan.warps} splits={plan.splits}",
         "algorithmic_bytes_per_launch": a_shard["smem_bytes"],
         "per_unit": "2 B of shared-memory table read per int16 lookup-add; lookups = M*(K/g)*N",
         "peak_source": f"derived: {SM_COUNT} SMs x {SMEM_BYTES_PER_CLK_SM} B/clk x "
@@ -633,7 +635,8 @@ def main():
                         "lookup-adds, int32 accumulation, fp32 dequant",
         "data": "synthetic",
         "config": bench_config(wl, world),
-        "kernels": "K3 quantize + fused Vec-LUT mpGeMM with fp32 dequant (K1)"
+        "kernels": "K3 quantize + fused Vec-LUT mpGeMM with fp32 dequant ("
+                   + ("K1-32" if plan.n_cta == 32 else "K1") + ")"
                    + ((" with the all-gather of row shards fused into the epilogue "
                        "(NVLink peer stores + cross-GPU barrier)" if peer is not None
                        else " + NCCL all-gather of row shards") if world > 1 else ""),

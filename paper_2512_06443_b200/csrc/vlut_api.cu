@@ -409,7 +409,7 @@ double plan_for(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
 // factor, a cheaper epilogue (no DSMEM exchange at splits = 1) and the
 // DSMEM reduction of 128-byte rows when split.
 #ifndef VLUT_K32_FACTOR
-#define VLUT_K32_FACTOR 1.08
+#define VLUT_K32_FACTOR 1.00
 #endif
 double plan_for32(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
   const int KG = (K + g - 1) / g;

@@ -176,12 +176,54 @@ __device__ __forceinline__ void build_tables32(uint32_t tab_s, uint32_t a_s, int
 #define VLUT_K32_NX 1
 #endif
 constexpr int kNX32 = VLUT_K32_NX;
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;  // PTX prmt default mode: selector msb = replicate the byte's sign
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+// Per-lane PRMT selectors of the index decode (computed once): a pair's two
+// groups sit at bytes bb0, bb0 + 1 (bb0 in {0, 2}) of an index word; lane
+// side `so` = 0 reads group 2jp in steps 0..3 (line A), so = 1 group 2jp+1.
+//   pos[bb0/2][0|1]: byte of line A | B into the low byte (zeros above)
+//   sgn[bb0/2][0|1]: that byte's sign (msb) replicated over all 32 bits
+struct Sel32 {
+  uint32_t pos[2][2], sgn[2][2];
+  __device__ __forceinline__ void init(int so) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t xa = (uint32_t)(2 * h + so), xb = (uint32_t)(2 * h + 1 - so);
+      pos[h][0] = 0x4440u | xa;
+      pos[h][1] = 0x4440u | xb;
+      sgn[h][0] = 0x8888u | (xa * 0x1111u);
+      sgn[h][1] = 0x8888u | (xb * 0x1111u);
+    }
+  }
+};
+
+// Pairs [SUB*PAIRS, ...) of the K-tile.  PB pairs per load batch (8 LDS.128
+// each).  Index decode per 4-group word with byte-SIMD ops: |i - z| for all
+// four bytes in one VABSDIFF4, the signs in bit 7 of (i + 128 - z) (no
+// carries: i + 128 - z < 256), the negation count by POPC; per pair two PRMTs
+// pick the lane's line-A / line-B positions (no SELs), two more the signs.
+// Slots k < NX negate by XOR (ALU pipe), k >= NX by multiply (FMA pipe).
 template <int G, int PB>
 __device__ __forceinline__ void lookup_sub32(const int SUB, uint32_t tab, const uint32_t (&iwa)[4],
-                                             const uint32_t (&rot)[8], bool lo,
+                                             const uint32_t (&rot)[8], const Sel32& sel,
                                              uint32_t (&sw)[4][4], int32_t& nneg) {
   using C = Cfg32<G>;
   static_assert(C::PAIRS % PB == 0, "pairs per batch");
+  constexpr uint32_t Z4 = (uint32_t)C::ZERO * 0x01010101u;
+  constexpr uint32_t NB4 = (uint32_t)(128 - C::ZERO) * 0x01010101u;
+  constexpr int NWD = C::GS / 4;  // index words of this sub-stage
+  uint32_t aw[NWD], ntw[NWD];
+#pragma unroll
+  for (int wd = 0; wd < NWD; ++wd) {
+    const uint32_t word = iwa[(SUB * C::GS) / 4 + wd];
+    aw[wd] = __vabsdiffu4(word, Z4);               // |i - z| per byte
+    ntw[wd] = ~(word + NB4);                       // bit 7 set <=> i < z (negate)
+    nneg -= __popc(ntw[wd] & 0x80808080u);
+  }
 #pragma unroll
   for (int jb = 0; jb < C::PAIRS; jb += PB) {
     uint4 va[PB][4], vb[PB][4];
@@ -189,20 +231,12 @@ __device__ __forceinline__ void lookup_sub32(const int SUB, uint32_t tab, const 
 #pragma unroll
     for (int q = 0; q < PB; ++q) {
       const int jp = jb + q;
-      const int b0 = SUB * C::GS + 2 * jp;  // even: b0, b0 + 1 in one index word
-      const uint32_t word = iwa[b0 >> 2];
-      const int i0 = (int)((word >> (8 * (b0 & 3))) & C::IDX_MASK);
-      const int i1 = (int)((word >> (8 * ((b0 + 1) & 3))) & C::IDX_MASK);
-      const int d0 = i0 - C::ZERO, d1 = i1 - C::ZERO;
-      const uint32_t m0 = (uint32_t)(d0 >> 31), m1 = (uint32_t)(d1 >> 31);
-      const uint32_t p0 = (uint32_t)((d0 ^ (int)m0) - (int)m0);
-      const uint32_t p1 = (uint32_t)((d1 ^ (int)m1) - (int)m1);
-      nneg += (int)m0 + (int)m1;
+      const int wd = (2 * jp) >> 2, h = jp & 1;  // word, byte pair (bytes 2h, 2h+1)
       const uint32_t base = tab + (uint32_t)(jp * C::PAIR_BYTES);
-      const uint32_t l0 = base + p0 * 128u, l1 = base + p1 * 128u;
-      const uint32_t la = lo ? l0 : l1, lb = lo ? l1 : l0;
-      ma[q] = lo ? m0 : m1;
-      mb[q] = lo ? m1 : m0;
+      const uint32_t la = base + prmt(aw[wd], 0u, sel.pos[h][0]) * 128u;
+      const uint32_t lb = base + prmt(aw[wd], 0u, sel.pos[h][1]) * 128u;
+      ma[q] = prmt(ntw[wd], 0u, sel.sgn[h][0]);
+      mb[q] = prmt(ntw[wd], 0u, sel.sgn[h][1]);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {  // lines are 128-aligned: + == |
         va[q][k] = lds128(la + rot[k]);
@@ -364,7 +398,8 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
     uint32_t rot[8];  // chunk (lane & 7) ^ s of a 128-byte line
 #pragma unroll
     for (int s = 0; s < 8; ++s) rot[s] = (uint32_t)((((lane & 7) ^ s) & 7) * 16);
-    const bool lo = (lane & 4) == 0;
+    Sel32 sel;
+    sel.init((lane & 4) ? 1 : 0);  // lanes (lane & 7) >= 4 read group 2jp+1 first
     const uint32_t taddr =
         tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(32 * (warp >> 2));
     uint32_t sw[4][4];
@@ -388,7 +423,7 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
           iwa[0] = iw.x; iwa[1] = iw.y; iwa[2] = iw.z; iwa[3] = iw.w;
         }
 #ifndef VLUT_K32_NOLOOKUP  // (timing experiment only)
-        lookup_sub32<G, PB>(sub, tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES), iwa, rot, lo,
+        lookup_sub32<G, PB>(sub, tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES), iwa, rot, sel,
                             sw, nneg);
 #endif
         __syncwarp();

@@ -141,7 +141,7 @@ def test_planner_uses_slot_for_small_n(v):
     assert p1.slot == 1 and p16.slot == 1
     assert p1.splits > 1 and p1.grid_ctas <= 148 * 2
     p256 = v.plan_ws(6912, 2560, 256, 4)
-    assert p256.n_cta in (64, p256.nw * p256.tpw)
+    assert p256.slot == 0 and p256.n_cta in (64, 32)  # K1 (64-token) or K1-32 tiles
 
 
 @pytest.mark.parametrize("N,g", [(1, 4), (16, 4), (1, 5), (4, 5), (64, 4)])
