@@ -436,8 +436,65 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
       }
     }
     pdl_wait();  // (no-op by now) formally orders the epilogue's a_scale reads
+#ifndef VLUT_K32_TILE_EPI
+    if (S == 1) {
+      // ---- direct epilogue (no split-K): this thread's row is complete in
+      // TMEM once its last flush is done -- read it back and store the fp32
+      // (or int32) row straight to global memory, warp by warp, while slower
+      // warps still look up (no block barrier, no shared tile).  Slot k of
+      // this lane holds tokens 8c .. 8c+7, c = (lane ^ k) & 3.
+      const int32_t bias_total = C::BIAS * kKgTile * ntiles;
+      uint32_t v[2][16];
+      if (ntiles > 0) {
+        tmem_ld16(taddr, v[0]);
+        tmem_ld16(taddr + 16, v[1]);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[h][i] = 0;
+      }
+      const int m = m0 + tid;
+      if (m < p.M) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int c = (lane ^ k) & 3;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int n = n0 + 8 * c + 4 * hh;
+            if (n >= p.N) continue;  // N % 16 == 0: a quad is all-in or all-out
+            const uint32_t* x = v[k >> 1] + 8 * (k & 1) + 4 * hh;
+            const int a0 = (int)(x[0] - bias_total), a1 = (int)(x[1] - bias_total);
+            const int a2 = (int)(x[2] - bias_total), a3 = (int)(x[3] - bias_total);
+            if constexpr (ACC_ONLY) {
+              *reinterpret_cast<int4*>(reinterpret_cast<int32_t*>(p.out) + (size_t)m * p.N + n) =
+                  make_int4(a0, a1, a2, a3);
+            } else {
+              const int ul = 8 * c + 4 * hh;
+              *reinterpret_cast<float4*>(p.out + (size_t)m * p.N + n) =
+                  make_float4(__fmul_rn((float)a0, scale_s[ul]), __fmul_rn((float)a1, scale_s[ul + 1]),
+                              __fmul_rn((float)a2, scale_s[ul + 2]), __fmul_rn((float)a3, scale_s[ul + 3]));
+            }
+          }
+        }
+      }
+      // TMEM is released by warp 0 once every lookup warp has read its columns
+      tmem_fence_before();
+      bar_sync(6, L::MCTA);
+      if (warp == 0) {
+        tmem_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
+                     "n"(L::TMEM_COLS)
+                     : "memory");
+      }
+    }
+#endif
   }
   pdl_launch_dependents();
+#ifndef VLUT_K32_TILE_EPI
+  if (S == 1) return;  // builders have nothing left; lookup warps stored their rows
+#endif
 
   VLUT_STAMP(3);
   // ---- int32 tile -> shared (a5): row r = 128 bytes = 8 units of 4 tokens;
