@@ -100,7 +100,7 @@ class ClockSampler:
                 self.reasons |= int(r)
             except Exception:
                 pass
-            time.sleep(0.002)  # sparse: the sampler competes with the launch thread for the GIL
+            time.sleep(0.001)  # sparse: the sampler competes with the launch thread for the GIL
 
     def __enter__(self):
         if self.ok:
@@ -112,6 +112,22 @@ class ClockSampler:
         if self.ok:
             self._stop.set()
             self.t.join()
+
+    @staticmethod
+    def merge(*samplers):
+        """One summary over several sampling windows (timed steps + per-kernel
+        passes): median SM clock over all samples, union of reasons."""
+        ok = [c for c in samplers if c.ok]
+        if not ok:
+            return samplers[0].summary()
+        smp = [x for c in ok for x in c.samples]
+        reasons = 0
+        for c in ok:
+            reasons |= c.reasons
+        rs = [name for bit, name in ClockSampler.REASONS.items() if reasons & bit and bit != 0x1]
+        return {"sm_mhz": float(statistics.median(smp)) if smp else None,
+                "sm_max_mhz": float(ok[0].max_mhz), "reasons": rs, "samples": len(smp),
+                "windows": "timed steps + per-kernel passes"}
 
     def summary(self):
         if not self.ok:
@@ -497,27 +513,29 @@ def main():
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    # per-kernel passes (outside the clock sampler: no GIL contention), one
+    # per-kernel passes (a second clock-sampling window: the timed steps above
+    # last only a few ms), one
     # loop per kernel: each launch right after its own L2 flush, which runs on
     # the GPU while the host enqueues the event and the kernel (no host
     # submission latency in the window).  Separate loops because a preceding
     # K3 + synchronize measurably slows the next K1 launch (+6 us, idle-gap
     # effect, scripts/k1_timing_variants.py) -- inside the step, K1 follows
     # K3 back to back and takes ~step - K3.
-    for i in range(args.steps):
-        e = kev[i]
-        flush.zero_()
-        e[0].record(stream)
-        v.quantize(x, q=q, scale=s, stream=stream)
-        e[1].record(stream)
-        torch.cuda.synchronize()
-    for i in range(args.steps):
-        e = kev[i]
-        flush.zero_()
-        e[2].record(stream)
-        v.mpgemm_ws(pw, q, s, synth.W_SCALE, out=out_r, ws=ws, stream=stream)
-        e[3].record(stream)
-        torch.cuda.synchronize()
+    with ClockSampler(dev) as clk2:
+        for i in range(args.steps):
+            e = kev[i]
+            flush.zero_()
+            e[0].record(stream)
+            v.quantize(x, q=q, scale=s, stream=stream)
+            e[1].record(stream)
+            torch.cuda.synchronize()
+        for i in range(args.steps):
+            e = kev[i]
+            flush.zero_()
+            e[2].record(stream)
+            v.mpgemm_ws(pw, q, s, synth.W_SCALE, out=out_r, ws=ws, stream=stream)
+            e[3].record(stream)
+            torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     step_ms = [e[0].elapsed_time(e[1]) for e in evs]
@@ -648,7 +666,7 @@ def main():
         "roofline": roofline,
         "e2e": e2e,
     }
-    clocks = clk.summary()
+    clocks = ClockSampler.merge(clk, clk2)
     line["clocks"] = clocks
 
     if world == 1 and not args.no_cpu:
