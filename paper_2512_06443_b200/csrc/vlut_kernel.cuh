@@ -297,6 +297,7 @@ struct alignas(64) Params {
   int m_pad, kg_tiles;
   int splits;              // cluster size along K
   int a_vec;               // 16 (TMA), 4 or 1: activation staging width
+  int a3d;                 // K1-32: a_map is the 3-D view [r][group][token] (K % g == 0)
   int out_vec4;            // 1 if out rows allow aligned 16-byte stores
   int out_t;               // 1: out is [N][M] (feature-major, fused output transposition)
   const float* mul_in;     // optional fp32 [M][N]: out = fl(out * mul_in) (gate (.) up glue)
@@ -381,6 +382,15 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
       "%3}], [%4];\n" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(mbar)
       : "memory");
 }
 

@@ -122,7 +122,12 @@ __device__ __forceinline__ void stage32(const Params& p, int kt, int buf, int m0
     if (do_idx && bt == 0 && idx_rows > 0)
       bulk_g2s(smem_u32(idx_dst), p.payload + ((size_t)kt * p.m_pad + m0) * 16,
                (uint32_t)(idx_rows * 16), stg_mbar);
-    if (do_act && bt == 0) tma_load_2d(smem_u32(a_dst), &p.a_map, n0, k0, stg_mbar);
+    if (do_act && bt == 0) {
+      if (p.a3d)  // [r][group][token]: box (32 tokens, 16 groups, g rows)
+        tma_load_3d(smem_u32(a_dst), &p.a_map, n0, kt * kKgTile, 0, stg_mbar);
+      else
+        tma_load_2d(smem_u32(a_dst), &p.a_map, n0, k0, stg_mbar);
+    }
   }
 }
 
@@ -136,9 +141,13 @@ __device__ __forceinline__ void stage32(const Params& p, int kt, int buf, int m0
 // the shared-memory queue full, and builders issuing 4-byte stores could not
 // keep up (measured: halving their stores took K1-32 from 94 to 86 us).
 //
+// The activation tile is staged either as [group][r][32 tokens] (2-D map)
+// or, when K % g == 0, as [r][group][32 tokens] (3-D map): then the four
+// groups a builder load phase reads (same r, consecutive groups) fall in
+// four different 32-byte bank windows instead of one (4-way conflicts).
 template <int G>
 __device__ __forceinline__ void build_tables32(uint32_t tab_s, uint32_t a_s, int grp0, int bw,
-                                               int lane) {
+                                               int lane, bool a3d) {
   using C = Cfg32<G>;
   // warps per pair group: g = 4 -> 2 (two groups of 4 pairs), g = 5 -> 4
   constexpr int WPG = kBuilderWarps / (C::PAIRS / 4);
@@ -156,7 +165,8 @@ __device__ __forceinline__ void build_tables32(uint32_t tab_s, uint32_t a_s, int
     uint32_t x0, x1;
     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n"
                  : "=r"(x0), "=r"(x1)
-                 : "r"(a_s + (uint32_t)(((grp0 + jg) * G + r) * kN32 + 8 * c)));
+                 : "r"(a_s + (uint32_t)((a3d ? (r * kKgTile + grp0 + jg) : ((grp0 + jg) * G + r)) *
+                                             kN32 + 8 * c)));
     x0 ^= 0x80808080u;  // int8 a -> a + 128
     x1 ^= 0x80808080u;
     const uint32_t U[4] = {__byte_perm(x0, 0u, 0x4140), __byte_perm(x0, 0u, 0x4342),
@@ -376,7 +386,8 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
       }
 #ifndef VLUT_K32_NOBUILD  // (timing experiment only: tables left unbuilt)
       build_tables32<G>(tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES),
-                        a_s0 + (uint32_t)((T % C::STAGE) * C::A_BYTES), sub * C::GS, bw, lane);
+                        a_s0 + (uint32_t)((T % C::STAGE) * C::A_BYTES), sub * C::GS, bw, lane,
+                        p.a3d != 0);
 #endif
       __syncwarp();
       if (lane == 0) mbar_arrive(mbar + m32_full<C::NBUF>(u % C::NBUF));
