@@ -148,7 +148,8 @@ vlut_status encode_a_map(CUtensorMap* map, const int8_t* A, int K, int N, int g,
 // 3-D view of A for K1-32: dims (N tokens, K/g groups, g rows of a group),
 // strides (g*N, N) bytes -- the box (32, 16, g) lands in shared memory as
 // [r][group][token] (conflict-free builder loads, vlut_kernel32.cuh)
-vlut_status encode_a_map3d(CUtensorMap* map, const int8_t* A, int K, int N, int g) {
+vlut_status encode_a_map3d(CUtensorMap* map, const int8_t* A, int K, int N, int g,
+                           int box_n = vlut::kN32) {
   static EncodeTiledFn fn = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -162,7 +163,7 @@ vlut_status encode_a_map3d(CUtensorMap* map, const int8_t* A, int K, int N, int 
   if (!fn) return fail(VLUT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)(K / g), (cuuint64_t)g};
   const cuuint64_t strides[2] = {(cuuint64_t)g * N, (cuuint64_t)N};
-  const cuuint32_t box[3] = {(cuuint32_t)vlut::kN32, (cuuint32_t)vlut::kKgTile, (cuuint32_t)g};
+  const cuuint32_t box[3] = {(cuuint32_t)box_n, (cuuint32_t)vlut::kKgTile, (cuuint32_t)g};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)A, dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -915,8 +916,12 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
   const uintptr_t ap = (uintptr_t)A;
   p.a_vec = (N % 16 == 0 && (ap & 15) == 0) ? 16 : ((N % 4 == 0 && (ap & 3) == 0) ? 4 : 1);
   if (p.a_vec == 16) {
-    p.a3d = (n32 && K % W->g == 0 && !getenv("VLUT_NO_A3D")) ? 1 : 0;
-    st = p.a3d ? encode_a_map3d(&p.a_map, A, K, N, W->g)
+    // [r][group][token] staging (conflict-free wide-builder loads) whenever
+    // K % g == 0; K1's 4-byte builders (kWideBuild false) read [group][r]
+    const int wq = plan.warps;
+    const bool wide = n32 || (wq <= VLUT_WIDE_MAX_WARPS);
+    p.a3d = (wide && K % W->g == 0 && !getenv("VLUT_NO_A3D")) ? 1 : 0;
+    st = p.a3d ? encode_a_map3d(&p.a_map, A, K, N, W->g, n32 ? vlut::kN32 : vlut::kNcta)
                : encode_a_map(&p.a_map, A, K, N, W->g, n32 ? vlut::kN32 : vlut::kNcta);
     if (st != VLUT_OK) return st;
   }

@@ -423,7 +423,12 @@ __device__ __forceinline__ void stage_tile_bulk(const Params& p, int kt, int buf
     if (do_idx && bt == 0 && idx_rows > 0)
       bulk_g2s(smem_u32(idx_dst), p.payload + ((size_t)kt * p.m_pad + m0) * 16,
                (uint32_t)(idx_rows * 16), stg_mbar);
-    if (do_act && bt == 0) tma_load_2d(smem_u32(a_dst), &p.a_map, n0, k0, stg_mbar);
+    if (do_act && bt == 0) {
+      if (p.a3d)  // [r][group][token]: box (64 tokens, 16 groups, g rows)
+        tma_load_3d(smem_u32(a_dst), &p.a_map, n0, kt * kKgTile, 0, stg_mbar);
+      else
+        tma_load_2d(smem_u32(a_dst), &p.a_map, n0, k0, stg_mbar);
+    }
   }
 }
 
@@ -596,7 +601,7 @@ __device__ __forceinline__ void build_units(int h, uint32_t row0, const uint32_t
 // Lane 8 q + ch: group q of the set, tokens 8 ch .. 8 ch + 7.
 template <int G, int BW = kBuilderWarps>
 __device__ __forceinline__ void build_tables_wide(uint32_t tab_s, uint32_t a_s, int grp0, int bw,
-                                                  int lane) {
+                                                  int lane, bool a3d = false) {
   using C = Cfg<G>;
   constexpr uint32_t K1 = 0x00010001u;
   constexpr uint32_t C128 = 128u * K1;
@@ -612,7 +617,8 @@ __device__ __forceinline__ void build_tables_wide(uint32_t tab_s, uint32_t a_s, 
       uint32_t x0, x1;
       asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n"
                    : "=r"(x0), "=r"(x1)
-                   : "r"(a_s + (uint32_t)(((grp0 + j) * G + r) * kNcta + 8 * ch)));
+                   : "r"(a_s + (uint32_t)((a3d ? (r * kKgTile + grp0 + j) : ((grp0 + j) * G + r)) *
+                                               kNcta + 8 * ch)));
       x0 ^= 0x80808080u;
       x1 ^= 0x80808080u;
       const uint32_t U[4] = {__byte_perm(x0, 0u, 0x4140), __byte_perm(x0, 0u, 0x4342),
@@ -902,7 +908,7 @@ __global__ void __launch_bounds__((WARPS + kBW<WARPS, 1>) * 32, 1)
       if constexpr (kWideBuild<WARPS>)
         build_tables_wide<G, L::BW>(tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES),
                                     a_s0 + (uint32_t)((T % kStageBufs) * C::A_BYTES), sub * C::GS,
-                                    bw, lane);
+                                    bw, lane, p.a3d != 0);
       else
         build_tables<G, L::BW>(tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES),
                                a_s0 + (uint32_t)((T % kStageBufs) * C::A_BYTES), sub * C::GS, bw,

@@ -444,7 +444,7 @@ __global__ void __launch_bounds__((WARPS + kBW<WARPS, RPT>) * 32, 1)
       if constexpr (kWideBuild<WARPS>)
         build_tables_wide<G, L::BW>(tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES),
                                     a_s0 + (uint32_t)((T % kStageBufs) * C::A_BYTES), sub * C::GS,
-                                    bw, lane);
+                                    bw, lane, p.a3d != 0);
       else
         build_tables<G, L::BW>(tab_s + (uint32_t)((u % C::NBUF) * C::TAB_BYTES),
                                a_s0 + (uint32_t)((T % kStageBufs) * C::A_BYTES), sub * C::GS, bw,
