@@ -95,6 +95,11 @@ __device__ __forceinline__ void stage_idx(uint32_t dst, const uint8_t* src, int 
     bulk_g2s(dst + o, src + o, (uint32_t)min(piece, bytes - o), mbar);
 }
 constexpr int kLastOnlyBytes = 8192;              // split-K tiles up to this size: the last CTA finishes them
+#ifndef VLUT_SLOT_BULK_SMALL
+constexpr bool kRedRegs = true;   // last-only tiles: partials added by red.add from registers
+#else
+constexpr bool kRedRegs = false;  // (A/B) bulk reduce-add of the shared tile
+#endif
 
 template <int G, int NW, int TPW>
 struct SL {
@@ -576,6 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
     const int ld = min(p.N, L::NTOK);
 #pragma unroll
     for (int q = 0; q < L::RPL; ++q) {
+      if (kRedRegs && S > 1 && p.last_only) break;  // partials go out by red.add below
       const int r = q * kLookupThreads + warp * 32 + lane;
       if constexpr (L::NTOK >= 4) {
         if (ld == L::NTOK) {  // 16-byte vector stores
@@ -614,6 +620,25 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
     }
     fence_proxy_async_smem();  // the tile is read by bulk-reduce copies
     pdl_wait();  // epilogue reads a_scale / the workspace of the previous kernel
+    if (kRedRegs && S > 1 && p.last_only) {
+      // small split-K tiles (decode): each thread adds its partial rows
+      // straight from registers into the zero-kept workspace (red.add, no
+      // shared tile and no bulk copy to wait for); the arrival below -- a CTA
+      // barrier, then thread 0's acq_rel atomic, whose release is cumulative
+      // over the barrier -- orders them before the last CTA's reads
+      const int ntok_v = min(L::NTOK, p.N - n0);
+#pragma unroll
+      for (int q = 0; q < L::RPL; ++q) {
+        const int m = m0 + q * kLookupThreads + warp * 32 + lane;
+        if (m >= p.M) continue;
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+#pragma unroll
+          for (int e = 0; e < TPW; ++e)
+            if (w * TPW + e < ntok_v)
+              red_add_s32(p.ws_acc + (size_t)m * p.N + n0 + w * TPW + e, acc[q][w][e]);
+      }
+    }
     // the tile's generation before this CTA arrives (it cannot move before
     // then; read after pdl_wait so a previous launch's bump is visible)
     if (tid == 0 && S > 1 && !p.last_only)
@@ -633,8 +658,9 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
   if (S > 1) {
     // (1) partial -> zero-kept workspace: one bulk reduce-add when the CTA's
     // rows are contiguous there (N <= NTOK), one per row when rows are >= 64 B
-    const bool contig = (p.N <= L::NTOK) && ((elems & 3) == 0);
-    const bool rowwise = !contig && (p.N > L::NTOK) && (ntok_valid >= 16) &&
+    const bool red_done = kRedRegs && p.last_only;  // added from registers above
+    const bool contig = !red_done && (p.N <= L::NTOK) && ((elems & 3) == 0);
+    const bool rowwise = !red_done && !contig && (p.N > L::NTOK) && (ntok_valid >= 16) &&
                          ((ntok_valid & 3) == 0) && ((p.N & 3) == 0);
     if (contig) {
       if (tid == 0) {
@@ -648,7 +674,7 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
                            (uint32_t)(ntok_valid * 4));
         bulk_commit_wait_all();
       }
-    } else if (warp < kLW) {
+    } else if (!red_done && warp < kLW) {
 #pragma unroll 4
       for (int e = tid; e < elems; e += kLookupThreads) {
         const int r = e / ntok_valid, c = e - r * ntok_valid;
