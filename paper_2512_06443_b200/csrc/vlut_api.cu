@@ -639,14 +639,16 @@ vlut_status launch_k1_32(const vlut::Params& p, int S, int NT, int MT, cudaStrea
   cfg.dynamicSmemBytes = L::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (unsigned)S;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = (unsigned)S;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  // no cluster attribute without split-K (a plain launch; the S = 1 path
+  // never touches the cluster)
+  cfg.numAttrs = (S > 1 || getenv("VLUT_K32_CLUSTER1")) ? 2 : 1;
   VLUT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
   return VLUT_OK;
 }
