@@ -1555,6 +1555,10 @@ vlut_status vlut_quantize(const float* x, const float* y, int K, int N, int8_t* 
   while (CL < 8 && ((long long)K > (long long)CL * vlut::kQRows * vlut::kQCache || tok_blocks * CL < 296))
     CL *= 2;
   if (CL > K) CL = 1;
+  if (const char* e = getenv("VLUT_QCL")) {  // (development A/B knob)
+    const int c = atoi(e);
+    if (c == 1 || c == 2 || c == 4 || c == 8) CL = c;
+  }
   if (tok_blocks > 65535) return fail(VLUT_ERR_SHAPE, "N too large");
   const bool aligned = (N % 4 == 0) && ((((uintptr_t)x) | ((uintptr_t)(y ? y : x))) & 15) == 0 &&
                        (((uintptr_t)q) & 3) == 0;
