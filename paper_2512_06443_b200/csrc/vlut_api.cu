@@ -15,6 +15,7 @@
 #include "vlut_aux_kernels.cuh"
 #include "vlut_kernel.cuh"
 #include "vlut_kernel32.cuh"
+#include "vlut_kernel32_sk.cuh"
 #include "vlut_kernel_sk.cuh"
 #include "vlut_kernel_slot.cuh"
 #include <atomic>
@@ -480,6 +481,60 @@ double plan_for32(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
   return best_cost;
 }
 
+// K1-32 under stream-K (vlut_kernel32_sk.cuh): (warps, rows per thread) in
+// {12 x 1, 16 x 1, 12 x 2}; same cost units as plan_sk (half wavefronts
+// per 32-token row), plus the per-thread-row partial traffic of split tiles.
+#ifndef VLUT_SK32_FACTOR
+#define VLUT_SK32_FACTOR 1.00
+#endif
+int smem_bytes_sk32(int g, int warps, int rpt) {
+#define S32(G_, W_, R_) \
+  if (g == G_ && warps == W_ && rpt == R_) return vlut::Layout32<G_, W_, R_, true>::SMEM;
+  S32(4, 12, 1) S32(4, 16, 1) S32(4, 12, 2)
+  S32(5, 12, 1) S32(5, 16, 1) S32(5, 12, 2)
+#undef S32
+  return 0;
+}
+
+double plan_sk32(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
+  const int KG = (K + g - 1) / g;
+  const int kgt = (KG + VLUT_KG_TILE - 1) / VLUT_KG_TILE;
+  const int NT = (N + vlut::kN32 - 1) / vlut::kN32;
+  const int half_rows = (pow3i(g) + 1) / 2;
+  double best_cost = 1e300;
+  if (getenv("VLUT_NO_SK32") || getenv("VLUT_NO_K32")) return best_cost;
+  // Only 12 warps x 2 rows is planned: 12 x 1 / 16 x 1 lost to the cluster
+  // K1-32 and K1-SK everywhere they were measured, 16 x 2 and 12 x 4 rows
+  // spill (3-30 % slower).  The split-tile epilogues work per thread row
+  // (~16 B/clk): a CTA typically has a producer and an owner segment.
+  const int warps_opts[1] = {12};
+  const int rpt_opts[1] = {2};
+  for (int wi = 0; wi < 1; ++wi) {
+    const int warps = warps_opts[wi], rpt = rpt_opts[wi];
+    if (smem_bytes_sk32(g, warps, rpt) > 232448) continue;  // 227 KB opt-in per CTA
+    const int mcta = 32 * warps * rpt;
+    const long long MT = (M + mcta - 1) / mcta;
+    const long long U = MT * NT * kgt;
+    const long long grid = U < sms ? U : sms;
+    const double units = (double)((U + grid - 1) / grid);
+    double cost = units * VLUT_KG_TILE * 0.5 * ((double)mcta * VLUT_SK32_FACTOR + half_rows);
+    cost += 4000.0 + 16.0 * mcta;
+    const double per_tile = (double)grid / (double)(MT * NT);
+    if (per_tile > 1.0) cost += (per_tile - 1.0) * (double)mcta * 128.0 / 16.0;
+    if (cost < best_cost * 0.995) {
+      best_cost = cost;
+      best->warps = warps;
+      best->splits = 1;
+      best->m_cta = mcta;
+      best->n_cta = vlut::kN32;
+      best->grid_ctas = (int)grid;
+      best->smem_bytes = smem_bytes_sk32(g, warps, rpt);
+      best->streamk = 1;
+    }
+  }
+  return best_cost;
+}
+
 // ------------------------------------------------------------ K2 (lane-slot) planner
 // K2 variants: (nw, tpw) with n_cta = nw * tpw tokens per CTA.
 inline bool slot_variant_ok(int g, int nw, int tpw) {
@@ -651,6 +706,46 @@ vlut_status launch_k1_32(const vlut::Params& p, int S, int NT, int MT, cudaStrea
   cfg.numAttrs = (S > 1 || getenv("VLUT_K32_CLUSTER1")) ? 2 : 1;
   VLUT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
   return VLUT_OK;
+}
+
+template <int G, int WARPS, int RPT, bool ACC>
+vlut_status launch_sk32(const vlut::Params& p, const vlut::SkParams& sk, int grid,
+                        cudaStream_t st) {
+  using L = vlut::Layout32<G, WARPS, RPT, true>;
+  auto kern = vlut::vlut_mpgemm32_sk_kernel<G, WARPS, RPT, ACC>;
+  static std::once_flag flags[64];
+  static cudaError_t errs[64];
+  int dev = 0;
+  VLUT_CUDA_TRY(cudaGetDevice(&dev));
+  std::call_once(flags[dev & 63], [&] {
+    errs[dev & 63] = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+  });
+  VLUT_CUDA_TRY(errs[dev & 63]);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid, 1, 1);
+  cfg.blockDim = dim3(L::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = L::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeCooperative;  // owners wait for producers: co-resident
+  attr[1].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  VLUT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p, sk));
+  return VLUT_OK;
+}
+
+template <bool ACC>
+vlut_status dispatch_sk32(int g, int warps, int rpt, const vlut::Params& p,
+                          const vlut::SkParams& sk, int grid, cudaStream_t st) {
+#define D32(G_, W_, R_) \
+  if (g == G_ && warps == W_ && rpt == R_) return launch_sk32<G_, W_, R_, ACC>(p, sk, grid, st);
+  D32(4, 12, 1) D32(4, 16, 1) D32(4, 12, 2)
+  D32(5, 12, 1) D32(5, 16, 1) D32(5, 12, 2)
+#undef D32
+  return fail(VLUT_ERR_UNSUPPORTED, "no K1-32 stream-K variant g=%d warps=%d rows=%d", g, warps, rpt);
 }
 
 template <bool ACC>
@@ -842,11 +937,14 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
                   plan.splits);
     if (plan.streamk && (!ws || acc_in || out_t))
       return fail(VLUT_ERR_INVALID_ARGUMENT, "stream-K plan needs a workspace and [M][N] output");
-    if (plan.n_cta == vlut::kN32 && plan.streamk)
-      return fail(VLUT_ERR_UNSUPPORTED, "32-token tiles: cluster schedule only");
     // m_cta selects the rows per lookup thread: 0 or 32 * warps -> 1; 64 * warps
-    // -> 2 (stream-K with 8 or 12 warps)
-    if (plan.m_cta && plan.m_cta != 32 * plan.warps &&
+    // -> 2 (stream-K with 8 or 12 warps; 32-token stream-K with 12 warps)
+    if (plan.n_cta == vlut::kN32 && plan.streamk) {
+      const int r = plan.m_cta ? plan.m_cta / (32 * plan.warps) : 1;
+      if ((plan.m_cta && plan.m_cta % (32 * plan.warps)) || !smem_bytes_sk32(W->g, plan.warps, r))
+        return fail(VLUT_ERR_UNSUPPORTED,
+                    "32-token stream-K: 12 or 16 warps x 1 row, or 12 warps x 2 rows");
+    } else if (plan.m_cta && plan.m_cta != 32 * plan.warps &&
         !(plan.m_cta == 64 * plan.warps && plan.warps <= 12 && plan.streamk))
       return fail(VLUT_ERR_UNSUPPORTED, "m_cta=%d: 32*warps, or 64*warps (8/12 warps) stream-K",
                   plan.m_cta);
@@ -867,6 +965,14 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
         plan = p32;
         c_best = c32;
       }
+      if (ws) {
+        vlut_launch_plan s32 = {};
+        const double cs32 = plan_sk32(M, K, N, W->g, d.sms, &s32);
+        if (cs32 < c_best) {
+          plan = s32;
+          c_best = cs32;
+        }
+      }
     }
     if (plain_epilogue && N <= kSlotAutoMaxN) {
       vlut_launch_plan sl = {};
@@ -885,6 +991,10 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
   if (plan.streamk && (((uintptr_t)ws) & 15)) return fail(VLUT_ERR_MISALIGNED, "workspace not 16-B aligned");
   if (plan.splits > W->kg_tiles) plan.splits = 1;
   const bool n32 = plan.n_cta == vlut::kN32 && !plan.streamk;
+  const bool sk32 = plan.n_cta == vlut::kN32 && plan.streamk;
+  if (sk32 && (!k32_ok(A, out, N, acc_in, out_t, mul_in, amax_out) || g_peer_tls.n))
+    return fail(VLUT_ERR_UNSUPPORTED,
+                "32-token tiles: N %% 16 == 0, 16-B aligned A / out, plain epilogue only");
   if (n32) {
     if (!k32_ok(A, out, N, acc_in, out_t, mul_in, amax_out) || g_peer_tls.n)
       return fail(VLUT_ERR_UNSUPPORTED,
@@ -896,8 +1006,10 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
       return fail(VLUT_ERR_UNSUPPORTED, "needs %d B shared memory, device allows %d", smem32,
                   d.smem_optin);
   }
-  const int rpt = (plan.streamk && plan.m_cta == 64 * plan.warps) ? 2 : 1;
-  const int smem = smem_bytes_for(W->g, plan.warps, rpt);
+  const int rpt = sk32 ? (plan.m_cta ? plan.m_cta / (32 * plan.warps) : 1)
+                  : (plan.streamk && plan.m_cta == 64 * plan.warps) ? 2 : 1;
+  const int smem = sk32 ? smem_bytes_sk32(W->g, plan.warps, rpt)
+                        : smem_bytes_for(W->g, plan.warps, rpt);
   if (smem > d.smem_optin)
     return fail(VLUT_ERR_UNSUPPORTED, "needs %d B shared memory, device allows %d", smem,
                 d.smem_optin);
@@ -921,10 +1033,11 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
     // [r][group][token] staging (conflict-free wide-builder loads) whenever
     // K % g == 0; K1's 4-byte builders (kWideBuild false) read [group][r]
     const int wq = plan.warps;
-    const bool wide = n32 || (wq <= VLUT_WIDE_MAX_WARPS);
+    const bool t32 = n32 || sk32;
+    const bool wide = t32 || (wq <= VLUT_WIDE_MAX_WARPS);
     p.a3d = (wide && K % W->g == 0 && !getenv("VLUT_NO_A3D")) ? 1 : 0;
-    st = p.a3d ? encode_a_map3d(&p.a_map, A, K, N, W->g, n32 ? vlut::kN32 : vlut::kNcta)
-               : encode_a_map(&p.a_map, A, K, N, W->g, n32 ? vlut::kN32 : vlut::kNcta);
+    st = p.a3d ? encode_a_map3d(&p.a_map, A, K, N, W->g, t32 ? vlut::kN32 : vlut::kNcta)
+               : encode_a_map(&p.a_map, A, K, N, W->g, t32 ? vlut::kN32 : vlut::kNcta);
     if (st != VLUT_OK) return st;
   }
   p.out_t = out_t;
@@ -937,7 +1050,7 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
   p.amax_rows = amax_rows;
   p.out_vec4 = ((out_t ? M : N) % 4 == 0 && (((uintptr_t)out) & 15) == 0) ? 1 : 0;
   const int mcta = 32 * plan.warps * rpt;
-  const long long NT = (N + vlut::kNcta - 1) / vlut::kNcta;
+  const long long NT = (N + (sk32 ? vlut::kN32 : vlut::kNcta) - 1) / (sk32 ? vlut::kN32 : vlut::kNcta);
   const long long MT = (M + mcta - 1) / mcta;
   if (NT > 65535 || MT > 65535) return fail(VLUT_ERR_SHAPE, "grid too large");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -950,8 +1063,12 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
     sk.flags = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + sk_part_bytes(d.sms));
     sk.epoch = 1u;  // flags are reset by their consumers: graph-replay safe
     const int grid = (int)(sk.U < d.sms ? sk.U : d.sms);
-    st = acc_only ? dispatch_sk<true>(W->g, plan.warps, rpt, p, sk, grid, s)
-                  : dispatch_sk<false>(W->g, plan.warps, rpt, p, sk, grid, s);
+    if (sk32)
+      st = acc_only ? dispatch_sk32<true>(W->g, plan.warps, rpt, p, sk, grid, s)
+                    : dispatch_sk32<false>(W->g, plan.warps, rpt, p, sk, grid, s);
+    else
+      st = acc_only ? dispatch_sk<true>(W->g, plan.warps, rpt, p, sk, grid, s)
+                    : dispatch_sk<false>(W->g, plan.warps, rpt, p, sk, grid, s);
     if (st != VLUT_OK) return st;
     return ok();
   }
@@ -1354,12 +1471,17 @@ vlut_status vlut_plan_ws(int M, int K, int N, int g, vlut_launch_plan* plan) {
     *plan = skp;
     c = c_sk;
   }
-  vlut_launch_plan p32 = {};
+  vlut_launch_plan p32 = {}, s32 = {};
   if (N % 16 == 0 && !getenv("VLUT_NO_K32")) {
     const double c32 = plan_for32(M, K, N, g, d.sms, &p32);
     if (c32 < c) {
       *plan = p32;
       c = c32;
+    }
+    const double cs32 = plan_sk32(M, K, N, g, d.sms, &s32);
+    if (cs32 < c) {
+      *plan = s32;
+      c = cs32;
     }
   }
   if (N <= kSlotAutoMaxN && plan_slot(M, K, N, g, d.sms, N == 1 ? 1 : 2, 0, 0, true, &slp) < c)

@@ -46,7 +46,7 @@ __device__ __forceinline__ constexpr int m32_empty(int b) { return 8 * NB + 8 * 
 template <int NB>
 __device__ __forceinline__ constexpr int m32_stage(int s) { return 16 * NB + 8 * s; }
 
-template <int G>
+template <int G, bool SK = false>
 struct Cfg32 {
   static constexpr int R = pow3(G);
   static constexpr int ZERO = (R - 1) / 2;
@@ -54,7 +54,9 @@ struct Cfg32 {
 #ifndef VLUT_K32_NBUF
 #define VLUT_K32_NBUF 3
 #endif
-  static constexpr int NBUF = (G == 4) ? VLUT_K32_NBUF : 2;  // table buffers
+  // table buffers (the stream-K variant keeps 2: its index tiles hold up to
+  // 1536 rows)
+  static constexpr int NBUF = (G == 4 && !SK) ? VLUT_K32_NBUF : 2;
   static constexpr int GS = (G == 4) ? 16 : 8;      // groups per sub-stage (even)
   static constexpr int PAIRS = GS / 2;
   static constexpr int SUBS = kKgTile / GS;
@@ -72,27 +74,34 @@ struct Cfg32 {
 #ifndef VLUT_K32_AHEAD
 #define VLUT_K32_AHEAD 2
 #endif
-  static constexpr int AHEAD = VLUT_K32_AHEAD;
+  static constexpr int AHEAD = SK ? 1 : VLUT_K32_AHEAD;
   static constexpr int STAGE = NBUF + AHEAD;
   static_assert(STAGE * 8 + 16 * NBUF <= 96, "mbarrier region");
   static_assert(kFlushTiles * kKgTile * 2 * BIAS <= 65535, "SWAR field overflow");
 };
 
-template <int G, int WARPS>
+// RPT output rows per lookup thread (row block rb = rows rb*NLT + tid); SK =
+// the stream-K variant's buffer counts.
+template <int G, int WARPS, int RPT = 1, bool SK = false>
 struct Layout32 {
+  using C = Cfg32<G, SK>;
   static constexpr int NLT = WARPS * 32;
   static constexpr int THREADS = NLT + kBuilderWarps * 32;
   static constexpr int BUILDER0 = NLT;
-  static constexpr int MCTA = NLT;
-  static constexpr int RED_BYTES = MCTA * kN32 * 4;   // int32 tile [row][32]
-  static constexpr int TMEM_COLS = 32 * ((WARPS + 3) / 4) <= 32 ? 32
-                                   : (32 * ((WARPS + 3) / 4) <= 64 ? 64 : 128);
-  static constexpr int TAB_REGION = Cfg32<G>::NBUF * Cfg32<G>::TAB_BYTES > RED_BYTES
-                                        ? Cfg32<G>::NBUF * Cfg32<G>::TAB_BYTES : RED_BYTES;
+  static constexpr int MCTA = NLT * RPT;
+  // int32 tile [row][32] of the cluster epilogue (the stream-K epilogue
+  // works from registers: no tile)
+  static constexpr int RED_BYTES = SK ? 0 : MCTA * kN32 * 4;
+  static constexpr int CB = 32 * ((WARPS + 3) / 4);   // TMEM columns per row block
+  static constexpr int TMEM_COLS = CB * RPT <= 32 ? 32 : CB * RPT <= 64 ? 64
+                                   : CB * RPT <= 128 ? 128 : CB * RPT <= 256 ? 256 : 512;
+  static_assert(CB * RPT <= 512, "TMEM columns");
+  static constexpr int TAB_REGION = C::NBUF * C::TAB_BYTES > RED_BYTES
+                                        ? C::NBUF * C::TAB_BYTES : RED_BYTES;
   static constexpr int IDX_OFF = TAB_REGION;
   static constexpr int IDX_BYTES = MCTA * 16;
-  static constexpr int A_OFF = IDX_OFF + Cfg32<G>::STAGE * IDX_BYTES;
-  static constexpr int MISC_OFF = A_OFF + Cfg32<G>::STAGE * Cfg32<G>::A_BYTES;
+  static constexpr int A_OFF = IDX_OFF + C::STAGE * IDX_BYTES;
+  static constexpr int MISC_OFF = A_OFF + C::STAGE * C::A_BYTES;
   static constexpr int MBAR_OFF = MISC_OFF + 16;
   static constexpr int SCALE_OFF = MBAR_OFF + 96;
   static constexpr int SMEM = SCALE_OFF + kN32 * 4;
@@ -101,12 +110,12 @@ struct Layout32 {
 };
 
 // ---------------------------------------------------------------- staging (a2)
-template <int G, int WARPS>
+template <int G, int WARPS, int RPT = 1, bool SK = false>
 __device__ __forceinline__ void stage32(const Params& p, int kt, int buf, int m0, int n0,
                                         uint8_t* smem, int bt, uint32_t stg_mbar, bool do_idx,
                                         bool do_act, bool arm) {
-  using C = Cfg32<G>;
-  using L = Layout32<G, WARPS>;
+  using C = Cfg32<G, SK>;
+  using L = Layout32<G, WARPS, RPT, SK>;
   constexpr int NB = kBuilderWarps * 32;
   const int idx_rows = max(0, min(L::MCTA, p.m_pad - m0));
   const int k0 = kt * kKgTile * G;

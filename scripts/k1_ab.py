@@ -24,7 +24,10 @@ PLANS = {"auto": None, "c12x2": (12, 2, 0, 0), "w12r2": (12, 1, 768, 1), "w8r2":
          "n32w12": (12, 1, 0, 0, 32), "n32w16": (16, 1, 0, 0, 32), "n32w8": (8, 1, 0, 0, 32),
          "n32w12s2": (12, 2, 0, 0, 32), "n32w16s2": (16, 2, 0, 0, 32), "n32w8s2": (8, 2, 0, 0, 32),
          "n32w12s4": (12, 4, 0, 0, 32), "n32w12s8": (12, 8, 0, 0, 32), "n32w8s8": (8, 8, 0, 0, 32),
-         "n32w16s8": (16, 8, 0, 0, 32), "n32w8s4": (8, 4, 0, 0, 32), "n32w16s4": (16, 4, 0, 0, 32)}
+         "n32w16s8": (16, 8, 0, 0, 32), "n32w8s4": (8, 4, 0, 0, 32), "n32w16s4": (16, 4, 0, 0, 32),
+         "sk32w12r1": (12, 1, 384, 1, 32), "sk32w16r1": (16, 1, 512, 1, 32),
+         "sk32w12r2": (12, 1, 768, 1, 32), "sk32w16r2": (16, 1, 1024, 1, 32),
+         "sk32w12r4": (12, 1, 1536, 1, 32)}
 
 
 def main():

@@ -38,7 +38,7 @@ def _inputs(K, N, seed):
     return oracle.quantize(x)
 
 
-@pytest.mark.parametrize("plan_kind", ["streamk", "streamk_rpt2", "slot_split", "auto"])
+@pytest.mark.parametrize("plan_kind", ["streamk", "streamk_rpt2", "streamk32", "slot_split", "auto"])
 def test_graph_replay_with_new_inputs(v, plan_kind):
     """A captured mpGeMM replayed three times with different activations in
     the same buffers: every replay must equal the oracle.  (With per-launch
@@ -48,6 +48,7 @@ def test_graph_replay_with_new_inputs(v, plan_kind):
     N = 8 if plan_kind == "slot_split" else 256
     plan = {"streamk": v.LaunchPlan(16, 1, streamk=1),
             "streamk_rpt2": v.LaunchPlan(12, 1, m_cta=768, streamk=1),
+            "streamk32": v.LaunchPlan(12, 1, m_cta=768, n_cta=32, streamk=1),
             "slot_split": v.slot_plan(tpw=2, splits=5),
             "auto": None}[plan_kind]
     W = synth.ternary_weights(M, K, seed=77)

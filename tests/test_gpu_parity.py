@@ -511,6 +511,33 @@ def test_streamk_acc_bit_exact(v, M, K, N, g, warps, rpt):
         assert np.array_equal(acc.cpu().numpy(), oracle.gemm_i32(W, A))
 
 
+@pytest.mark.parametrize("M,K,N,g", SHAPES32 + [(6912, 2560, 256, 4), (2560, 2560, 2048, 4),
+                                               (3072, 4600, 512, 5)])
+@pytest.mark.parametrize("warps,rpt", [(12, 1), (16, 1), (12, 2)])
+def test_streamk32_acc_and_fp32(v, M, K, N, g, warps, rpt):
+    """K1-32 under stream-K (32-token tiles, 1 or 2 rows per lookup thread,
+    split tiles combined through workspace partials): int32 bit-exact, fp32
+    bit-identical to the oracle's fixed-order dequant."""
+    W = synth.ternary_weights(M, K, seed=7 * M + K)
+    A = synth.int8_activations(K, N, seed=N + 41)
+    s = synth.token_scales(N, seed=N + 1)
+    pw = v.pack_weights_device(to_dev(W), g)
+    plan = v.LaunchPlan(warps, 1, m_cta=32 * warps * rpt, n_cta=32, streamk=1)
+    ws = torch.zeros_like(v.workspace(dev()))
+    acc = v.mpgemm_acc_ws(pw, to_dev(A), plan=plan, ws=ws)
+    out = v.mpgemm_ws(pw, to_dev(A), to_dev(s), synth.W_SCALE, plan=plan, ws=ws)
+    torch.cuda.synchronize()
+    if M * N * K > 2e9:  # large case: sampled rows
+        pick = np.unique(synth.rng(2).integers(0, M, size=24))
+        ref = oracle.gemm_i32(W[pick], A)
+        assert np.array_equal(acc.cpu().numpy()[pick], ref)
+        check_fp32(out.cpu().numpy()[pick], ref, s, synth.W_SCALE)
+    else:
+        ref = oracle.gemm_i32(W, A)
+        assert np.array_equal(acc.cpu().numpy(), ref)
+        check_fp32(out.cpu().numpy(), ref, s, synth.W_SCALE)
+
+
 @pytest.mark.parametrize("M,K,N,g", [(6912, 2560, 256, 4), (3072, 23040, 1024, 5), (385, 1024, 130, 4)])
 def test_streamk_fp32_and_planner_identity(v, M, K, N, g):
     W = synth.ternary_weights(M, K, seed=M)
