@@ -44,6 +44,14 @@ SM_MAX_MHZ_FALLBACK = 1965.0
 HBM_FALLBACK_GBS = 6650.0    # B200_PROFILING.md fallback
 
 
+
+def plan_label(pl):
+    """Kernel family and launch shape a LaunchPlan selects (vlut.h dispatch)."""
+    if pl.slot:
+        return f"K2 lane-slot tpw={pl.tpw} nw={pl.nw} splits={pl.splits}"
+    fam = ("K1-32" if pl.n_cta == 32 else "K1") + ("-SK" if pl.streamk else "")
+    return f"{fam} warps={pl.warps} m_cta={pl.m_cta} n_cta={pl.n_cta} splits={pl.splits}"
+
 def load_peaks():
     try:
         with open(MEASURED_PEAKS) as f:
@@ -973,8 +981,7 @@ def sweep(v, dev, stream, flush, reps=10):
             else:
                 t = timeit(pw, A, sc, out)
                 timing = "per-launch events, L2 flushed"
-            kern = (f"K2 lane-slot tpw={pl.tpw} nw={pl.nw} splits={pl.splits}" if pl.slot else
-                    f"K1 warps={pl.warps} m_cta={pl.m_cta} n_cta={pl.n_cta} splits={pl.splits} streamk={pl.streamk}")
+            kern = plan_label(pl)
             e = {"config": 4, "M": lin.M, "K": lin.K, "N": N, "g": g, "us": t * 1e6,
                  "kernel": kern, "timing": timing,
                  "tokens_s": N / t, "gops": 2 * lin.M * lin.K * N / t / 1e9,
@@ -1090,8 +1097,7 @@ def config_table(path, oracle_budget_s=0.6):
         hbm_b = pw.nbytes + K * N + 4 * N + 4 * M * N
         t_roof = max(hbm_b / hbm, lk / r_lu)
         pl = v.plan_ws(M, K, N, g)
-        kern = (f"K2 tpw={pl.tpw} nw={pl.nw} splits={pl.splits}" if pl.slot else
-                f"K1 warps={pl.warps} m_cta={pl.m_cta} n_cta={pl.n_cta} splits={pl.splits} streamk={pl.streamk}")
+        kern = plan_label(pl)
         call = lambda p_: (lambda: v.mpgemm_ws(p_, A, sc, synth.W_SCALE, out=out, ws=ws))
         with ClockSampler(dev) as clk:
             if N <= 64:
