@@ -225,7 +225,9 @@ vlut_status vlut_mpgemm_ex(const vlut_packed_weights* W, const int8_t* A,
  *               Regions: stream-K partials and partial-ready flags (each
  *               flag is set by its producer CTA and reset by its consumer in
  *               the same launch), K2 split-K arrival counts and int32
- *               accumulators (every K2 launch leaves them zero again) and
+ *               accumulators (at decode-size tiles: counted 64-bit words,
+ *               count << 40 | biased sum; every K2 launch leaves them zero
+ *               again) and
  *               per-tile generation words (monotonic, read on the device).
  *               No host-side per-launch state: captured CUDA graphs may be
  *               replayed.  Stream-K and K2 split-K launches are cooperative

@@ -888,6 +888,10 @@ vlut_status run_slot(const vlut_packed_weights* W, const int8_t* A, const float*
   }
   p.last_only =
       ((long long)pl.m_cta * std::min(N, pl.n_cta) * 4 <= vlut::slot::kLastOnlyBytes) ? 1 : 0;
+  // counted 64-bit meeting (decode): 8-byte words, at most 255 partials
+  if (vlut::slot::kAtom64 && p.last_only &&
+      (S > vlut::slot::kAtom64MaxSplits || (size_t)M * (size_t)N * 8 > kSlotAccBytes))
+    p.last_only = 0;
   vlut_status st = dispatch_slot(g, pl.nw, tpw, p, S, (int)NTt, (int)MT,
                                  static_cast<cudaStream_t>(stream));
   if (st != VLUT_OK) return st;

@@ -7,6 +7,28 @@
 
 namespace vlut {
 
+#ifndef VLUT_Q_EARLY_TRIGGER
+#define VLUT_Q_EARLY_TRIGGER 1
+#endif
+// Quantizer PDL order.  The dependent mpGeMM launches once every CTA of the
+// quantizer has triggered, and touches nothing but the packed weights (which
+// no kernel writes) before its own griddepcontrol.wait -- which returns only
+// after this quantizer completed, and this quantizer's wait after ITS
+// predecessor (e.g. the previous layer's mpGeMM) completed: the chain stays
+// ordered.  Triggering BEFORE waiting therefore lets the next mpGeMM launch
+// (and start streaming its weights) while this quantizer still waits for
+// the previous kernel, instead of only after it.  All CTAs of this grid are
+// resident when the dependent launches, so it cannot starve them.
+__device__ __forceinline__ void pdl_trigger_then_wait() {
+  if (VLUT_Q_EARLY_TRIGGER) {
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  } else {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  }
+}
+
 // ---------------------------------------------------------------- K3 quantize (a7)
 // A thread-block cluster of CL CTAs owns 16 consecutive tokens; CTA `rank`
 // owns a contiguous 1/CL slice of the K rows.  Each thread loads float4s
@@ -87,9 +109,8 @@ __global__ void __launch_bounds__(kQThreads)
   const int k_end = (int)(((long long)(rank + 1) * K) / CL);
   VLUT_STAMP(0);
   // PDL: x may be the previous kernel's output; let the next kernel launch early
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  pdl_trigger_then_wait();
   VLUT_STAMP(1);
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   float4 cache[kQCache];
   float m[4] = {0.f, 0.f, 0.f, 0.f};
   // every load of the register cache is issued before any use (a multiply
@@ -222,8 +243,7 @@ __global__ void __launch_bounds__(kQfThreads)
   const long long f0 = (long long)rank * per;
   const long long f1 = min(total4, f0 + per);
   if (tid < 16) red[tid] = 0u;
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  pdl_trigger_then_wait();
   const float4* x4 = reinterpret_cast<const float4*>(x);
   float4 c[kQfCache];
 #pragma unroll
@@ -317,8 +337,7 @@ __global__ void __launch_bounds__(256)
   const int units = K / gran;
   const int k_begin = gran * (int)(((long long)rank * units) / CL);
   const int k_end = gran * (int)(((long long)(rank + 1) * units) / CL);
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  pdl_trigger_then_wait();
   auto load = [&](int n, int k) -> float {
     const size_t o = (size_t)n * K + k;
     return y ? __fmul_rn(__ldg(x + o), __ldg(y + o)) : __ldg(x + o);

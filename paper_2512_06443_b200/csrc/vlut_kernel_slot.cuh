@@ -41,8 +41,9 @@
 //                 (cp.reduce.async.bulk .add.s32: one per CTA when its rows
 //                 are contiguous there) and the CTAs arrive at an acq_rel
 //                 counter; the last to arrive re-arms it.  Tiles <= 8 KB
-//                 (decode): that last CTA alone finishes the tile (epilogue +
-//                 re-zeroing), the others exit without waiting.  Larger
+//                 (decode): each partial element is one counted 64-bit atomic
+//                 add (kAtom64 below); whichever thread adds an element's last
+//                 contribution finishes that element, nobody waits.  Larger
 //                 tiles: the last one bumps the tile's generation word, the
 //                 CTAs (co-resident: cooperative launch) wait for it and each
 //                 finishes 1/S of the tile, so no single CTA serialises it.
@@ -100,6 +101,32 @@ constexpr bool kRedRegs = true;   // last-only tiles: partials added by red.add 
 #else
 constexpr bool kRedRegs = false;  // (A/B) bulk reduce-add of the shared tile
 #endif
+#ifndef VLUT_SLOT_ATOM64
+#define VLUT_SLOT_ATOM64 1
+#endif
+// last-only tiles (decode): every partial element goes out as ONE 64-bit
+// atomic add carrying (1 << 40) + (partial + 2^31): bits 40.. count the
+// contributions, bits 0..39 hold the biased sum (S <= 255 partials of < 2^32
+// each cannot carry into the count).  The thread whose add returns count
+// S - 1 holds the tile's last contribution to that element: it forms the sum
+// (old + its own, minus S 2^31), runs the epilogue for it and re-zeroes the
+// word.  No arrival counter, no CTA barrier, no read-back of the workspace:
+// one L2 round trip instead of three (red -> acq_rel arrival -> loads).
+constexpr bool kAtom64 = VLUT_SLOT_ATOM64 != 0;
+#ifndef VLUT_SLOT_LDG
+#define VLUT_SLOT_LDG 1
+#endif
+// One table word per lookup (NW = 1: decode, N <= 2): every lookup thread
+// copies its OWN index rows (16 B per row and K-tile, lane-consecutive rows:
+// coalesced) into its slots of the shared ring with cp.async, a whole ring
+// (STAGES tiles) at entry -- the weights do not depend on the previous
+// kernel -- and one tile per tile consumed, one commit group per tile
+// (the thread reads back only what it copied: no CTA-wide handshake).
+// Measured (scripts/hbm_floor.cu, 17.7 MB): one bulk-copy ring per SM
+// streams it in >= 6.4 us, per-thread loads issued up front in 4.3-5.1 us.
+// The producer then stages only the (tiny) activation tiles.
+constexpr bool kCpIdxAll = VLUT_SLOT_LDG != 0;
+constexpr int kAtom64MaxSplits = 255;
 
 template <int G, int NW, int TPW>
 struct SL {
@@ -157,6 +184,11 @@ struct SlotParams {
 __device__ __forceinline__ void red_add_s32(int32_t* p, int32_t v) {
   asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long atom_add_u64(unsigned long long* p, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.relaxed.gpu.global.add.u64 %0, [%1], %2;\n" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
   unsigned old;
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
@@ -181,6 +213,17 @@ __device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+// per-thread asynchronous 16-byte global -> shared copy (L1 bypassed)
+__device__ __forceinline__ void cp_async16(uint32_t dst_s, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst_s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
   uint32_t v;
@@ -297,6 +340,15 @@ __device__ __forceinline__ int act_value(const SlotParams& p, uint32_t act_s, in
 template <int G, int NW, int TPW>
 __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_constant__ SlotParams p) {
   using L = SL<G, NW, TPW>;
+  // last-only tiles hold <= 8 KB: at >= 1024 rows per CTA, <= 2 tokens
+  constexpr bool kA64 = kAtom64 && L::NTOK <= 2;
+  // per-thread copies where the ring is short (g = 5: 2 stages beside the
+  // 243-row tables; a bulk stage is refilled only after all 16 lookup warps
+  // and both builders released it): config 4 g = 5 N = 1 8.24 -> 7.61 us.
+  // With the 8-stage g = 4 ring the bulk copies are as fast or faster
+  // (7.54 vs 7.75 us; profiles/r02_decode.txt)
+  constexpr bool kLdgIdx = kCpIdxAll && NW == 1 && L::STAGES < 4;
+  constexpr int PF = kLdgIdx ? L::STAGES : 2;  // kLdgIdx: tiles in flight per thread
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -326,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
     mbar_init(mbar + 24, kLW);
     for (int s = 0; s < L::STAGES; ++s) {
       mbar_init(mbar + 32 + 8 * s, 1);
-      mbar_init(mbar + IFREE0 + 8 * s, kLW + kBW);  // ring slot read by lookups and builders
+      mbar_init(mbar + IFREE0 + 8 * s, kLdgIdx ? kBW : kLW + kBW);  // ring slot readers
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -346,9 +398,10 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
         const int kt = kt0 + t;
         const int ab = p.act_tma ? act_tile_bytes(p, kt, G) : 0;
         const uint32_t stg = mbar + 32 + 8 * t;
-        mbar_expect_tx(stg, (uint32_t)(rows * 16 + ab));
-        stage_idx(idx_s + (uint32_t)(t * L::IDX_BYTES), p.payload + ((size_t)kt * p.m_pad + m0) * 16,
-                  rows * 16, stg);
+        mbar_expect_tx(stg, (uint32_t)((kLdgIdx ? 0 : rows * 16) + ab));
+        if (!kLdgIdx)
+          stage_idx(idx_s + (uint32_t)(t * L::IDX_BYTES), p.payload + ((size_t)kt * p.m_pad + m0) * 16,
+                    rows * 16, stg);
       }
       // (2) activations come from the previous kernel (quantizer)
       pdl_wait();
@@ -371,9 +424,10 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
         if (kRampStages > 0 && t == kRampStages) mbar_wait(mbar + 32, 0);
         const int ab = p.act_tma ? act_tile_bytes(p, kt, G) : 0;
         const uint32_t stg = mbar + 32 + 8 * st;
-        mbar_expect_tx(stg, (uint32_t)(rows * 16 + ab));
-        stage_idx(idx_s + (uint32_t)(st * L::IDX_BYTES), p.payload + ((size_t)kt * p.m_pad + m0) * 16,
-                  rows * 16, stg);
+        mbar_expect_tx(stg, (uint32_t)((kLdgIdx ? 0 : rows * 16) + ab));
+        if (!kLdgIdx)
+          stage_idx(idx_s + (uint32_t)(st * L::IDX_BYTES), p.payload + ((size_t)kt * p.m_pad + m0) * 16,
+                    rows * 16, stg);
         if (ab > 0)
           bulk_g2s(act_s + (uint32_t)(st * L::ACT_BYTES), p.A + (size_t)kt * kKgTile * G * p.N,
                    (uint32_t)ab, stg);
@@ -486,24 +540,69 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
 #pragma unroll
       for (int w = 0; w < NW; ++w) sw[q][w] = 0;
     int since_flush = 0;
+    // kLdgIdx: this thread's index rows of tile t -> its slots of ring stage
+    // t % STAGES (cp.async, one commit group per tile, empty past the end)
+    auto cp_tile = [&](int t) {
+      if (t < ntiles) {
+        const int st = t % L::STAGES;
+#pragma unroll
+        for (int q = 0; q < L::RPL; ++q) {
+          const int r = q * kLookupThreads + warp * 32 + lane;
+          if (m0 + q * kLookupThreads + warp * 32 < p.m_pad)
+            cp_async16(idx_s + (uint32_t)(st * L::IDX_BYTES + r * 16),
+                       p.payload + ((size_t)(kt0 + t) * p.m_pad + m0 + r) * 16);
+        }
+      }
+      cp_async_commit();
+    };
+    // ramp: tiles 0 and 1 at entry; the rest of the ring once tile 0 has
+    // landed (the first tile is not queued behind a whole ring of requests)
+    if constexpr (kLdgIdx) {
+      cp_tile(0);
+      cp_tile(1);
+    }
     // one K-tile with table buffer B (compile time: the buffer offset folds
     // into the LDS immediate, one PRMT forms the rest of each address)
     auto tile = [&](auto Bc, int t) {
       constexpr int B = decltype(Bc)::value;
-      const int st = t % L::STAGES;
-      mbar_wait(mbar + 32 + 8 * st, (t / L::STAGES) & 1);  // index rows landed
-      if (t == 0) VLUT_STAMP(1);
-      if (t == ntiles - 1) VLUT_STAMP(7);
       uint4 v[L::RPL];
+      if constexpr (kLdgIdx) {
+        // this thread's rows of tile t have landed (groups younger than t's:
+        // tile 0 -> tile 1's; later tiles -> PF - 1 of them)
+        if (t == 0) {
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<PF - 1>();
+        }
+        const int st = t % L::STAGES;
+        if (t == 0) VLUT_STAMP(1);
+        if (t == ntiles - 1) VLUT_STAMP(7);
 #pragma unroll
-      for (int q = 0; q < L::RPL; ++q) {
-        const int r = q * kLookupThreads + warp * 32 + lane;
-        v[q] = (m0 + q * kLookupThreads + warp * 32 < p.m_pad)
-                   ? *reinterpret_cast<const uint4*>(smem + L::IDX_OFF + st * L::IDX_BYTES + r * 16)
-                   : make_uint4(0, 0, 0, 0);
+        for (int q = 0; q < L::RPL; ++q) {
+          const int r = q * kLookupThreads + warp * 32 + lane;
+          v[q] = (m0 + q * kLookupThreads + warp * 32 < p.m_pad)
+                     ? *reinterpret_cast<const uint4*>(smem + L::IDX_OFF + st * L::IDX_BYTES + r * 16)
+                     : make_uint4(0, 0, 0, 0);
+        }
+        if (t == 0) {  // end of the ramp: the ring's other free slots (2 .. PF-1)
+#pragma unroll 1
+          for (int j = 2; j < PF; ++j) cp_tile(j);
+        }
+      } else {
+        const int st = t % L::STAGES;
+        mbar_wait(mbar + 32 + 8 * st, (t / L::STAGES) & 1);  // index rows landed
+        if (t == 0) VLUT_STAMP(1);
+        if (t == ntiles - 1) VLUT_STAMP(7);
+#pragma unroll
+        for (int q = 0; q < L::RPL; ++q) {
+          const int r = q * kLookupThreads + warp * 32 + lane;
+          v[q] = (m0 + q * kLookupThreads + warp * 32 < p.m_pad)
+                     ? *reinterpret_cast<const uint4*>(smem + L::IDX_OFF + st * L::IDX_BYTES + r * 16)
+                     : make_uint4(0, 0, 0, 0);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(mbar + IFREE0 + 8 * st);  // ring slot's index rows consumed
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(mbar + IFREE0 + 8 * st);  // ring slot's index rows consumed
       mbar_wait(mbar + 8 * B, (t >> 1) & 1);           // table t built
       if (t == 0) VLUT_STAMP(2);
 #pragma unroll
@@ -540,6 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
           }
         }
       }
+      if constexpr (kLdgIdx) cp_tile(t + PF);  // refill the slot just read
       __syncwarp();
       if (lane == 0) mbar_arrive(mbar + 16 + 8 * B);  // table buffer B free
       if constexpr (TPW == 2) {
@@ -581,7 +681,7 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
     const int ld = min(p.N, L::NTOK);
 #pragma unroll
     for (int q = 0; q < L::RPL; ++q) {
-      if (kRedRegs && S > 1 && p.last_only) break;  // partials go out by red.add below
+      if ((kRedRegs || kA64) && S > 1 && p.last_only) break;  // partials go out from registers below
       const int r = q * kLookupThreads + warp * 32 + lane;
       if constexpr (L::NTOK >= 4) {
         if (ld == L::NTOK) {  // 16-byte vector stores
@@ -620,7 +720,50 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
     }
     fence_proxy_async_smem();  // the tile is read by bulk-reduce copies
     pdl_wait();  // epilogue reads a_scale / the workspace of the previous kernel
-    if (kRedRegs && S > 1 && p.last_only) {
+    if (kA64 && S > 1 && p.last_only) {
+      // small split-K tiles (decode), counted 64-bit atomics (kAtom64 above):
+      // all of the thread's adds first (their round trips overlap), then the
+      // elements it completed
+      unsigned long long* ws64 = reinterpret_cast<unsigned long long*>(p.ws_acc);
+      const int ntok_v = min(L::NTOK, p.N - n0);
+      unsigned long long old[L::RPL][NW][TPW];
+#pragma unroll
+      for (int q = 0; q < L::RPL; ++q) {
+        const int m = m0 + q * kLookupThreads + warp * 32 + lane;
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+#pragma unroll
+          for (int e = 0; e < TPW; ++e) {
+            old[q][w][e] = 0;
+            if (m < p.M && w * TPW + e < ntok_v)
+              old[q][w][e] = atom_add_u64(ws64 + (size_t)m * p.N + n0 + w * TPW + e,
+                                          (1ull << 40) + (unsigned long long)((uint32_t)acc[q][w][e] ^ 0x80000000u));
+          }
+      }
+#pragma unroll
+      for (int q = 0; q < L::RPL; ++q) {
+        const int m = m0 + q * kLookupThreads + warp * 32 + lane;
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+#pragma unroll
+          for (int e = 0; e < TPW; ++e) {
+            const int c = w * TPW + e;
+            if (m < p.M && c < ntok_v && (unsigned)(old[q][w][e] >> 40) == (unsigned)(S - 1)) {
+              const unsigned long long low = (old[q][w][e] & ((1ull << 40) - 1)) +
+                                             (unsigned long long)((uint32_t)acc[q][w][e] ^ 0x80000000u);
+              const int32_t a = (int32_t)(uint32_t)(low - (unsigned long long)S * 0x80000000ull);
+              const size_t o = (size_t)m * p.N + n0 + c;
+              ws64[o] = 0ull;  // zero-kept for the next launch (after its griddepcontrol.wait)
+              if (p.acc_only) {
+                reinterpret_cast<int32_t*>(p.out)[o] = a;
+              } else {
+                const float sc = __fmul_rn(__ldg(p.a_scale + n0 + c), p.w_scale);
+                reinterpret_cast<float*>(p.out)[o] = __fmul_rn((float)a, sc);
+              }
+            }
+          }
+      }
+    } else if (kRedRegs && S > 1 && p.last_only) {
       // small split-K tiles (decode): each thread adds its partial rows
       // straight from registers into the zero-kept workspace (red.add, no
       // shared tile and no bulk copy to wait for); the arrival below -- a CTA
@@ -645,6 +788,10 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
       g0 = ld_relaxed_gpu(p.ws_cnt + 2 * (blockIdx.z * gridDim.y + blockIdx.y) + 1);
   }
   pdl_launch_dependents();
+  if (kA64 && S > 1 && p.last_only) {  // finished element by element above
+    VLUT_STAMP(5);  // (thread 0: its own elements done)
+    return;
+  }
   __syncthreads();  // int32 tile complete
   VLUT_STAMP(4);
 

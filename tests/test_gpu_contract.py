@@ -38,18 +38,20 @@ def _inputs(K, N, seed):
     return oracle.quantize(x)
 
 
-@pytest.mark.parametrize("plan_kind", ["streamk", "streamk_rpt2", "streamk32", "slot_split", "auto"])
+@pytest.mark.parametrize("plan_kind", ["streamk", "streamk_rpt2", "streamk32", "slot_split",
+                                       "slot_decode", "auto"])
 def test_graph_replay_with_new_inputs(v, plan_kind):
     """A captured mpGeMM replayed three times with different activations in
     the same buffers: every replay must equal the oracle.  (With per-launch
     host epochs, a replay would reuse the captured epoch and owners would add
     stale partials -- the handshake must carry no host-side state.)"""
     M, K, g = 1000, 2560, 4
-    N = 8 if plan_kind == "slot_split" else 256
+    N = {"slot_split": 8, "slot_decode": 1}.get(plan_kind, 256)
     plan = {"streamk": v.LaunchPlan(16, 1, streamk=1),
             "streamk_rpt2": v.LaunchPlan(12, 1, m_cta=768, streamk=1),
             "streamk32": v.LaunchPlan(12, 1, m_cta=768, n_cta=32, streamk=1),
             "slot_split": v.slot_plan(tpw=2, splits=5),
+            "slot_decode": v.slot_plan(tpw=1, splits=20),
             "auto": None}[plan_kind]
     W = synth.ternary_weights(M, K, seed=77)
     pw = v.pack_weights(W, g, device=dev())

@@ -119,6 +119,30 @@ def test_slot_fp32_vector_and_scalar(v, M, K, N, g):
         check_fp32(o.cpu().numpy(), ref, s, synth.W_SCALE)
 
 
+@pytest.mark.parametrize("N,tpw", [(1, 1), (2, 2), (1, 2)])
+def test_slot_counted_meeting_extremes(v, N, tpw):
+    """Decode-size tiles meet through counted 64-bit atomics (count << 40 |
+    sum of partial + 2^31): up to 148 partials per element, each at the int32
+    extremes of its K range, positive and negative, must sum exactly, and
+    again on the same workspace (each launch leaves its words zero)."""
+    M, K, g = 1000, 46080, 4
+    W = np.ones((M, K), np.int8)
+    W[1::2] = -1
+    W[2::4] = 0
+    W[3::8, ::3] = 0
+    A = np.full((K, N), -128, np.int8)
+    A[::5] = 127
+    pw = v.pack_weights(W, g, device=dev())
+    ref = oracle.gemm_i32(W, A)
+    ws = torch.zeros_like(v.workspace(dev()))
+    for splits in (2, 45, 148):
+        for rep in range(2):
+            acc = v.mpgemm_acc_ws(pw, to_dev(A), plan=v.slot_plan(tpw=tpw, splits=splits), ws=ws)
+            torch.cuda.synchronize()
+            assert np.array_equal(acc.cpu().numpy(), ref), (splits, rep)
+    assert ref.min() < -2**20 and ref.max() > 2**20
+
+
 def test_slot_workspace_stays_clean_and_deterministic(v):
     # the split-K workspace region must be zero again after every launch:
     # alternate shapes and variants on one workspace, compare each repeat
