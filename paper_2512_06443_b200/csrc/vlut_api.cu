@@ -1066,7 +1066,11 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
     sk.ws = static_cast<int32_t*>(ws);
     sk.flags = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + sk_part_bytes(d.sms));
     sk.epoch = 1u;  // flags are reset by their consumers: graph-replay safe
-    const int grid = (int)(sk.U < d.sms ? sk.U : d.sms);
+    int grid = (int)(sk.U < d.sms ? sk.U : d.sms);
+    if (const char* e = getenv("VLUT_SK_GRID")) {  // (experiment) override the persistent grid
+      const int gx = atoi(e);
+      if (gx > 0 && gx < grid) grid = gx;
+    }
     if (sk32)
       st = acc_only ? dispatch_sk32<true>(W->g, plan.warps, rpt, p, sk, grid, s)
                     : dispatch_sk32<false>(W->g, plan.warps, rpt, p, sk, grid, s);

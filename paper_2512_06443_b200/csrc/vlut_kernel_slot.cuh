@@ -347,7 +347,11 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
   // and both builders released it): config 4 g = 5 N = 1 8.24 -> 7.61 us.
   // With the 8-stage g = 4 ring the bulk copies are as fast or faster
   // (7.54 vs 7.75 us; profiles/r02_decode.txt)
+#ifdef VLUT_SLOT_CP_ALL  // (experiment) per-thread copies at every ring depth
+  constexpr bool kLdgIdx = kCpIdxAll && NW == 1;
+#else
   constexpr bool kLdgIdx = kCpIdxAll && NW == 1 && L::STAGES < 4;
+#endif
   constexpr int PF = kLdgIdx ? L::STAGES : 2;  // kLdgIdx: tiles in flight per thread
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x;
@@ -603,7 +607,9 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
         __syncwarp();
         if (lane == 0) mbar_arrive(mbar + IFREE0 + 8 * st);  // ring slot's index rows consumed
       }
+#ifndef VLUT_SLOT_XNOTAB  // (experiment) lookups do not wait for their table: wrong sums
       mbar_wait(mbar + 8 * B, (t >> 1) & 1);           // table t built
+#endif
       if (t == 0) VLUT_STAMP(2);
 #pragma unroll
       for (int q = 0; q < L::RPL; ++q) {
