@@ -230,8 +230,9 @@ vlut_status vlut_mpgemm_ex(const vlut_packed_weights* W, const int8_t* A,
  *               again) and
  *               per-tile generation words (monotonic, read on the device).
  *               No host-side per-launch state: captured CUDA graphs may be
- *               replayed.  Stream-K and K2 split-K launches are cooperative
- *               (their CTAs wait for each other, so all are co-resident).
+ *               replayed.  Stream-K and K2 split-K launches whose CTAs
+ *               wait for each other are cooperative (all co-resident);
+ *               K2's decode-size tiles meet without waiting and are not.
  * vlut_workspace_bytes() returns 0 without a CUDA device (~36 MB on B200).
  */
 size_t vlut_workspace_bytes(void);

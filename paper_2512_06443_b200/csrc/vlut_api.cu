@@ -629,9 +629,11 @@ vlut_status launch_slot(const vlut::slot::SlotParams& p, int S, int NTt, int MT,
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
-  // split-K CTAs of a tile wait for each other: all CTAs must be co-resident
+  // split-K CTAs of a tile wait for each other (generation handshake): all
+  // CTAs must be co-resident.  Last-only tiles never wait: no cooperative
+  // launch, so the grid may overlap its neighbours (PDL).
   attr[1].id = cudaLaunchAttributeCooperative;
-  attr[1].val.cooperative = S > 1 ? 1 : 0;
+  attr[1].val.cooperative = (S > 1 && !(p.last_only && !getenv("VLUT_SLOT_COOP_ALWAYS"))) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   VLUT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
