@@ -22,7 +22,8 @@ for i, (M, K, N, g) in enumerate(shapes):
 plans = [None, v.LaunchPlan(8, 1), v.LaunchPlan(12, 2), v.LaunchPlan(16, 4),
          v.LaunchPlan(16, 1, streamk=1), v.LaunchPlan(12, 1, m_cta=768, streamk=1),
          v.LaunchPlan(8, 1, m_cta=512, streamk=1), v.slot_plan(tpw=2), v.slot_plan(tpw=1),
-         v.slot_plan(tpw=2, splits=1)]
+         v.slot_plan(tpw=2, splits=1), v.LaunchPlan(12, 1, n_cta=32), v.LaunchPlan(16, 2, n_cta=32),
+         v.LaunchPlan(12, 1, m_cta=768, n_cta=32, streamk=1)]
 streams = [torch.cuda.Stream() for _ in range(3)]
 wss = [torch.zeros_like(v.workspace(dev)) for _ in streams]
 refs = {}
@@ -37,6 +38,8 @@ while time.time() - t0 < secs:
     plan = plans[pi]
     if plan is not None and plan.slot and N > 64:
         plan = None
+    if plan is not None and plan.n_cta == 32 and N % 16:
+        plan = None  # 32-token tiles need N % 16 == 0
     with torch.cuda.stream(streams[si]):
         acc = v.mpgemm_acc_ws(pw, A, plan=plan, ws=wss[si], stream=streams[si])
     pending.append((ci, pi, acc))
