@@ -888,12 +888,15 @@ vlut_status run_slot(const vlut_packed_weights* W, const int8_t* A, const float*
     p.ws_cnt = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + slot_cnt_off(d.sms));
     p.ws_acc = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + slot_acc_off(d.sms));
   }
-  p.last_only =
-      ((long long)pl.m_cta * std::min(N, pl.n_cta) * 4 <= vlut::slot::kLastOnlyBytes) ? 1 : 0;
-  // counted 64-bit meeting (decode): 8-byte words, at most 255 partials
-  if (vlut::slot::kAtom64 && p.last_only &&
-      (S > vlut::slot::kAtom64MaxSplits || (size_t)M * (size_t)N * 8 > kSlotAccBytes))
-    p.last_only = 0;
+  // last_only: no CTA waits for another.  Variants with few tokens per CTA
+  // meet through counted 64-bit atomics (8-byte words, at most 255
+  // partials); the others let the last CTA finish tiles up to 8 KB
+  if (vlut::slot::kAtom64 && pl.nw * tpw <= vlut::slot::kA64MaxTok)
+    p.last_only = (S <= vlut::slot::kAtom64MaxSplits && (size_t)M * (size_t)N * 8 <= kSlotAccBytes)
+                      ? 1 : 0;
+  else
+    p.last_only =
+        ((long long)pl.m_cta * std::min(N, pl.n_cta) * 4 <= vlut::slot::kLastOnlyBytes) ? 1 : 0;
   vlut_status st = dispatch_slot(g, pl.nw, tpw, p, S, (int)NTt, (int)MT,
                                  static_cast<cudaStream_t>(stream));
   if (st != VLUT_OK) return st;

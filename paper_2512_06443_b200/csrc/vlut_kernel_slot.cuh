@@ -127,6 +127,13 @@ constexpr bool kAtom64 = VLUT_SLOT_ATOM64 != 0;
 // The producer then stages only the (tiny) activation tiles.
 constexpr bool kCpIdxAll = VLUT_SLOT_LDG != 0;
 constexpr int kAtom64MaxSplits = 255;
+#ifndef VLUT_SLOT_A64_TOK
+#define VLUT_SLOT_A64_TOK 2
+#endif
+// variants with at most this many tokens per CTA meet through the counted
+// 64-bit atomics (whatever their tile size); wider ones keep the bulk
+// reduce-add + generation handshake
+constexpr int kA64MaxTok = VLUT_SLOT_A64_TOK;
 
 template <int G, int NW, int TPW>
 struct SL {
@@ -340,8 +347,7 @@ __device__ __forceinline__ int act_value(const SlotParams& p, uint32_t act_s, in
 template <int G, int NW, int TPW>
 __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_constant__ SlotParams p) {
   using L = SL<G, NW, TPW>;
-  // last-only tiles hold <= 8 KB: at >= 1024 rows per CTA, <= 2 tokens
-  constexpr bool kA64 = kAtom64 && L::NTOK <= 2;
+  constexpr bool kA64 = kAtom64 && L::NTOK <= kA64MaxTok;
   // per-thread copies where the ring is short (g = 5: 2 stages beside the
   // 243-row tables; a bulk stage is refilled only after all 16 lookup warps
   // and both builders released it): config 4 g = 5 N = 1 8.24 -> 7.61 us.

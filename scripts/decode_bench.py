@@ -46,8 +46,11 @@ def run(libpath):
     dev = torch.device("cuda")
     ws = v.workspace(dev)
     res = []
-    for (M, K, N, g) in [(3072, 23040, 1, 4), (3072, 23040, 1, 5), (6912, 2560, 1, 4),
-                         (2560, 6912, 1, 4), (3072, 23040, 16, 4), (3072, 23040, 64, 4)]:
+    shapes = [(3072, 23040, 1, 4), (3072, 23040, 1, 5), (6912, 2560, 1, 4),
+              (2560, 6912, 1, 4), (3072, 23040, 16, 4), (3072, 23040, 64, 4)]
+    if os.environ.get("DECODE_SHAPES"):  # "M,K,N,g;M,K,N,g;..."
+        shapes = [tuple(int(x) for x in t.split(",")) for t in os.environ["DECODE_SHAPES"].split(";")]
+    for (M, K, N, g) in shapes:
         W = torch.from_numpy(synth.ternary_weights(M, K, 1)).to(dev)
         pw0 = v.pack_weights_device(W, g)
         copies = int(min(96, max(2, -(-300_000_000 // pw0.nbytes))))
