@@ -613,9 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
         __syncwarp();
         if (lane == 0) mbar_arrive(mbar + IFREE0 + 8 * st);  // ring slot's index rows consumed
       }
-#ifndef VLUT_SLOT_XNOTAB  // (experiment) lookups do not wait for their table: wrong sums
       mbar_wait(mbar + 8 * B, (t >> 1) & 1);           // table t built
-#endif
       if (t == 0) VLUT_STAMP(2);
 #pragma unroll
       for (int q = 0; q < L::RPL; ++q) {
