@@ -503,13 +503,18 @@ double plan_sk32(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
   const int half_rows = (pow3i(g) + 1) / 2;
   double best_cost = 1e300;
   if (getenv("VLUT_NO_SK32") || getenv("VLUT_NO_K32")) return best_cost;
-  // Only 12 warps x 2 rows is planned: 12 x 1 / 16 x 1 lost to the cluster
-  // K1-32 and K1-SK everywhere they were measured, 16 x 2 and 12 x 4 rows
-  // spill (3-30 % slower).  The split-tile epilogues work per thread row
+  // 12 warps x 2 rows is planned (and 12 x 1 at g = 5, below): 16 x 1 lost
+  // to the cluster K1-32 and K1-SK everywhere it was measured, 16 x 2 and
+  // 12 x 4 rows spill (3-30 % slower).  The split-tile epilogues work per thread row
   // (~16 B/clk): a CTA typically has a producer and an owner segment.
-  const int warps_opts[1] = {12};
-  const int rpt_opts[1] = {2};
-  for (int wi = 0; wi < 1; ++wi) {
+  // 12 x 1 as well at g = 5, where it replaces K1-SK at mid N (config 4
+  // N = 64: 115.8 -> 107.4 us); at g = 4 its cost model also picks it where
+  // the cluster K1-32 is faster (configs[1] weights N = 80 / 96: 39.5 -> 45.3
+  // us; profiles/r02_sk32_plan_r1.txt), so g = 4 plans 12 x 2 only
+  const int warps_opts[2] = {12, 12};
+  const int rpt_opts[2] = {2, 1};
+  const int n_opts = (g == 5) ? 2 : 1;
+  for (int wi = 0; wi < n_opts; ++wi) {
     const int warps = warps_opts[wi], rpt = rpt_opts[wi];
     if (smem_bytes_sk32(g, warps, rpt) > 232448) continue;  // 227 KB opt-in per CTA
     const int mcta = 32 * warps * rpt;

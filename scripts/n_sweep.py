@@ -7,6 +7,8 @@ import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2512_06443_b200 as v
 from paper_2512_06443_b200 import synth
+if len(sys.argv) > 1:  # optional libvlut.so build to sweep
+    v.lib_path = os.path.abspath(sys.argv[1])
 dev = torch.device("cuda")
 M, K, g = 6912, 2560, 4
 R_LU = 148 * 64 * 1965e6
