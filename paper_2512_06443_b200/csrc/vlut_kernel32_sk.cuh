@@ -137,6 +137,15 @@ __device__ __forceinline__ void sk32_epilogue(const Params& p, const SkParams& s
   }
 }
 
+// The raw-int32 variant's epilogue as a real call: inlined, ptxas spilled
+// registers inside that variant's lookup loop (the fp32 variant is clean).
+template <int G, int WARPS, int RPT>
+__device__ __noinline__ void sk32_epilogue_acc(const Params& p, const SkParams& sk, const SkSeg sg,
+                                               int KT, int cta, int NCTA, int tid, int lane,
+                                               uint32_t taddr0) {
+  sk32_epilogue<G, WARPS, RPT, true>(p, sk, sg, KT, cta, NCTA, tid, lane, taddr0);
+}
+
 template <int G, int WARPS, int RPT, bool ACC_ONLY>
 __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
     vlut_mpgemm32_sk_kernel(const __grid_constant__ Params p, const SkParams sk) {
@@ -271,7 +280,10 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
         first = false;
       }
       if (seg_end) {
-        sk32_epilogue<G, WARPS, RPT, ACC_ONLY>(p, sk, cur.seg, KT, cta, NCTA, tid, lane, taddr0);
+        if constexpr (ACC_ONLY)
+          sk32_epilogue_acc<G, WARPS, RPT>(p, sk, cur.seg, KT, cta, NCTA, tid, lane, taddr0);
+        else
+          sk32_epilogue<G, WARPS, RPT, false>(p, sk, cur.seg, KT, cta, NCTA, tid, lane, taddr0);
         first = true;  // the next segment re-initialises TMEM
       }
       cur.next();
