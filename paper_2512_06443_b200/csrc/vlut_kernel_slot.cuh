@@ -95,7 +95,10 @@ __device__ __forceinline__ void stage_idx(uint32_t dst, const uint8_t* src, int 
   for (int o = 0; o < bytes; o += piece)
     bulk_g2s(dst + o, src + o, (uint32_t)min(piece, bytes - o), mbar);
 }
-constexpr int kLastOnlyBytes = 8192;              // split-K tiles up to this size: the last CTA finishes them
+#ifndef VLUT_SLOT_LAST_ONLY_BYTES
+#define VLUT_SLOT_LAST_ONLY_BYTES 8192
+#endif
+constexpr int kLastOnlyBytes = VLUT_SLOT_LAST_ONLY_BYTES;  // split-K tiles up to this size: the last CTA finishes them
 #ifndef VLUT_SLOT_BULK_SMALL
 constexpr bool kRedRegs = true;   // last-only tiles: partials added by red.add from registers
 #else
