@@ -28,7 +28,7 @@ PLANS = {"auto": None, "c12x2": (12, 2, 0, 0), "w12r2": (12, 1, 768, 1), "w8r2":
          "sk32w12r1": (12, 1, 384, 1, 32), "sk32w16r1": (16, 1, 512, 1, 32),
          "sk32w12r2": (12, 1, 768, 1, 32), "sk32w16r2": (16, 1, 1024, 1, 32),
          "sk32w12r4": (12, 1, 1536, 1, 32), "sk32w12r3": (12, 1, 1152, 1, 32),
-         "sk32w8r3": (8, 1, 768, 1, 32)}
+         "sk32w8r3": (8, 1, 768, 1, 32), "sk32w8r2": (8, 1, 512, 1, 32)}
 
 
 def main():
