@@ -36,7 +36,10 @@ namespace vlut {
 // config 4 g = 5 N = 1024 1089 -> 1073 us; at g = 4 the eager form is ~1.5 %
 // faster on config 5's gate shape).
 template <int G, int WARPS, int RPT>
-constexpr bool kLazyRx = (G == 5 && RPT == 2 && WARPS == 12);
+#ifndef VLUT_SK_LAZY16
+#define VLUT_SK_LAZY16 0
+#endif
+constexpr bool kLazyRx = (G == 5 && RPT == 2 && WARPS == 12) || (VLUT_SK_LAZY16 && WARPS == 16);
 
 struct SkParams {
   int NT, MT;           // N-tiles, M-tiles
