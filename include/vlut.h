@@ -261,6 +261,28 @@ vlut_status vlut_mpgemm_scalar_lut(const vlut_packed_weights* W, const int8_t* A
                                    int N, const vlut_launch_plan* plan, void* workspace,
                                    size_t ws_bytes, void* stream);
 
+/*
+ * Fused decode step (one token, N = 1): the per-token int8 quantization of
+ * the activation (s = absmax / 127, 1 if absmax is 0; q =
+ * clamp(round-half-away(x / s), +-127)) and the scalar-LUT mpGeMM + fp32
+ * dequant of vlut_mpgemm_scalar_lut in ONE launch: every CTA of the K2 decode
+ * kernel takes the absmax of x itself and its table builders quantize the
+ * features they need, so there is no quantizer launch and no int8 round trip
+ * (the scalar LUT for decoding).  Results are bit-identical to
+ * vlut_quantize followed by vlut_mpgemm_scalar_lut.
+ *   x         : device fp32 [K] (the token's activations; 16-B alignment and
+ *               K % 4 == 0 take the vector path), may be the previous
+ *               kernel's output (read after griddepcontrol.wait)
+ *   out       : device fp32 [M]
+ *   scale_out : device fp32 [1] <- s, or NULL
+ *   workspace : as vlut_mpgemm_ws, or NULL for the library's per-stream one
+ * Errors: INVALID_ARGUMENT, SHAPE / CORRUPT_DESCRIPTOR (descriptor), MISALIGNED
+ * (x / out / scale_out not 4-B aligned), CUDA.
+ */
+vlut_status vlut_mpgemm_decode(const vlut_packed_weights* W, const float* x, float w_scale,
+                               float* out, float* scale_out, int M, int K, void* workspace,
+                               size_t ws_bytes, void* stream);
+
 /* Raw int32 accumulators, no scales (bit-exact test hook):
  *   acc_out : device int32 [M][N].  Other arguments as vlut_mpgemm_ex. */
 vlut_status vlut_mpgemm_acc(const vlut_packed_weights* W, const int8_t* A,

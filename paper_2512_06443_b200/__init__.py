@@ -24,6 +24,7 @@ __all__ = [
     "VlutError", "PackedWeights", "LaunchPlan", "lib", "lib_path", "packed_bytes",
     "pack_weights", "pack_weights_device", "unpack_weights_host", "plan", "mpgemm",
     "mpgemm_ex", "mpgemm_acc", "quantize", "last_error", "EXPORTS", "group_schedule",
+    "mpgemm_decode",
     "MixedPackedWeights", "pack_weights_mixed", "mpgemm_mixed", "mpgemm_layout", "quantize_t",
     "linear", "workspace", "plan_ws", "mpgemm_ws", "mpgemm_acc_ws", "mpgemm_fused",
     "quantize_amax", "mpgemm_scalar_lut", "slot_plan", "mpgemm_allgather",
@@ -138,6 +139,9 @@ EXPORTS = {
                                 ctypes.c_float, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                 ctypes.c_int, ctypes.POINTER(_Plan), ctypes.c_void_p,
                                 ctypes.c_size_t, ctypes.c_void_p], ctypes.c_int),
+    "vlut_mpgemm_decode": ([ctypes.POINTER(_Desc), ctypes.c_void_p, ctypes.c_float,
+                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                            ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p], ctypes.c_int),
     "vlut_mpgemm_allgather": ([ctypes.POINTER(_Desc), ctypes.c_void_p, ctypes.c_void_p,
                                ctypes.c_float, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
@@ -697,6 +701,32 @@ def mpgemm_scalar_lut(W: PackedWeights, A, a_scale, w_scale: float, out=None,
                                             float(w_scale), op, M, K, N, pp, wsp, wsn,
                                             ctypes.c_void_p(st.cuda_stream)))
     return out
+
+
+def mpgemm_decode(W: PackedWeights, x, w_scale: float, out=None, scale_out=None, ws=None,
+                  stream=None):
+    """Fused decode step (N = 1): fp32 activations x [K] (or [K][1]) -> fp32
+    out [M], quantization inside the K2 decode kernel (vlut_mpgemm_decode);
+    bit-identical to quantize() + mpgemm_scalar_lut().  Returns (out, scale)."""
+    import torch
+    if x.dim() == 2 and x.shape[1] == 1:
+        x = x.reshape(-1)
+    if x.dim() != 1:
+        raise ValueError("x: expected fp32 [K] (one token)")
+    K = x.shape[0]
+    dev = x.device
+    M = W.M
+    st = _stream(stream, dev)
+    xp = _arg(x, "x", torch.float32, (K,), dev)
+    out, op = _out(out, (M,), torch.float32, dev)
+    scale_out, sp = _out(scale_out, (1,), torch.float32, dev, "scale_out")
+    if ws is None:
+        ws = workspace(dev, st)
+    wsp, wsn = _ws_arg(ws, dev)
+    with torch.cuda.device(dev):
+        _check(lib().vlut_mpgemm_decode(_weights(W, K, dev), xp, float(w_scale), op, sp, M, K,
+                                        wsp, wsn, ctypes.c_void_p(st.cuda_stream)))
+    return out, scale_out
 
 
 # ---------------------------------------------------------------- fused all-gather (a8)

@@ -845,7 +845,8 @@ constexpr int kSlotAutoMaxN = 64;
 
 vlut_status run_slot(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,
                      float w_scale, void* out, int M, int K, int N, vlut_launch_plan plan,
-                     void* ws, size_t ws_bytes, void* stream, bool acc_only, const DeviceInfo& d) {
+                     void* ws, size_t ws_bytes, void* stream, bool acc_only, const DeviceInfo& d,
+                     const float* xq = nullptr, float* scale_out = nullptr) {
   const int g = W->g;
   const int tpw = plan.tpw ? plan.tpw : 2;
   const bool have_ws = ws != nullptr;
@@ -888,7 +889,10 @@ vlut_status run_slot(const vlut_packed_weights* W, const int8_t* A, const float*
   p.kg_tiles = W->kg_tiles;
   p.splits = S;
   p.acc_only = acc_only ? 1 : 0;
-  p.act_tma = (N <= vlut::slot::kActNMax && (((uintptr_t)A) & 15) == 0) ? 1 : 0;
+  p.act_tma = (!xq && N <= vlut::slot::kActNMax && (((uintptr_t)A) & 15) == 0) ? 1 : 0;
+  p.xq = xq;
+  p.scale_out = scale_out;
+  p.q_ring = getenv("VLUT_DECODE_NO_RING") ? 0 : 1;  // (test switch: the fallback path)
   if (have_ws) {
     p.ws_cnt = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + slot_cnt_off(d.sms));
     p.ws_acc = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + slot_acc_off(d.sms));
@@ -1445,6 +1449,32 @@ vlut_status vlut_mpgemm_scalar_lut(const vlut_packed_weights* W, const int8_t* A
   pl.tpw = 1;
   return run_mpgemm(W, A, a_scale, w_scale, out, M, K, N, &pl, stream, false, nullptr, 0,
                     workspace, ws_bytes);
+}
+
+vlut_status vlut_mpgemm_decode(const vlut_packed_weights* W, const float* x, float w_scale,
+                               float* out, float* scale_out, int M, int K, void* workspace,
+                               size_t ws_bytes, void* stream) {
+  if (M < 0 || K <= 0) return fail(VLUT_ERR_INVALID_ARGUMENT, "bad sizes M=%d K=%d", M, K);
+  if (M == 0) return ok();
+  vlut_status st = check_desc(W, M, K);
+  if (st != VLUT_OK) return st;
+  if (!x || !out) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL device pointer");
+  if ((((uintptr_t)x) | ((uintptr_t)out) | ((uintptr_t)scale_out)) & 3)
+    return fail(VLUT_ERR_MISALIGNED, "x / out / scale_out not 4-B aligned");
+  DeviceInfo d;
+  st = device_info(&d);
+  if (st != VLUT_OK) return st;
+  std::unique_lock<std::mutex> lk(g_ws_mu, std::defer_lock);
+  if (!workspace) {  // the library's per-stream workspace, as vlut_mpgemm
+    lk.lock();
+    internal_workspace_locked(stream, &workspace, &ws_bytes);
+  }
+  const bool have_ws = workspace && ws_bytes >= sk_workspace_bytes(d.sms) &&
+                       ((uintptr_t)workspace & 15) == 0;
+  vlut_launch_plan sl = {};
+  plan_slot(M, K, 1, W->g, d.sms, 1, 1, 0, have_ws, &sl);  // one scalar word: N = 1
+  return run_slot(W, nullptr, nullptr, w_scale, out, M, K, 1, sl, have_ws ? workspace : nullptr,
+                  ws_bytes, stream, false, d, x, scale_out);
 }
 
 vlut_status vlut_mpgemm_allgather(const vlut_packed_weights* W, const int8_t* A,

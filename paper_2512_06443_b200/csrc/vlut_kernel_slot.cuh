@@ -164,7 +164,8 @@ struct SL {
   static constexpr int ACT_OFF = IDX_OFF + STAGES * IDX_BYTES;
   static constexpr int MBAR_OFF = ACT_OFF + STAGES * ACT_BYTES;  // FULL[2] EMPTY[2] STG[S] IFREE[S]
   static constexpr int MISC_OFF = MBAR_OFF + 32 + 16 * kMaxStages;
-  static constexpr int SMEM = MISC_OFF + 16;
+  static constexpr int FUSE_OFF = MISC_OFF + 16;  // fused decode: 16 warp maxima + the scale
+  static constexpr int SMEM = FUSE_OFF + 80;
   static constexpr int BIAS = (TPW == 2) ? 128 * G : 0;
   static_assert(TPW == 1 || TPW == 2, "1 or 2 tokens per table word");
   static_assert(STAGES >= 2, "staging ring needs two stages");
@@ -189,7 +190,23 @@ struct SlotParams {
                            // between launches, generation monotonic
   int last_only;           // splits > 1: 1 = the last CTA to arrive finishes the whole tile
                            // (small tiles), 0 = every CTA finishes 1/S of it
+  // fused decode (vlut_mpgemm_decode, N = 1): the fp32 activations [K]; every
+  // CTA takes their absmax itself (all of K, from L2 after the first reader),
+  // s = amax / 127 (1 if 0), and its builders quantize q = clamp(round(x /
+  // s), +-127) -- K3's arithmetic, bit for bit -- so no quantizer launch and
+  // no int8 round trip.  A / a_scale unused; scale_out (optional) <- s.
+  const float* xq;
+  float* scale_out;
+  int q_ring;              // fused decode: 1 = codes through shared memory when the CTA's
+                           // slice fits the activation ring (0: per-tile global reads)
 };
+
+// K3's code (vlut_aux_kernels.cuh q_code): the same IEEE division and rounding
+__device__ __forceinline__ int slot_q_code(float v, float s) {
+  float r = roundf(__fdiv_rn(v, s));
+  r = fminf(fmaxf(r, -127.f), 127.f);
+  return (int)r;
+}
 
 __device__ __forceinline__ void red_add_s32(int32_t* p, int32_t v) {
   asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
@@ -451,6 +468,11 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
     const int bw = warp - kLW;
     const int j = lane & 15;
     pdl_wait();  // the global-memory tail of A comes from the previous kernel
+    float xs = 1.f;  // fused decode: the token's scale, from the lookup warps
+    if (p.xq) {
+      bar_sync(2, (kLW + kBW) * 32);
+      xs = *reinterpret_cast<const float*>(smem + L::FUSE_OFF + 64);
+    }
 #pragma unroll 1
     for (int t = 0; t < ntiles; ++t) {
       const int b = t & 1, st = t % L::STAGES;
@@ -506,7 +528,13 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
           for (int r = 0; r < G; ++r) {
             const int k = k0 + j * G + r;
             if constexpr (TPW == 1) {
-              U[wi][r] = (uint32_t)act_value(p, as, ab, k0, k, n0 + w);
+              if (p.xq)  // fused decode (N = 1): the code the lookup warps stored, or now
+                U[wi][r] = (p.q_ring && ntiles * kKgTile * G <= L::STAGES * L::ACT_BYTES)
+                               ? (uint32_t)(int32_t)reinterpret_cast<const int8_t*>(
+                                     smem + L::ACT_OFF)[t * kKgTile * G + j * G + r]
+                               : (uint32_t)(k < p.K ? slot_q_code(__ldg(p.xq + k), xs) : 0);
+              else
+                U[wi][r] = (uint32_t)act_value(p, as, ab, k0, k, n0 + w);
             } else {
               const int nn = n0 + 2 * w;
               U[wi][r] = (uint32_t)(act_value(p, as, ab, k0, k, nn) + 128) |
@@ -573,6 +601,75 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
     if constexpr (kLdgIdx) {
       cp_tile(0);
       cp_tile(1);
+    }
+    if (p.xq) {
+      // fused decode: the token's absmax over all K (the weight stream is
+      // already in flight), s = amax / 127, handed to the builders
+      pdl_wait();  // x may be the previous kernel's output
+      float mx = 0.f;
+      // every load of a round issued before any use (one L2 round trip per
+      // round, not per load: 12 x 16 B per thread covers K = 24576)
+      constexpr int QU = 12;
+      if ((p.K & 3) == 0 && (((uintptr_t)p.xq) & 15) == 0) {
+        const float4* x4 = reinterpret_cast<const float4*>(p.xq);
+        const int n4 = p.K / 4;
+        for (int i0 = tid; i0 < n4; i0 += QU * kLookupThreads) {
+          float4 a[QU];
+#pragma unroll
+          for (int u = 0; u < QU; ++u) {
+            const int i = i0 + u * kLookupThreads;
+            a[u] = i < n4 ? __ldg(x4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int u = 0; u < QU; ++u)
+            mx = fmaxf(fmaxf(mx, fabsf(a[u].x)),
+                       fmaxf(fabsf(a[u].y), fmaxf(fabsf(a[u].z), fabsf(a[u].w))));
+        }
+      } else {
+        for (int i0 = tid; i0 < p.K; i0 += QU * kLookupThreads) {
+          float a[QU];
+#pragma unroll
+          for (int u = 0; u < QU; ++u) {
+            const int i = i0 + u * kLookupThreads;
+            a[u] = i < p.K ? __ldg(p.xq + i) : 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < QU; ++u) mx = fmaxf(mx, fabsf(a[u]));
+        }
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+      float* red = reinterpret_cast<float*>(smem + L::FUSE_OFF);
+      if (lane == 0) red[warp] = mx;
+      bar_sync(1, kLookupThreads);
+      float a = red[0];
+#pragma unroll
+      for (int w = 1; w < kLW; ++w) a = fmaxf(a, red[w]);
+      const float sc = (a == 0.f) ? 1.f : __fdiv_rn(a, 127.f);
+      if (tid == 0) {
+        red[16] = sc;
+        if (p.scale_out && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) *p.scale_out = sc;
+      }
+      // this CTA's K slice quantized into the (otherwise unused) activation
+      // ring, so the builders read codes from shared memory instead of
+      // paying a global-memory round trip per K-tile
+      const int nq = ntiles * kKgTile * G;
+      if (p.q_ring && nq <= L::STAGES * L::ACT_BYTES) {
+        int8_t* qs = reinterpret_cast<int8_t*>(smem + L::ACT_OFF);
+        const int kb = kt0 * kKgTile * G;
+        for (int e0 = tid; e0 < nq; e0 += QU * kLookupThreads) {
+          float xv[QU];
+#pragma unroll
+          for (int u = 0; u < QU; ++u) {
+            const int k = kb + e0 + u * kLookupThreads;
+            xv[u] = (e0 + u * kLookupThreads < nq && k < p.K) ? __ldg(p.xq + k) : 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < QU; ++u)
+            if (e0 + u * kLookupThreads < nq) qs[e0 + u * kLookupThreads] = (int8_t)slot_q_code(xv[u], sc);
+        }
+      }
+      bar_sync(2, (kLW + kBW) * 32);  // the builders wait here for red[16] and the codes
     }
     // one K-tile with table buffer B (compile time: the buffer offset folds
     // into the LDS immediate, one PRMT forms the rest of each address)
@@ -770,7 +867,8 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
               if (p.acc_only) {
                 reinterpret_cast<int32_t*>(p.out)[o] = a;
               } else {
-                const float sc = __fmul_rn(__ldg(p.a_scale + n0 + c), p.w_scale);
+                const float sc = __fmul_rn(p.xq ? *reinterpret_cast<const float*>(smem + L::FUSE_OFF + 64)
+                                                : __ldg(p.a_scale + n0 + c), p.w_scale);
                 reinterpret_cast<float*>(p.out)[o] = __fmul_rn((float)a, sc);
               }
             }
@@ -904,7 +1002,8 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
         if (p.acc_only) {
           reinterpret_cast<int32_t*>(p.out)[o] = a[b];
         } else {
-          const float sc = __fmul_rn(__ldg(p.a_scale + n0 + c), p.w_scale);
+          const float sc = __fmul_rn(p.xq ? *reinterpret_cast<const float*>(smem + L::FUSE_OFF + 64)
+                                                : __ldg(p.a_scale + n0 + c), p.w_scale);
           reinterpret_cast<float*>(p.out)[o] = __fmul_rn((float)a[b], sc);
         }
       }

@@ -66,12 +66,21 @@ def run(libpath):
                 v.mpgemm_ws(p_, A, s, 0.02, out=out, ws=ws)
             return f
         tp = bench([pair(p) for p in pws])
+        tf = None
+        if N == 1 and hasattr(v, "mpgemm_decode"):
+            xf = x[:, 0].contiguous()
+            of = torch.empty((M,), device=dev)
+            sf = torch.empty((1,), device=dev)
+            tf = bench([(lambda p_: (lambda: v.mpgemm_decode(p_, xf, 0.02, out=of, scale_out=sf,
+                                                              ws=ws)))(p) for p in pws])
         pl = v.plan_ws(M, K, N, g)
-        r = dict(M=M, K=K, N=N, g=g, us=t, us_pair=tp, frac_hbm=hbm / HBM / (t * 1e-6),
+        r = dict(M=M, K=K, N=N, g=g, us=t, us_pair=tp, us_fused=tf,
+                 frac_hbm=hbm / HBM / (t * 1e-6),
                  plan=f"slot={pl.slot} tpw={pl.tpw} nw={pl.nw} S={pl.splits}")
         res.append(r)
+        fused = f"  fused decode {tf:7.2f} us" if tf is not None else ""
         print(f"{os.path.basename(libpath or 'libvlut.so'):24s} M={M:5d} K={K:5d} N={N:3d} g={g}: "
-              f"{t:7.2f} us (frac HBM {r['frac_hbm']:.3f})  quantize+mpgemm {tp:7.2f} us  "
+              f"{t:7.2f} us (frac HBM {r['frac_hbm']:.3f})  quantize+mpgemm {tp:7.2f} us{fused}  "
               f"[{r['plan']}]", flush=True)
         del pws, pw0, W
         torch.cuda.empty_cache()

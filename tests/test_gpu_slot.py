@@ -233,3 +233,69 @@ def test_north_star_mpgemm_under_graph_capture(v):
     g.replay()
     torch.cuda.synchronize()
     check_fp32(out.cpu().numpy(), oracle.gemm_i32(W, q), s, synth.W_SCALE)
+
+
+@pytest.mark.parametrize("M,K,g,kind", [(3072, 23040, 4, "normal"), (3072, 23040, 5, "normal"),
+                                        (6912, 2560, 4, "normal"), (1000, 1300, 4, "normal"),
+                                        (70, 85, 5, "normal"), (2100, 1283, 5, "padk"),
+                                        (700, 640, 4, "zeros"), (700, 640, 4, "huge"),
+                                        (1000, 1300, 4, "unaligned")])
+def test_fused_decode_matches_oracle(v, M, K, g, kind):
+    """vlut_mpgemm_decode (N = 1): quantization inside the K2 decode kernel.
+    The scale and the fp32 output must be bit-identical to the oracle's
+    quantize -> int32 GEMM -> fp32 dequant, for ragged M / K, a zero-padded
+    last g = 5 group, an all-zero token (scale 1), values at the int8 clamp and
+    an unaligned x (scalar absmax path)."""
+    W = synth.ternary_weights(M, K, seed=M + K)
+    x = synth.activations_f32(K, 1, seed=K)[:, 0].copy()
+    if kind == "zeros":
+        x[:] = 0.0
+    elif kind == "huge":
+        x *= 1e30
+        x[::7] = -3e38
+    pw = v.pack_weights(W, g, device=dev(), pad_k=(kind == "padk"))
+    q, s = oracle.quantize(x[:, None])
+    ref = oracle.dequant_f32(oracle.gemm_i32(W, q), s, synth.W_SCALE)[:, 0]
+    if kind == "unaligned":
+        buf = torch.zeros(K + 1, dtype=torch.float32, device=dev())
+        buf[1:] = to_dev(x)
+        xd = buf[1:]
+    else:
+        xd = to_dev(x)
+    for rep in range(2):  # the workspace words must be zero again after each launch
+        out, sc = v.mpgemm_decode(pw, xd, synth.W_SCALE)
+        torch.cuda.synchronize()
+        assert np.array_equal(sc.cpu().numpy().view(np.int32), s.view(np.int32)), rep
+        assert np.array_equal(out.cpu().numpy().view(np.int32), ref.view(np.int32)), rep
+
+
+def test_fused_decode_global_code_path(v, monkeypatch):
+    """The builders' fallback (each feature quantized from global memory when
+    a CTA's K slice does not fit the activation ring), forced on."""
+    monkeypatch.setenv("VLUT_DECODE_NO_RING", "1")
+    for (M, K, g) in [(3072, 23040, 4), (2100, 1283, 5)]:
+        W = synth.ternary_weights(M, K, seed=K)
+        x = synth.activations_f32(K, 1, seed=M)[:, 0].copy()
+        pw = v.pack_weights(W, g, device=dev(), pad_k=(K % g != 0))
+        q, s = oracle.quantize(x[:, None])
+        ref = oracle.dequant_f32(oracle.gemm_i32(W, q), s, synth.W_SCALE)[:, 0]
+        out, sc = v.mpgemm_decode(pw, to_dev(x), synth.W_SCALE)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.int32), ref.view(np.int32))
+
+
+def test_fused_decode_equals_quantize_then_scalar_lut(v):
+    """The fused step and the two-launch step (quantize, then the scalar-LUT
+    mpGeMM) are the same computation: identical bits, chained over 5 layers
+    where each layer's output is the next one's input."""
+    M = K = 2560
+    pws = [v.pack_weights(synth.ternary_weights(M, K, seed=900 + i), 4, device=dev())
+           for i in range(5)]
+    x = to_dev(synth.activations_f32(K, 1, seed=31)[:, 0].copy())
+    a = b = x
+    for pw in pws:
+        a, _ = v.mpgemm_decode(pw, a, synth.W_SCALE)
+        qb, sb = v.quantize(b[:, None].contiguous())
+        b = v.mpgemm_scalar_lut(pw, qb, sb, synth.W_SCALE)[:, 0].contiguous()
+    torch.cuda.synchronize()
+    assert torch.equal(a.view(torch.int32), b.view(torch.int32))
