@@ -614,10 +614,10 @@ double plan_slot(int M, int K, int N, int g, int sms, int tpw, int nw_force, int
 }
 
 // ------------------------------------------------------------ launches
-template <int G, int NW, int TPW>
+template <int G, int NW, int TPW, bool FQ = false>
 vlut_status launch_slot(const vlut::slot::SlotParams& p, int S, int NTt, int MT, cudaStream_t st) {
   using L = vlut::slot::SL<G, NW, TPW>;
-  auto kern = vlut::slot::vlut_slot_kernel<G, NW, TPW>;
+  auto kern = vlut::slot::vlut_slot_kernel<G, NW, TPW, FQ>;
   static std::once_flag flags[64];
   static cudaError_t errs[64];
   int dev = 0;
@@ -659,6 +659,11 @@ int slot_smem(int g, int nw, int tpw) {
 
 vlut_status dispatch_slot(int g, int nw, int tpw, const vlut::slot::SlotParams& p, int S, int NTt,
                           int MT, cudaStream_t st) {
+  if (p.xq) {  // fused decode: one scalar word
+    if (nw == 1 && tpw == 1 && g == 4) return launch_slot<4, 1, 1, true>(p, S, NTt, MT, st);
+    if (nw == 1 && tpw == 1 && g == 5) return launch_slot<5, 1, 1, true>(p, S, NTt, MT, st);
+    return fail(VLUT_ERR_UNSUPPORTED, "fused decode: nw = tpw = 1 only");
+  }
 #define X(G_, NW_, TPW_) \
   if (g == G_ && nw == NW_ && tpw == TPW_) return launch_slot<G_, NW_, TPW_>(p, S, NTt, MT, st);
   VLUT_SLOT_VARIANTS(X)

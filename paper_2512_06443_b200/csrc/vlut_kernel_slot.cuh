@@ -364,9 +364,12 @@ __device__ __forceinline__ int act_value(const SlotParams& p, uint32_t act_s, in
   return (int)__ldg(p.A + (size_t)k * p.N + n);
 }
 
-template <int G, int NW, int TPW>
+// FQ: the fused-decode instantiation (vlut_mpgemm_decode; NW = TPW = 1), a
+// separate kernel so the int8-input kernels carry none of its code
+template <int G, int NW, int TPW, bool FQ = false>
 __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_constant__ SlotParams p) {
   using L = SL<G, NW, TPW>;
+  static_assert(!FQ || (NW == 1 && TPW == 1), "fused decode: one scalar word");
   constexpr bool kA64 = kAtom64 && L::NTOK <= kA64MaxTok;
   // per-thread copies where the ring is short (g = 5: 2 stages beside the
   // 243-row tables; a bulk stage is refilled only after all 16 lookup warps
@@ -469,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
     const int j = lane & 15;
     pdl_wait();  // the global-memory tail of A comes from the previous kernel
     float xs = 1.f;  // fused decode: the token's scale, from the lookup warps
-    if (p.xq) {
+    if constexpr (FQ) {
       bar_sync(2, (kLW + kBW) * 32);
       xs = *reinterpret_cast<const float*>(smem + L::FUSE_OFF + 64);
     }
@@ -528,13 +531,14 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
           for (int r = 0; r < G; ++r) {
             const int k = k0 + j * G + r;
             if constexpr (TPW == 1) {
-              if (p.xq)  // fused decode (N = 1): the code the lookup warps stored, or now
+              if constexpr (FQ) {  // fused decode (N = 1): the code the lookup warps stored, or now
                 U[wi][r] = (p.q_ring && ntiles * kKgTile * G <= L::STAGES * L::ACT_BYTES)
                                ? (uint32_t)(int32_t)reinterpret_cast<const int8_t*>(
                                      smem + L::ACT_OFF)[t * kKgTile * G + j * G + r]
                                : (uint32_t)(k < p.K ? slot_q_code(__ldg(p.xq + k), xs) : 0);
-              else
+              } else {
                 U[wi][r] = (uint32_t)act_value(p, as, ab, k0, k, n0 + w);
+              }
             } else {
               const int nn = n0 + 2 * w;
               U[wi][r] = (uint32_t)(act_value(p, as, ab, k0, k, nn) + 128) |
@@ -602,7 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
       cp_tile(0);
       cp_tile(1);
     }
-    if (p.xq) {
+    if constexpr (FQ) {
       // fused decode: the token's absmax over all K (the weight stream is
       // already in flight), s = amax / 127, handed to the builders
       pdl_wait();  // x may be the previous kernel's output
@@ -867,7 +871,7 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
               if (p.acc_only) {
                 reinterpret_cast<int32_t*>(p.out)[o] = a;
               } else {
-                const float sc = __fmul_rn(p.xq ? *reinterpret_cast<const float*>(smem + L::FUSE_OFF + 64)
+                const float sc = __fmul_rn(FQ ? *reinterpret_cast<const float*>(smem + L::FUSE_OFF + 64)
                                                 : __ldg(p.a_scale + n0 + c), p.w_scale);
                 reinterpret_cast<float*>(p.out)[o] = __fmul_rn((float)a, sc);
               }
@@ -1002,7 +1006,7 @@ __global__ void __launch_bounds__(kThreads, 1) vlut_slot_kernel(const __grid_con
         if (p.acc_only) {
           reinterpret_cast<int32_t*>(p.out)[o] = a[b];
         } else {
-          const float sc = __fmul_rn(p.xq ? *reinterpret_cast<const float*>(smem + L::FUSE_OFF + 64)
+          const float sc = __fmul_rn(FQ ? *reinterpret_cast<const float*>(smem + L::FUSE_OFF + 64)
                                                 : __ldg(p.a_scale + n0 + c), p.w_scale);
           reinterpret_cast<float*>(p.out)[o] = __fmul_rn((float)a[b], sc);
         }
