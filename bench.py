@@ -995,6 +995,19 @@ def sweep(v, dev, stream, flush, reps=10):
                     p_, A, sc, synth.W_SCALE, out=out, ws=ws)), pws)
                 e["scalar_lut_us"] = ts * 1e6
                 e["vec_over_scalar_speedup"] = ts / t
+            if N == 1:
+                # a whole decode step: quantize + mpGeMM (two launches), and
+                # the same step fused into one kernel (vlut_mpgemm_decode)
+                xf = x[:, 0].contiguous()
+                of = torch.empty((lin.M,), dtype=torch.float32, device=dev)
+                sf = torch.empty((1,), dtype=torch.float32, device=dev)
+                tq = timeit_batched(lambda p_: (lambda: (
+                    v.quantize(x, q=A, scale=sc),
+                    v.mpgemm_ws(p_, A, sc, synth.W_SCALE, out=out, ws=ws))), pws)
+                tf = timeit_batched(lambda p_: (lambda: v.mpgemm_decode(
+                    p_, xf, synth.W_SCALE, out=of, scale_out=sf, ws=ws)), pws)
+                e["decode_step_us"] = tq * 1e6
+                e["fused_decode_step_us"] = tf * 1e6
             res.append(e)
         del pw, pws
     c3 = synth.CONFIGS[3]
