@@ -240,3 +240,35 @@ def test_pack_device_then_mpgemm_back_to_back(v):
         torch.cuda.synchronize()
         ref = oracle.dequant_f32(oracle.gemm_i32(W, q), s, synth.W_SCALE)
         assert np.array_equal(out.cpu().numpy().view(np.int32), ref.view(np.int32)), i
+
+
+def test_fused_decode_graph_replay_with_new_inputs(v):
+    """vlut_mpgemm_decode captured once and replayed with new activations in
+    the same buffer: the absmax, the codes and the counted split-K meeting
+    carry no state between replays."""
+    M, K, g = 3072, 23040, 4
+    W = synth.ternary_weights(M, K, seed=5)
+    pw = v.pack_weights(W, g, device=dev())
+    xd = torch.empty((K,), dtype=torch.float32, device=dev())
+    out = torch.empty((M,), dtype=torch.float32, device=dev())
+    sc = torch.empty((1,), dtype=torch.float32, device=dev())
+    ws = torch.zeros_like(v.workspace(dev()))
+    st = torch.cuda.Stream()
+    xd.copy_(to_dev(synth.activations_f32(K, 1, seed=1)[:, 0].copy()))
+    with torch.cuda.stream(st):
+        v.mpgemm_decode(pw, xd, synth.W_SCALE, out=out, scale_out=sc, ws=ws)  # warm-up
+    st.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr, stream=st):
+        v.mpgemm_decode(pw, xd, synth.W_SCALE, out=out, scale_out=sc, ws=ws)
+    for trial in range(3):
+        x = synth.activations_f32(K, 1, seed=50 + trial)[:, 0].copy() * (10.0 ** trial)
+        xd.copy_(to_dev(x))
+        out.fill_(float("nan"))
+        torch.cuda.synchronize()
+        gr.replay()
+        torch.cuda.synchronize()
+        q, s = oracle.quantize(x[:, None])
+        ref = oracle.dequant_f32(oracle.gemm_i32(W, q), s, synth.W_SCALE)[:, 0]
+        assert np.array_equal(sc.cpu().numpy().view(np.int32), s.view(np.int32)), trial
+        assert np.array_equal(out.cpu().numpy().view(np.int32), ref.view(np.int32)), trial
