@@ -464,7 +464,7 @@ def main():
                     torch.cuda.synchronize()
                     dist.barrier()
                     v.mpgemm_allgather(pw, q, s, synth.W_SCALE, target, r0, peers,
-                                       stream=stream)
+                                       stream=stream, multicast=pe.multicast(M, N))
                     barrier()
                     torch.cuda.synchronize()
                     okt = torch.tensor([1 if torch.equal(buf, out_full) else 0], device=dev)
@@ -488,7 +488,8 @@ def main():
         v.quantize(x, q=q, scale=s, stream=st)
         if peer is not None:
             buf, target, peers, barrier = peer.get(M, N, dev)
-            v.mpgemm_allgather(pw, q, s, synth.W_SCALE, target, r0, peers, stream=stream)
+            v.mpgemm_allgather(pw, q, s, synth.W_SCALE, target, r0, peers, stream=stream,
+                               multicast=peer.multicast(M, N))
             barrier()
             return
         v.mpgemm_ws(pw, q, s, synth.W_SCALE, out=out_r, ws=ws, stream=st)

@@ -373,6 +373,20 @@ vlut_status vlut_mpgemm_allgather(const vlut_packed_weights* W, const int8_t* A,
                                   void* stream);
 
 /*
+ * The same with the all-gather done by the NVSwitch (NVLS multicast): out_mc
+ * is the multicast address of the ranks' [M_total][N] fp32 buffers (e.g.
+ * torch symmetric memory's multicast_ptr; 16-B aligned).  The K1 epilogue
+ * stores every 16-byte unit ONCE, with multimem.st (the only access PTX
+ * defines on a multimem address), and the switch replicates it into every
+ * rank's copy, this rank's included.  Ordering as above (a cross-GPU barrier
+ * before any rank reads).  Errors: VLUT_ERR_INVALID_ARGUMENT (NULL address,
+ * row0 < 0), VLUT_ERR_MISALIGNED; otherwise as vlut_mpgemm.
+ */
+vlut_status vlut_mpgemm_allgather_multicast(const vlut_packed_weights* W, const int8_t* A,
+                                            const float* a_scale, float w_scale, float* out_mc,
+                                            int M, int K, int N, int row0, void* stream);
+
+/*
  * Per-token absmax int8 quantizer (a7; w1.6A8 named at P:102; formula
  * S:339-347, reading c8), IEEE single precision throughout:
  *   x'[k][n] = x[k][n] * (y ? y[k][n] : 1)      (fp32 multiply, config 5's

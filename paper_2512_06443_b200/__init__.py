@@ -146,6 +146,10 @@ EXPORTS = {
                                ctypes.c_float, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
                                ctypes.c_int, ctypes.c_void_p], ctypes.c_int),
+    "vlut_mpgemm_allgather_multicast": ([ctypes.POINTER(_Desc), ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_float, ctypes.c_void_p, ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_void_p], ctypes.c_int),
     "vlut_launches_per_mpgemm": ([], ctypes.c_int),
     "vlut_cached_workspaces": ([], ctypes.c_int),
     "vlut_release_workspaces": ([], ctypes.c_int),
@@ -731,13 +735,24 @@ def mpgemm_decode(W: PackedWeights, x, w_scale: float, out=None, scale_out=None,
 
 # ---------------------------------------------------------------- fused all-gather (a8)
 def mpgemm_allgather(W: PackedWeights, A, a_scale, w_scale: float, out_full, row0: int,
-                     peer_ptrs=(), stream=None):
+                     peer_ptrs=(), stream=None, multicast: bool = False):
     """Shard rows [row0, row0 + W.M) of out_full [M_total][N] (a tensor or a
-    raw device address, e.g. a multicast address), stored there and to every
-    peer buffer in ``peer_ptrs`` (device pointers mapped into this process)
-    by the K1 epilogue.  Returns out_full."""
+    raw device address), stored there and to every peer buffer in
+    ``peer_ptrs`` (device pointers mapped into this process) by the K1
+    epilogue.  multicast=True: out_full is a multicast address (an int; no
+    peers) and the epilogue stores through it with multimem.st.  Returns
+    out_full."""
     import torch
     K, N, dev = _act(A)
+    if multicast:
+        if not isinstance(out_full, int) or peer_ptrs:
+            raise ValueError("multicast: out_full must be the multicast address, no peers")
+        with torch.cuda.device(dev):
+            _check(lib().vlut_mpgemm_allgather_multicast(
+                _weights(W, K, dev), _dev_ptr(A), _arg(a_scale, "a_scale", torch.float32, (N,), dev),
+                float(w_scale), ctypes.c_void_p(out_full), W.M, K, N, int(row0),
+                _stream_ptr(stream, dev)))
+        return out_full
     arr = (ctypes.c_void_p * max(1, len(peer_ptrs)))(*[ctypes.c_void_p(int(x)) for x in peer_ptrs])
     # out_full: a tensor, or a raw device address (e.g. a multicast address)
     if isinstance(out_full, int):

@@ -28,6 +28,7 @@ thread_local std::string g_err;
 // thread-local so concurrent callers on other threads are unaffected.
 struct PeerTls {
   int n = 0;
+  int mc = 0;  // the output pointer is a multicast address
   float* ptr[vlut::kMaxPeers] = {};
 };
 thread_local PeerTls g_peer_tls;
@@ -1065,8 +1066,9 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
   }
   p.out_t = out_t;
   p.n_peers = g_peer_tls.n;
+  p.out_mc = g_peer_tls.mc;
   for (int i = 0; i < g_peer_tls.n; ++i) p.peer_out[i] = g_peer_tls.ptr[i];
-  if (p.n_peers && (plan.streamk || acc_only || out_t || acc_in))
+  if ((p.n_peers || p.out_mc) && (plan.streamk || n32 || sk32 || acc_only || out_t || acc_in))
     return fail(VLUT_ERR_UNSUPPORTED, "fused all-gather: cluster schedule, fp32 [M][N] output only");
   p.mul_in = mul_in;
   p.amax_out = amax_out;
@@ -1507,6 +1509,26 @@ vlut_status vlut_mpgemm_allgather(const vlut_packed_weights* W, const int8_t* A,
                     false);
   }
   g_peer_tls.n = 0;
+  return st;
+}
+
+vlut_status vlut_mpgemm_allgather_multicast(const vlut_packed_weights* W, const int8_t* A,
+                                            const float* a_scale, float w_scale, float* out_mc,
+                                            int M, int K, int N, int row0, void* stream) {
+  if (!out_mc || row0 < 0) return fail(VLUT_ERR_INVALID_ARGUMENT, "bad output / row0");
+  if (((uintptr_t)out_mc) & 15) return fail(VLUT_ERR_MISALIGNED, "multicast address not 16-B aligned");
+  if (M == 0 || N == 0) return ok();
+  g_peer_tls.n = 0;
+  g_peer_tls.mc = 1;
+  vlut_launch_plan pl = {};
+  DeviceInfo d;
+  vlut_status st = device_info(&d);
+  if (st == VLUT_OK) {
+    plan_for(M, K, N, W ? W->g : 4, d.sms, &pl);
+    st = run_mpgemm(W, A, a_scale, w_scale, out_mc + (size_t)row0 * N, M, K, N, &pl, stream,
+                    false);
+  }
+  g_peer_tls.mc = 0;
   return st;
 }
 

@@ -308,7 +308,21 @@ struct alignas(64) Params {
   // offset to this shard's first row, same [M][N] indexing as `out`
   float* peer_out[kMaxPeers];
   int n_peers;
+  // 1: `out` is a multicast address (NVLS: the NVSwitch replicates each store
+  // into every rank's copy); stored with multimem.st, the only access PTX
+  // defines on a multimem address
+  int out_mc;
 };
+
+// fp32 stores to a multicast (multimem) address
+__device__ __forceinline__ void st_mc_v4(float* p, float4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void st_mc_f32(float* p, float v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;\n" ::"l"(p), "f"(v) : "memory");
+}
 
 // ---------------------------------------------------------------- staging (a2)
 // Issued by the builder threads (bt in [0, 128)).  what: 1 = index vectors,
@@ -1167,13 +1181,21 @@ __global__ void __launch_bounds__((WARPS + kBW<WARPS, 1>) * 32, 1)
           }
           if (p.out_vec4 && n + 3 < p.N) {
             const float4 f4 = make_float4(f[0], f[1], f[2], f[3]);
-            *reinterpret_cast<float4*>(o) = f4;
+            if (p.out_mc)
+              st_mc_v4(o, f4);
+            else
+              *reinterpret_cast<float4*>(o) = f4;
             // fused all-gather: the same 16 bytes to every peer's copy (P2P
             // stores over NVLink, overlapping the other CTAs' compute)
             for (int pi = 0; pi < p.n_peers; ++pi)
               *reinterpret_cast<float4*>(p.peer_out[pi] + (size_t)m * p.N + n) = f4;
           } else {
-            for (int k = 0; k < 4 && n + k < p.N; ++k) o[k] = f[k];
+            for (int k = 0; k < 4 && n + k < p.N; ++k) {
+              if (p.out_mc)
+                st_mc_f32(o + k, f[k]);
+              else
+                o[k] = f[k];
+            }
             for (int pi = 0; pi < p.n_peers; ++pi)
               for (int k = 0; k < 4 && n + k < p.N; ++k) p.peer_out[pi][(size_t)m * p.N + n + k] = f[k];
           }

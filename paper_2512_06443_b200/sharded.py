@@ -106,6 +106,12 @@ class PeerOutputs:
         t, target, peers, h = self._bufs[key][i]
         return t, target, peers, (lambda: h.barrier(channel=0))
 
+    def multicast(self, M: int, N: int) -> bool:
+        """True if get(M, N, ...) hands out a multicast address (store it
+        with mpgemm_allgather(..., multicast=True))."""
+        pair = self._bufs.get((M, N))
+        return bool(pair) and pair[0][1] != pair[0][0].data_ptr()
+
     def transport(self, M: int, N: int, device) -> str:
         _, target, peers, _ = self.get(M, N, device)
         self.get(M, N, device)  # restore the alternation
@@ -282,7 +288,8 @@ class RowShardedLinear:
             import paper_2512_06443_b200 as v
             buf, target, peer_ptrs, barrier = self.peers.get(self.M, N, dev)
             if self.rows:
-                v.mpgemm_allgather(self.shard, A, a_scale, self.w_scale, target, self.r0, peer_ptrs)
+                v.mpgemm_allgather(self.shard, A, a_scale, self.w_scale, target, self.r0, peer_ptrs,
+                                   multicast=self.peers.multicast(self.M, N))
             barrier()
             if out is not None:
                 out.copy_(buf)

@@ -653,6 +653,103 @@ def test_mpgemm_allgather_rejects_bad_peers(v):
         v.mpgemm_allgather(pw, A, s, 0.02, out, 0, [out.data_ptr()] * 8)  # > 7 peers
 
 
+class _SingleDeviceMulticast:
+    """A multicast object with this one device as its only member (CUDA
+    driver API): `mc` is the multicast address, `uc` the unicast mapping of
+    the same physical memory.  Raises RuntimeError when unsupported."""
+
+    def __init__(self, nbytes):
+        from cuda.bindings import driver as cu
+        self.cu = cu
+        torch.zeros(1, device=dev())  # primary context current
+        idx = torch.cuda.current_device()
+
+        def ok(res, what=""):
+            res = res if isinstance(res, tuple) else (res,)
+            if res[0] != cu.CUresult.CUDA_SUCCESS:
+                raise RuntimeError(f"CUDA driver {what}: {res[0]}")
+            return res[1] if len(res) == 2 else res[1:]
+
+        d = ok(cu.cuDeviceGet(idx))
+        if not ok(cu.cuDeviceGetAttribute(
+                cu.CUdevice_attribute.CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, d)):
+            raise RuntimeError("no multicast support")
+        prop = cu.CUmulticastObjectProp()
+        prop.numDevices = 1
+        fd = cu.CUmemAllocationHandleType.CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR
+        prop.handleTypes = fd
+        prop.size = nbytes
+        gran = ok(cu.cuMulticastGetGranularity(
+            prop, cu.CUmulticastGranularity_flags.CU_MULTICAST_GRANULARITY_RECOMMENDED), "granularity")
+        self.size = size = -(-nbytes // gran) * gran
+        prop.size = size
+        self.mc_handle = ok(cu.cuMulticastCreate(prop), "cuMulticastCreate")
+        ok(cu.cuMulticastAddDevice(self.mc_handle, d), "cuMulticastAddDevice")
+        ap = cu.CUmemAllocationProp()
+        ap.type = cu.CUmemAllocationType.CU_MEM_ALLOCATION_TYPE_PINNED
+        ap.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+        ap.location.id = idx
+        ap.requestedHandleTypes = fd
+        self.mem = ok(cu.cuMemCreate(size, ap, 0), "cuMemCreate")
+        ok(cu.cuMulticastBindMem(self.mc_handle, 0, self.mem, 0, size, 0), "cuMulticastBindMem")
+        acc = cu.CUmemAccessDesc()
+        acc.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+        acc.location.id = idx
+        acc.flags = cu.CUmemAccess_flags.CU_MEM_ACCESS_FLAGS_PROT_READWRITE
+        self.vas = []
+        for h in (self.mem, self.mc_handle):
+            va = ok(cu.cuMemAddressReserve(size, gran, 0, 0), "cuMemAddressReserve")
+            ok(cu.cuMemMap(va, size, 0, h, 0), "cuMemMap")
+            ok(cu.cuMemSetAccess(va, size, [acc], 1), "cuMemSetAccess")
+            self.vas.append(va)
+        self.uc, self.mc = int(self.vas[0]), int(self.vas[1])
+
+    def close(self):
+        cu = self.cu
+        torch.cuda.synchronize()
+        for va in self.vas:
+            cu.cuMemUnmap(va, self.size)
+            cu.cuMemAddressFree(va, self.size)
+        cu.cuMulticastUnbind(self.mc_handle, 0, 0, self.size)
+        cu.cuMemRelease(self.mem)
+        cu.cuMemRelease(self.mc_handle)
+
+
+@pytest.mark.parametrize("M,K,N", [(256, 512, 64), (1000, 1280, 100), (333, 512, 63)])
+def test_mpgemm_allgather_multicast_single_device(v, M, K, N):
+    """vlut_mpgemm_allgather_multicast on real multicast memory (a one-member
+    multicast object): two emulated ranks store their row shards through the
+    multicast address with multimem.st; the unicast view holds the whole
+    output, bit-identical to the oracle, NaN past it."""
+    from paper_2512_06443_b200.sharded import shard_rows
+    nbytes = (M + 4) * N * 4
+    try:
+        mcb = _SingleDeviceMulticast(nbytes)
+    except (ImportError, RuntimeError) as ex:
+        pytest.skip(f"multicast object unavailable: {ex}")
+    try:
+        view = torch.full(((mcb.size // 4) // N, N), float("nan"), device=dev())
+        mcb.cu.cuMemcpy(mcb.uc, view.data_ptr(), view.numel() * 4)
+        W = synth.ternary_weights(M, K, seed=M + 7)
+        x = synth.activations_f32(K, N, seed=N + 7)
+        q, s = oracle.quantize(x)
+        qd, sd = to_dev(q), to_dev(s)
+        for r in range(2):
+            r0, r1, _ = shard_rows(M, 2, r)
+            pw = v.pack_weights(np.ascontiguousarray(W[r0:r1]), 4, device=dev())
+            v.mpgemm_allgather(pw, qd, sd, synth.W_SCALE, mcb.mc, r0, multicast=True)
+        torch.cuda.synchronize()
+        mcb.cu.cuMemcpy(view.data_ptr(), mcb.uc, view.numel() * 4)
+        torch.cuda.synchronize()
+        got = view.cpu().numpy()
+        check_fp32(got[:M], oracle.gemm_i32(W, q), s, synth.W_SCALE)
+        assert np.isnan(got[M:]).all()
+        with pytest.raises(v.VlutError):
+            v.mpgemm_allgather(pw, qd, sd, synth.W_SCALE, mcb.mc + 4, 0, multicast=True)
+    finally:
+        mcb.close()
+
+
 def test_peer_outputs_symmetric_memory_world1(v):
     """The symmetric-memory plumbing of the fused all-gather on a 1-rank
     NCCL group: allocation, rendezvous, alternating buffers, barrier."""
@@ -677,7 +774,8 @@ def test_peer_outputs_symmetric_memory_world1(v):
             assert peers0 == [] and peers1 == []
             assert b0.data_ptr() != b1.data_ptr() and b2.data_ptr() == b0.data_ptr()
             b0.fill_(float("nan"))
-            v.mpgemm_allgather(pw, to_dev(q), to_dev(s), synth.W_SCALE, t0, 0, peers0)
+            v.mpgemm_allgather(pw, to_dev(q), to_dev(s), synth.W_SCALE, t0, 0, peers0,
+                               multicast=po.multicast(128, 64))
             bar0()
             torch.cuda.synchronize()
             check_fp32(b0.cpu().numpy(), oracle.gemm_i32(W, q), s, synth.W_SCALE)
