@@ -400,6 +400,20 @@ vlut_status vlut_mpgemm_allgather_multicast(const vlut_packed_weights* W, const 
 vlut_status vlut_quantize(const float* x, const float* y, int K, int N,
                           int8_t* q, float* scale, void* stream);
 
+/*
+ * vlut_quantize with the K3 cluster size chosen by the caller: cluster 0 =
+ * the library's choice (== vlut_quantize); 1, 2, 4 or 8 = that many CTAs per
+ * 16-token block (fewer, narrower launches).  Cluster 1 is for running the
+ * quantizer of the NEXT independent batch on a second stream while an
+ * mpGeMM holds most SMs: its one-CTA clusters fit the SMs the mpGeMM grid
+ * leaves free (configs[1]: 144 of 148), where an 8-CTA cluster would wait
+ * for the mpGeMM to finish (profiles/r02_pipeline.txt).  Same codes and
+ * scales, bit for bit, for every cluster size.  Errors as vlut_quantize, and
+ * VLUT_ERR_INVALID_ARGUMENT for any other cluster value.
+ */
+vlut_status vlut_quantize_ex(const float* x, const float* y, int K, int N, int8_t* q,
+                             float* scale, int cluster, void* stream);
+
 /* The library's vlut_mpgemm workspaces (see Conventions): the number
  * currently cached (all devices), and a release of all of them (synchronises
  * each device that holds one, then frees; the next vlut_mpgemm call on a

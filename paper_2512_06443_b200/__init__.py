@@ -101,6 +101,9 @@ EXPORTS = {
                          ctypes.c_void_p], ctypes.c_int),
     "vlut_quantize": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "vlut_quantize_ex": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p],
+                         ctypes.c_int),
     "vlut_group_schedule": ([ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                              ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "vlut_mpgemm_mixed": ([ctypes.POINTER(_Desc), ctypes.POINTER(_Desc), ctypes.c_void_p,
@@ -429,8 +432,10 @@ def mpgemm_acc(W: PackedWeights, A, out=None, plan: Optional[LaunchPlan] = None,
     return out
 
 
-def quantize(x, y=None, q=None, scale=None, stream=None):
-    """Per-token absmax int8 quantizer of fp32 [K][N] (x * y if y given)."""
+def quantize(x, y=None, q=None, scale=None, stream=None, cluster: int = 0):
+    """Per-token absmax int8 quantizer of fp32 [K][N] (x * y if y given).
+    cluster: K3 CTAs per 16-token block (0 = the library's choice; 1 for a
+    quantizer overlapping an mpGeMM on another stream, see vlut_quantize_ex)."""
     import torch
     if x.dim() != 2:
         raise ValueError("x: expected fp32 [K][N]")
@@ -439,9 +444,9 @@ def quantize(x, y=None, q=None, scale=None, stream=None):
     q, qp = _out(q, (K, N), torch.int8, dev, "q")
     scale, sp = _out(scale, (N,), torch.float32, dev, "scale")
     with torch.cuda.device(dev):
-        _check(lib().vlut_quantize(_arg(x, "x", torch.float32, device=dev),
-                                   _arg(y, "y", torch.float32, (K, N), dev, optional=True),
-                                   K, N, qp, sp, _stream_ptr(stream, dev)))
+        _check(lib().vlut_quantize_ex(_arg(x, "x", torch.float32, device=dev),
+                                      _arg(y, "y", torch.float32, (K, N), dev, optional=True),
+                                      K, N, qp, sp, int(cluster), _stream_ptr(stream, dev)))
     return q, scale
 
 

@@ -1707,6 +1707,13 @@ vlut_status vlut_linear(const vlut_packed_weights* W, const float* x, float w_sc
 
 vlut_status vlut_quantize(const float* x, const float* y, int K, int N, int8_t* q, float* scale,
                           void* stream) {
+  return vlut_quantize_ex(x, y, K, N, q, scale, 0, stream);
+}
+
+vlut_status vlut_quantize_ex(const float* x, const float* y, int K, int N, int8_t* q,
+                             float* scale, int cluster, void* stream) {
+  if (!(cluster == 0 || cluster == 1 || cluster == 2 || cluster == 4 || cluster == 8))
+    return fail(VLUT_ERR_INVALID_ARGUMENT, "cluster must be 0, 1, 2, 4 or 8");
   if (K < 0 || N < 0) return fail(VLUT_ERR_INVALID_ARGUMENT, "bad sizes");
   if (K == 0 || N == 0) return ok();
   if (!x || !q || !scale) return fail(VLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
@@ -1720,7 +1727,7 @@ vlut_status vlut_quantize(const float* x, const float* y, int K, int N, int8_t* 
                          ((((uintptr_t)x) | ((uintptr_t)(y ? y : x))) & 15) == 0 &&
                          (((uintptr_t)q) & 3) == 0 &&
                          total4 <= (long long)vlut::kQfMaxCL * vlut::kQfThreads * vlut::kQfCache;
-    if (flat_ok && !getenv("VLUT_NO_QFLAT")) {
+    if (flat_ok && !cluster && !getenv("VLUT_NO_QFLAT")) {
       // CTAs: ~2 float4 per thread in flight, at most one cluster of 8
       long long CLl = (total4 + 2LL * vlut::kQfThreads - 1) / (2LL * vlut::kQfThreads);
       while (CLl < vlut::kQfMaxCL && total4 > CLl * vlut::kQfThreads * vlut::kQfCache) ++CLl;
@@ -1752,6 +1759,7 @@ vlut_status vlut_quantize(const float* x, const float* y, int K, int N, int8_t* 
   while (CL < 8 && ((long long)K > (long long)CL * vlut::kQRows * vlut::kQCache || tok_blocks * CL < 296))
     CL *= 2;
   if (CL > K) CL = 1;
+  if (cluster) CL = cluster;  // caller-chosen (e.g. 1: fits the SMs a concurrent mpGeMM leaves idle)
   if (const char* e = getenv("VLUT_QCL")) {  // (development A/B knob)
     const int c = atoi(e);
     if (c == 1 || c == 2 || c == 4 || c == 8) CL = c;

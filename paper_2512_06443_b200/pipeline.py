@@ -78,3 +78,70 @@ class HostPipeline:
     def synchronize(self) -> None:
         for s in (self.s_in, self.s_cmp, self.s_out):
             s.synchronize()
+
+
+class BatchPipeline:
+    """Independent device-resident activation batches through one Vec-LUT
+    linear, the quantizer of batch i+1 overlapping the mpGeMM of batch i.
+
+    The mpGeMM grid leaves SMs free (configs[1]: K1-32 runs 144 CTAs, one per
+    SM, on the 148), and the quantizer launched with one-CTA clusters
+    (``quantize(..., cluster=1)``, vlut_quantize_ex) fits them, so on a second
+    stream it runs under the mpGeMM instead of before it: the step costs the
+    mpGeMM alone (profiles/r02_pipeline.txt; an 8-CTA cluster cannot be
+    placed on the free SMs and waits for the mpGeMM).  Codes and scales are
+    double-buffered: batch i's quantizer waits for the mpGeMM of batch i-2
+    (the last reader of its buffer), batch i's mpGeMM for its quantizer.
+    Results are bit-identical to quantize-then-mpGeMM on one stream.
+
+    ``submit`` enqueues on the caller's current stream (the mpGeMMs) and the
+    pipeline's side stream (the quantizers) and can be captured in a CUDA
+    graph; ``join`` makes the current stream wait for the side stream.  An
+    input x must already be complete on the side stream's timeline: written
+    before the first ``submit`` on the current stream, or signalled by the
+    ``ready`` event passed with it.
+    """
+
+    def __init__(self, W: "v.PackedWeights", w_scale: float, K: int, N: int, device, ws=None,
+                 plan=None):
+        import torch
+        self.torch = torch
+        self.W, self.w_scale, self.K, self.N = W, float(w_scale), K, N
+        self.dev = torch.device(device)
+        self.ws = ws if ws is not None else v.workspace(self.dev)
+        self.plan = plan
+        self.side = torch.cuda.Stream(self.dev)
+        self.q = [torch.empty((K, N), dtype=torch.int8, device=self.dev) for _ in range(2)]
+        self.sc = [torch.empty((N,), dtype=torch.float32, device=self.dev) for _ in range(2)]
+        self.ev_q = [torch.cuda.Event() for _ in range(2)]  # codes of buffer b written
+        self.ev_k = [torch.cuda.Event() for _ in range(2)]  # codes of buffer b consumed
+        self.i = 0
+
+    def submit(self, x, out, W: "Optional[v.PackedWeights]" = None, ready=None) -> None:
+        """x: fp32 [K][N] on the device; out: fp32 [M][N]; W: packed weights
+        for this batch (default: the pipeline's)."""
+        torch = self.torch
+        b = self.i % 2
+        cs = torch.cuda.current_stream(self.dev)
+        if self.i == 0:
+            self.side.wait_stream(cs)
+        with torch.cuda.stream(self.side):
+            if ready is not None:
+                self.side.wait_event(ready)
+            if self.i >= 2:
+                self.side.wait_event(self.ev_k[b])
+            v.quantize(x, q=self.q[b], scale=self.sc[b], stream=self.side, cluster=1)
+            self.ev_q[b].record(self.side)
+        cs.wait_event(self.ev_q[b])
+        v.mpgemm_ws(W if W is not None else self.W, self.q[b], self.sc[b], self.w_scale, out=out,
+                    ws=self.ws, plan=self.plan, stream=cs)
+        self.ev_k[b].record(cs)
+        self.i += 1
+
+    def reset(self) -> None:
+        """Start a new sequence (e.g. before capturing one in a CUDA graph):
+        the next submit forks the side stream from the current one again."""
+        self.i = 0
+
+    def join(self) -> None:
+        self.torch.cuda.current_stream(self.dev).wait_stream(self.side)

@@ -62,6 +62,27 @@ def test_quantize_bit_exact(v, K, N):
     assert np.array_equal(q.cpu().numpy(), qr)
 
 
+@pytest.mark.parametrize("cluster", [1, 2, 4, 8])
+@pytest.mark.parametrize("K,N", [(2560, 256), (5, 3), (6912, 40), (23040, 16), (3, 1)])
+def test_quantize_caller_cluster_bit_exact(v, K, N, cluster):
+    """vlut_quantize_ex: every caller-chosen K3 cluster size gives the
+    oracle's codes and scales bit for bit (incl. K < cluster, N = 1)."""
+    x = synth.activations_f32(K, N, seed=3 * K + N)
+    y = synth.activations_f32(K, N, seed=5 * K + N)
+    for yy in (None, y):
+        q, s = v.quantize(to_dev(x), None if yy is None else to_dev(yy), cluster=cluster)
+        qr, sr = oracle.quantize(x if yy is None else (x * yy).astype(np.float32))
+        assert np.array_equal(s.cpu().numpy().view(np.int32), sr.view(np.int32))
+        assert np.array_equal(q.cpu().numpy(), qr)
+
+
+def test_quantize_rejects_bad_cluster(v):
+    x = to_dev(synth.activations_f32(64, 8, seed=1))
+    for c in (-1, 3, 16):
+        with pytest.raises(v.VlutError):
+            v.quantize(x, cluster=c)
+
+
 @pytest.mark.parametrize("K,N", [(2560, 1), (23040, 1), (6912, 2), (1000, 4), (4096, 8),
                                  (8192, 16), (12, 16), (4, 1), (65536, 2)])
 @pytest.mark.parametrize("with_y", [False, True])
@@ -591,6 +612,51 @@ def test_mpgemm_fused_mul_and_amax(v, M, K, N, rows, how):
 
 
 # ------------------------------------------------------------------ host pipeline (e2e path)
+@pytest.mark.parametrize("graph", [False, True])
+def test_batch_pipeline_matches_oracle(v, graph):
+    """pipeline.BatchPipeline (batch i+1's quantizer on a side stream under
+    batch i's mpGeMM, double-buffered codes): every batch's output is
+    bit-identical to the oracle, eager and captured in a CUDA graph replayed
+    twice with new inputs; weights alternate between two matrices."""
+    from paper_2512_06443_b200.pipeline import BatchPipeline
+    M, K, N, steps = 1000, 2560, 96, 7
+    Ws = [synth.ternary_weights(M, K, seed=90 + i) for i in range(2)]
+    pws = [v.pack_weights(W, 4, device=dev()) for W in Ws]
+    xs = [to_dev(synth.activations_f32(K, N, seed=100 + i)) for i in range(steps)]
+    outs = [torch.full((M, N), float("nan"), device=dev()) for _ in range(steps)]
+    bp = BatchPipeline(pws[0], synth.W_SCALE, K, N, dev())
+    torch.cuda.synchronize()
+
+    def run():
+        bp.reset()
+        for i in range(steps):
+            bp.submit(xs[i], outs[i], W=pws[i % 2])
+        bp.join()
+
+    def check():
+        for i in range(steps):
+            x = xs[i].cpu().numpy()
+            q, s = oracle.quantize(x)
+            check_fp32(outs[i].cpu().numpy(), oracle.gemm_i32(Ws[i % 2], q), s, synth.W_SCALE)
+
+    if not graph:
+        run()
+        torch.cuda.synchronize()
+        check()
+        return
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        run()
+    for rep in range(2):
+        for i in range(steps):
+            xs[i].copy_(to_dev(synth.activations_f32(K, N, seed=200 + 10 * rep + i)))
+            outs[i].fill_(float("nan"))
+        torch.cuda.synchronize()
+        gr.replay()
+        torch.cuda.synchronize()
+        check()
+
+
 def test_host_pipeline_matches_oracle(v):
     """bench.py's e2e path: pinned fp32 inputs -> HostPipeline (H2D, quantize,
     mpGeMM, D2H on three streams, 2 slots) -> pinned outputs; every step's
