@@ -333,7 +333,9 @@ size_t sk_part_bytes(int sms) { return (size_t)sms * 768 * 64 * 4; }  // max m_c
 size_t slot_cnt_off(int sms) { return sk_part_bytes(sms) + 4096; }
 size_t slot_acc_off(int sms) { return slot_cnt_off(sms) + (size_t)vlut::slot::kMaxCounters * 8; }
 constexpr size_t kSlotAccBytes = (size_t)16 << 20;
-size_t sk_workspace_bytes(int sms) { return slot_acc_off(sms) + kSlotAccBytes; }
+size_t sk32_acc_off(int sms) { return slot_acc_off(sms) + kSlotAccBytes; }
+// K1-32-SK fp32 split-tile accumulators: one [768][32] slot per CTA, zero between launches
+size_t sk_workspace_bytes(int sms) { return sk32_acc_off(sms) + (size_t)sms * 768 * 32 * 4; }
 
 // Best stream-K plan (persistent, grid = #SMs): every CTA gets ceil(U / sms)
 // K-tile units; cost in the same SMEM-cycle units as plan_for.
@@ -1092,6 +1094,14 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
       const int gx = atoi(e);
       if (gx > 0 && gx < grid) grid = gx;
     }
+    // K1-32-SK: split tiles meet in fp32 accumulators (exact while every
+    // partial sum stays below 2^24) when there are fewer tiles than CTAs --
+    // several producers per tile, whose reads would chain in the owner's
+    // fixup; with more tiles (<= 1 producer per tile) the int32 partial
+    // stores are cheaper than the L2 reductions (profiles/r02_sk32_fixup.txt)
+    const bool acc_f32 = sk32 && (long long)K * 128 < (1LL << 24) && MT * NT < grid &&
+                         !getenv("VLUT_SK32_INT_PARTIALS");
+    sk.acc = acc_f32 ? reinterpret_cast<float*>(static_cast<char*>(ws) + sk32_acc_off(d.sms)) : nullptr;
     if (sk32)
       st = acc_only ? dispatch_sk32<true>(W->g, plan.warps, rpt, p, sk, grid, s)
                     : dispatch_sk32<false>(W->g, plan.warps, rpt, p, sk, grid, s);

@@ -29,6 +29,16 @@
 
 namespace vlut {
 
+#ifndef VLUT_SK32_FIX_MLP
+#define VLUT_SK32_FIX_MLP 2
+#endif
+
+__device__ __forceinline__ void red_add_v4f32(float* p, float a, float b, float c, float d) {
+  asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "f"(a), "f"(b),
+               "f"(c), "f"(d)
+               : "memory");
+}
+
 template <int G, int WARPS, int RPT, bool ACC_ONLY>
 __device__ __forceinline__ void sk32_epilogue(const Params& p, const SkParams& sk, const SkSeg sg,
                                               int KT, int cta, int NCTA, int tid, int lane,
@@ -41,9 +51,22 @@ __device__ __forceinline__ void sk32_epilogue(const Params& p, const SkParams& s
   const bool producer = sg.kb < KT;
   const bool owner = !producer && sg.ka > 0;
   int c_lo = cta;
+  // split tiles meet in fp32 (sk.acc): every partial and every partial sum
+  // is an integer of magnitude <= K * 128 < 2^24 (the host enables it only
+  // then), so fp32 adds are exact and order-free -- each producer red.adds
+  // its rows into the accumulator of the tile's first producer CTA (no
+  // owner-side read per producer), the owner reads that one slot, adds its
+  // own rows and zeroes it for the next launch
+  const bool red_mode = sk.acc != nullptr;
+  const long long head = (long long)sg.tile * KT;
+  if (producer) VLUT_STAMP(5);
+  if (producer && red_mode) {
+    c_lo = cta;
+    while (c_lo > 0 && sk_begin(sk.U, NCTA, c_lo) > head) --c_lo;
+  }
   if (owner) {
+    VLUT_STAMP(2);
     // the tile's head units [tile*KT, tile*KT + ka) came from the preceding CTA(s)
-    const long long head = (long long)sg.tile * KT;
     c_lo = cta - 1;
     while (c_lo > 0 && sk_begin(sk.U, NCTA, c_lo) > head) --c_lo;
     if (tid == 0) {
@@ -57,6 +80,7 @@ __device__ __forceinline__ void sk32_epilogue(const Params& p, const SkParams& s
       }
     }
     bar_sync(6, NLT);
+    VLUT_STAMP(3);
   }
 #pragma unroll 1
   for (int rb = 0; rb < RPT; ++rb) {
@@ -76,6 +100,18 @@ __device__ __forceinline__ void sk32_epilogue(const Params& p, const SkParams& s
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           a[k][hh][j] = (int32_t)(v[k >> 1][8 * (k & 1) + 4 * hh + j] - (uint32_t)bias_total);
+    if (producer && red_mode) {
+      float* arow = sk.acc + ((size_t)c_lo * L::MCTA + row) * kN32;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = (lane ^ k) & 3;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+          red_add_v4f32(arow + 8 * c + 4 * hh, (float)a[k][hh][0], (float)a[k][hh][1],
+                        (float)a[k][hh][2], (float)a[k][hh][3]);
+      }
+      continue;
+    }
     if (producer) {
       int32_t* wrow = sk.ws + ((size_t)cta * L::MCTA + row) * kN32;
 #pragma unroll
@@ -88,25 +124,57 @@ __device__ __forceinline__ void sk32_epilogue(const Params& p, const SkParams& s
       }
       continue;
     }
-    if (owner) {
+    if (owner && red_mode) {
+      float* arow = sk.acc + ((size_t)c_lo * L::MCTA + row) * kN32;
+      float4 w4[4][2];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = (lane ^ k) & 3;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+          w4[k][hh] = __ldcg(reinterpret_cast<const float4*>(arow + 8 * c + 4 * hh));
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = (lane ^ k) & 3;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          a[k][hh][0] += (int32_t)w4[k][hh].x; a[k][hh][1] += (int32_t)w4[k][hh].y;
+          a[k][hh][2] += (int32_t)w4[k][hh].z; a[k][hh][3] += (int32_t)w4[k][hh].w;
+          __stcg(reinterpret_cast<float4*>(arow + 8 * c + 4 * hh), make_float4(0.f, 0.f, 0.f, 0.f));
+        }
+      }
+    } else if (owner) {
+      // producers' rows read VLUT_SK32_FIX_MLP at a time (all loads in flight
+      // before the adds): the fixup is a chain of L2 round trips, one per
+      // batch -- at N = 256 a tile has ~5 producers (r02_sk32_fixup.txt)
+      constexpr int FB = VLUT_SK32_FIX_MLP;
 #pragma unroll 1
-      for (int c2 = cta - 1; c2 >= c_lo; --c2) {
-        const int32_t* prow = sk.ws + ((size_t)c2 * L::MCTA + row) * kN32;
-        int4 w4[4][2];
+      for (int c2 = cta - 1; c2 >= c_lo; c2 -= FB) {
+        int4 w4[FB][4][2];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int c = (lane ^ k) & 3;
+        for (int f = 0; f < FB; ++f) {
+          const int cf = c2 - f >= c_lo ? c2 - f : c2;  // past the last producer: re-read, unused
+          const int32_t* prow = sk.ws + ((size_t)cf * L::MCTA + row) * kN32;
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh)
-            w4[k][hh] = __ldcg(reinterpret_cast<const int4*>(prow + 8 * c + 4 * hh));
+          for (int k = 0; k < 4; ++k) {
+            const int c = (lane ^ k) & 3;
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+              w4[f][k][hh] = __ldcg(reinterpret_cast<const int4*>(prow + 8 * c + 4 * hh));
+          }
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int f = 0; f < FB; ++f) {
+          if (c2 - f < c_lo) break;
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            a[k][hh][0] += w4[k][hh].x; a[k][hh][1] += w4[k][hh].y;
-            a[k][hh][2] += w4[k][hh].z; a[k][hh][3] += w4[k][hh].w;
-          }
+          for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              a[k][hh][0] += w4[f][k][hh].x; a[k][hh][1] += w4[f][k][hh].y;
+              a[k][hh][2] += w4[f][k][hh].z; a[k][hh][3] += w4[f][k][hh].w;
+            }
+        }
       }
     }
     if (m >= p.M) continue;
@@ -163,6 +231,7 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
   const long long u0 = sk_begin(sk.U, NCTA, cta), u1 = sk_begin(sk.U, NCTA, cta + 1);
   const int nunits = (int)(u1 - u0);
   const int nsub = nunits * C::SUBS;
+  VLUT_STAMP(0);
 
   const uint32_t tab_s = smem_u32(smem);
   const uint32_t idx_s = smem_u32(smem + L::IDX_OFF);
@@ -260,6 +329,7 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
       for (int sub = 0; sub < C::SUBS; ++sub) {
         const int u = t * C::SUBS + sub;
         mbar_wait(mbar + m32_full<C::NBUF>(u % C::NBUF), (u / C::NBUF) & 1);
+        if (u == 0) VLUT_STAMP(1);
 #pragma unroll
         for (int rb = 0; rb < RPT; ++rb) {
           const uint4 iw = lds128(idx_s + (uint32_t)((t % C::STAGE) * L::IDX_BYTES +
@@ -288,6 +358,7 @@ __global__ void __launch_bounds__((WARPS + kBuilderWarps) * 32, 1)
       }
       cur.next();
     }
+    VLUT_STAMP(4);
     pdl_wait();
     tmem_fence_before();
     bar_sync(6, L::NLT);

@@ -47,6 +47,10 @@ struct SkParams {
   int32_t* ws;          // [G][MCTA * 64] int32 partials
   unsigned* flags;      // [G] partial-ready flags: 0 between launches
   unsigned epoch;       // the 'ready' value (1)
+  // K1-32-SK with K * 128 < 2^24: split tiles meet in fp32 accumulators
+  // [G][MCTA * 32] (slot = the tile's first producer CTA), zero between
+  // launches; nullptr: the int32 partial slots above
+  float* acc;
 };
 
 struct SkSeg {

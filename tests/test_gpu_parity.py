@@ -559,6 +559,30 @@ def test_streamk32_acc_and_fp32(v, M, K, N, g, warps, rpt):
         check_fp32(out.cpu().numpy(), ref, s, synth.W_SCALE)
 
 
+@pytest.mark.parametrize("M,K,N,g,rpt", [(3072, 23040, 256, 5, 2), (3072, 4600, 512, 5, 1),
+                                         (700, 2560, 96, 4, 2), (128, 140000, 32, 4, 1)])
+def test_streamk32_split_meeting_repeated_launches(v, M, K, N, g, rpt):
+    """K1-32-SK split tiles meet in fp32 accumulators (exact: every partial
+    sum is an integer below 2^24; K >= 131072 keeps the int32 partials):
+    three launches on one workspace with new activations stay bit-exact, and
+    the accumulator region is all zero again after each launch."""
+    W = synth.ternary_weights(M, K, seed=M + 3)
+    pw = v.pack_weights_device(to_dev(W), g)
+    plan = v.LaunchPlan(12, 1, m_cta=384 * rpt, n_cta=32, streamk=1)
+    ws = torch.zeros_like(v.workspace(dev()))
+    acc_bytes = 148 * 768 * 32 * 4
+    big = M * N * K > 2e9
+    pick = np.unique(synth.rng(5).integers(0, M, size=16)) if big else np.arange(M)
+    for it in range(3):
+        A = synth.int8_activations(K, N, seed=50 + it)
+        if it == 1:
+            A[:] = -128  # extreme partial sums: -128 * (K / 2) per CTA half
+        acc = v.mpgemm_acc_ws(pw, to_dev(A), plan=plan, ws=ws)
+        torch.cuda.synchronize()
+        assert np.array_equal(acc.cpu().numpy()[pick], oracle.gemm_i32(W[pick], A))
+        assert int(torch.count_nonzero(ws[-acc_bytes:])) == 0
+
+
 @pytest.mark.parametrize("M,K,N,g", [(6912, 2560, 256, 4), (3072, 23040, 1024, 5), (385, 1024, 130, 4)])
 def test_streamk_fp32_and_planner_identity(v, M, K, N, g):
     W = synth.ternary_weights(M, K, seed=M)

@@ -72,6 +72,23 @@ def schedule(T, KT, G):
         # executed before its owner segment (owner last), so waits point to
         # strictly smaller CTA ids only -> acyclic
         assert all(c2 < c for c2 in deps)
+    # K1-32-SK fp32 meeting: a split tile's producers red.add into the slot
+    # of its first producer -- the CTA whose range holds the tile's head unit,
+    # found by each producer with the owner's walk -- so slots are distinct
+    # per tile and every producer and the owner agree on it
+    slots = {}
+    for c, (t, deps) in waits.items():
+        head = t * KT
+        slot = min(deps)
+        assert sk_begin(U, G, slot) <= head < sk_begin(U, G, slot + 1)
+        assert slot not in slots.values()
+        slots[t] = slot
+    for c, (t, ka, kb) in produced.items():
+        head = t * KT
+        c_lo = c
+        while c_lo > 0 and sk_begin(U, G, c_lo) > head:
+            c_lo -= 1
+        assert slots[t] == c_lo
     return cover, produced, waits
 
 
