@@ -16,7 +16,7 @@
  *     as void* (0 = legacy default stream).
  *   - The caller owns every buffer.  The library allocates device memory in
  *     one place only: vlut_mpgemm (the north-star signature, which has no
- *     workspace argument) keeps a bounded cache of workspaces (~36 MB each on
+ *     workspace argument) keeps a bounded cache of workspaces (~60 MB each on
  *     B200): at most 4 per device, each bound to one stream by its
  *     process-unique id (cudaStreamGetId -- a destroyed-then-recycled stream
  *     handle never aliases an old entry).  Created and zeroed on a stream's
@@ -228,12 +228,15 @@ vlut_status vlut_mpgemm_ex(const vlut_packed_weights* W, const int8_t* A,
  *               accumulators (at decode-size tiles: counted 64-bit words,
  *               count << 40 | biased sum; every K2 launch leaves them zero
  *               again) and
- *               per-tile generation words (monotonic, read on the device).
+ *               per-tile generation words (monotonic, read on the device),
+               and K1-32-SK fp32 split-tile accumulators (producers red.add
+               integer-valued partials, exact below 2^24; the tile's owner
+               reads and re-zeroes them in the same launch).
  *               No host-side per-launch state: captured CUDA graphs may be
  *               replayed.  Stream-K and K2 split-K launches whose CTAs
  *               wait for each other are cooperative (all co-resident);
  *               K2's decode-size tiles meet without waiting and are not.
- * vlut_workspace_bytes() returns 0 without a CUDA device (~36 MB on B200).
+ * vlut_workspace_bytes() returns 0 without a CUDA device (~60 MB on B200).
  */
 size_t vlut_workspace_bytes(void);
 vlut_status vlut_mpgemm_ws(const vlut_packed_weights* W, const int8_t* A, const float* a_scale,
