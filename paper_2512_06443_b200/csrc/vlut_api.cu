@@ -550,7 +550,7 @@ inline bool slot_variant_ok(int g, int nw, int tpw) {
   if (!(nw == 1 || nw == 2 || nw == 4 || nw == 8)) return false;
   return g == 4 || nw <= 2 || (nw == 4 && tpw == 1);  // g = 5: half tables at 4 scalar words
 }
-inline int slot_mcta(int g) { return g == 4 ? 1024 : 2048; }
+inline int slot_mcta(int g) { return g == 4 ? 32 * vlut::slot::kLW * VLUT_SLOT_RPL_G4 : 2048; }
 int slot_smem(int g, int nw, int tpw);
 
 // The narrowest variant covering N tokens in one N-tile (capped at the widest).

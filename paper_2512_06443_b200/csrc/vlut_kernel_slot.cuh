@@ -138,11 +138,14 @@ constexpr int kAtom64MaxSplits = 255;
 // reduce-add + generation handshake
 constexpr int kA64MaxTok = VLUT_SLOT_A64_TOK;
 
+#ifndef VLUT_SLOT_RPL_G4
+#define VLUT_SLOT_RPL_G4 2
+#endif
 template <int G, int NW, int TPW>
 struct SL {
   static constexpr int R = pow3(G);
   static constexpr int ZERO = (R - 1) / 2;
-  static constexpr int RPL = (G == 4) ? 2 : 4;    // rows per lookup lane
+  static constexpr int RPL = (G == 4) ? VLUT_SLOT_RPL_G4 : 4;  // rows per lookup lane
   static constexpr int MCTA = 32 * kLW * RPL;     // 1024 (g=4) / 2048 (g=5)
   static constexpr int NTOK = NW * TPW;           // tokens per CTA
   static constexpr int NWP = (NW + 1) / 2;        // 256-B row blocks (word pairs)
