@@ -108,7 +108,7 @@ class BatchPipeline:
         self.torch = torch
         self.W, self.w_scale, self.K, self.N = W, float(w_scale), K, N
         self.dev = torch.device(device)
-        self.ws = ws if ws is not None else v.workspace(self.dev)
+        self.ws = ws  # None: the binding's workspace of the stream each mpGeMM runs on
         self.plan = plan
         self.side = torch.cuda.Stream(self.dev)
         self.q = [torch.empty((K, N), dtype=torch.int8, device=self.dev) for _ in range(2)]
@@ -133,8 +133,9 @@ class BatchPipeline:
             v.quantize(x, q=self.q[b], scale=self.sc[b], stream=self.side, cluster=1)
             self.ev_q[b].record(self.side)
         cs.wait_event(self.ev_q[b])
+        ws = self.ws if self.ws is not None else v.workspace(self.dev, cs)
         v.mpgemm_ws(W if W is not None else self.W, self.q[b], self.sc[b], self.w_scale, out=out,
-                    ws=self.ws, plan=self.plan, stream=cs)
+                    ws=ws, plan=self.plan, stream=cs)
         self.ev_k[b].record(cs)
         self.i += 1
 
