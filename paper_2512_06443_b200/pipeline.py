@@ -108,7 +108,9 @@ class BatchPipeline:
         self.torch = torch
         self.W, self.w_scale, self.K, self.N = W, float(w_scale), K, N
         self.dev = torch.device(device)
-        self.ws = ws  # None: the binding's workspace of the stream each mpGeMM runs on
+        # one workspace (allocated here, outside any graph capture); the
+        # mpGeMMs are chained by events, so it is never used by two at once
+        self.ws = ws if ws is not None else v.workspace(self.dev)
         self.plan = plan
         self.side = torch.cuda.Stream(self.dev)
         self.q = [torch.empty((K, N), dtype=torch.int8, device=self.dev) for _ in range(2)]
@@ -133,9 +135,10 @@ class BatchPipeline:
             v.quantize(x, q=self.q[b], scale=self.sc[b], stream=self.side, cluster=1)
             self.ev_q[b].record(self.side)
         cs.wait_event(self.ev_q[b])
-        ws = self.ws if self.ws is not None else v.workspace(self.dev, cs)
+        if self.i >= 1:
+            cs.wait_event(self.ev_k[1 - b])  # the previous mpGeMM (same workspace), any stream
         v.mpgemm_ws(W if W is not None else self.W, self.q[b], self.sc[b], self.w_scale, out=out,
-                    ws=ws, plan=self.plan, stream=cs)
+                    ws=self.ws, plan=self.plan, stream=cs)
         self.ev_k[b].record(cs)
         self.i += 1
 
