@@ -54,9 +54,13 @@ struct Cfg32 {
 #ifndef VLUT_K32_NBUF
 #define VLUT_K32_NBUF 3
 #endif
-  // table buffers (the stream-K variant keeps 2: its index tiles hold up to
-  // 1536 rows)
-  static constexpr int NBUF = (G == 4 && !SK) ? VLUT_K32_NBUF : 2;
+  // table buffers: K1-32 VLUT_K32_NBUF; the stream-K variant (index tiles of
+  // up to 1536 rows) 3 at g = 4 (measured 0.2-1.1 % faster than 2,
+  // profiles/r02_sk32_fixup.txt) and 2 at g = 5 (243-row pair tables)
+#ifndef VLUT_SK32_NBUF4
+#define VLUT_SK32_NBUF4 3
+#endif
+  static constexpr int NBUF = (G == 4 && !SK) ? VLUT_K32_NBUF : (G == 4 ? VLUT_SK32_NBUF4 : 2);
   static constexpr int GS = (G == 4) ? 16 : 8;      // groups per sub-stage (even)
   static constexpr int PAIRS = GS / 2;
   static constexpr int SUBS = kKgTile / GS;
