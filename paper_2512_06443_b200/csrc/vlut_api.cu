@@ -516,7 +516,11 @@ double plan_sk32(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
   // us; profiles/r02_sk32_plan_r1.txt), so g = 4 plans 12 x 2 only
   const int warps_opts[2] = {12, 12};
   const int rpt_opts[2] = {2, 1};
-  const int n_opts = (g == 5) ? 2 : 1;
+  // end of round 2: with the fp32 split-tile meeting 12 x 1 also wins at
+  // g = 4 once K is long (config 4 N = 64 99.3 -> 92.7 us, config 5 down
+  // N = 128 62.5 -> 56.2 us); at K = 2560 (40 K-tiles) it still loses to the
+  // cluster K1-32 at N = 80 / 96 (profiles/r02_planner_ab.txt)
+  const int n_opts = (g == 5 || kgt >= 64) ? 2 : 1;
   for (int wi = 0; wi < n_opts; ++wi) {
     const int warps = warps_opts[wi], rpt = rpt_opts[wi];
     if (smem_bytes_sk32(g, warps, rpt) > 232448) continue;  // 227 KB opt-in per CTA
@@ -528,7 +532,13 @@ double plan_sk32(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
     double cost = units * VLUT_KG_TILE * 0.5 * ((double)mcta * VLUT_SK32_FACTOR + half_rows);
     cost += 4000.0 + 16.0 * mcta;
     const double per_tile = (double)grid / (double)(MT * NT);
-    if (per_tile > 1.0) cost += (per_tile - 1.0) * (double)mcta * 128.0 / 16.0;
+    // the owner's fixup: one producer's rows per L2 round trip with int32
+    // partials; with the fp32 meeting (fewer tiles than CTAs, K * 128 <
+    // 2^24) producers reduce in L2 and the owner reads one slot
+    double fix = per_tile - 1.0;
+    const bool f32_meet = (long long)K * 128 < (1LL << 24) && MT * NT < grid;
+    if (f32_meet && !getenv("VLUT_SK32_MODEL_OLD") && fix > 1.0) fix = 1.0;
+    if (per_tile > 1.0) cost += fix * (double)mcta * 128.0 / 16.0;
     if (cost < best_cost * 0.995) {
       best_cost = cost;
       best->warps = warps;
