@@ -233,7 +233,9 @@ vlut_status vlut_mpgemm_ex(const vlut_packed_weights* W, const int8_t* A,
                integer-valued partials, exact below 2^24; the tile's owner
                reads and re-zeroes them in the same launch).
  *               No host-side per-launch state: captured CUDA graphs may be
- *               replayed.  Stream-K and K2 split-K launches whose CTAs
+ *               replayed.  A launch that fails asynchronously can leave the
+ *               zero-kept regions dirty: re-zero the workspace before reusing
+ *               it after any CUDA error.  Stream-K and K2 split-K launches whose CTAs
  *               wait for each other are cooperative (all co-resident);
  *               K2's decode-size tiles meet without waiting and are not.
  * vlut_workspace_bytes() returns 0 without a CUDA device (~60 MB on B200).
