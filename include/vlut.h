@@ -229,9 +229,9 @@ vlut_status vlut_mpgemm_ex(const vlut_packed_weights* W, const int8_t* A,
  *               count << 40 | biased sum; every K2 launch leaves them zero
  *               again) and
  *               per-tile generation words (monotonic, read on the device),
-               and K1-32-SK fp32 split-tile accumulators (producers red.add
-               integer-valued partials, exact below 2^24; the tile's owner
-               reads and re-zeroes them in the same launch).
+ *               and K1-32-SK fp32 split-tile accumulators (producers red.add
+ *               integer-valued partials, exact below 2^24; the tile's owner
+ *               reads and re-zeroes them in the same launch).
  *               No host-side per-launch state: captured CUDA graphs may be
  *               replayed.  A launch that fails asynchronously can leave the
  *               zero-kept regions dirty: re-zero the workspace before reusing
