@@ -536,7 +536,7 @@ double plan_sk32(int M, int K, int N, int g, int sms, vlut_launch_plan* best) {
     // partials; with the fp32 meeting (fewer tiles than CTAs, K * 128 <
     // 2^24) producers reduce in L2 and the owner reads one slot
     double fix = per_tile - 1.0;
-    const bool f32_meet = (long long)K * 128 < (1LL << 24) && MT * NT < grid;
+    const bool f32_meet = (long long)K * 128 < (1LL << 24) && 2 * MT * NT <= grid;
     if (f32_meet && !getenv("VLUT_SK32_MODEL_OLD") && fix > 1.0) fix = 1.0;
     if (per_tile > 1.0) cost += fix * (double)mcta * 128.0 / 16.0;
     if (cost < best_cost * 0.995) {
@@ -1105,11 +1105,12 @@ vlut_status run_mpgemm(const vlut_packed_weights* W, const int8_t* A, const floa
       if (gx > 0 && gx < grid) grid = gx;
     }
     // K1-32-SK: split tiles meet in fp32 accumulators (exact while every
-    // partial sum stays below 2^24) when there are fewer tiles than CTAs --
-    // several producers per tile, whose reads would chain in the owner's
-    // fixup; with more tiles (<= 1 producer per tile) the int32 partial
-    // stores are cheaper than the L2 reductions (profiles/r02_sk32_fixup.txt)
-    const bool acc_f32 = sk32 && (long long)K * 128 < (1LL << 24) && MT * NT < grid &&
+    // partial sum stays below 2^24) when there are at least two CTAs per
+    // tile -- several producers per tile, whose reads would chain in the
+    // owner's fixup; with ~1 producer per tile the int32 partial stores are
+    // cheaper than the L2 reductions (6912 x 2560 N = 512, 144 tiles: 154.7
+    // vs 158.5 us; profiles/r02_sk32_fixup.txt)
+    const bool acc_f32 = sk32 && (long long)K * 128 < (1LL << 24) && 2 * MT * NT <= grid &&
                          !getenv("VLUT_SK32_INT_PARTIALS");
     sk.acc = acc_f32 ? reinterpret_cast<float*>(static_cast<char*>(ws) + sk32_acc_off(d.sms)) : nullptr;
     if (sk32)

@@ -559,11 +559,13 @@ def test_streamk32_acc_and_fp32(v, M, K, N, g, warps, rpt):
         check_fp32(out.cpu().numpy(), ref, s, synth.W_SCALE)
 
 
-@pytest.mark.parametrize("M,K,N,g,rpt", [(3072, 23040, 256, 5, 2), (3072, 4600, 512, 5, 1),
+@pytest.mark.parametrize("M,K,N,g,rpt", [(3072, 23040, 256, 5, 2), (3072, 4600, 64, 5, 1),
+                                         (3072, 4600, 512, 5, 1),
                                          (700, 2560, 96, 4, 2), (128, 140000, 32, 4, 1)])
 def test_streamk32_split_meeting_repeated_launches(v, M, K, N, g, rpt):
-    """K1-32-SK split tiles meet in fp32 accumulators (exact: every partial
-    sum is an integer below 2^24; K >= 131072 keeps the int32 partials):
+    """K1-32-SK split tiles meet in fp32 accumulators when there are >= 2
+    CTAs per tile (exact: every partial sum is an integer below 2^24; fewer
+    CTAs per tile or K >= 131072 keep the int32 partials):
     three launches on one workspace with new activations stay bit-exact, and
     the accumulator region is all zero again after each launch."""
     W = synth.ternary_weights(M, K, seed=M + 3)
