@@ -12,7 +12,10 @@ from decode_bench import bench  # noqa: E402
 R_LU = 148 * 64 * 1965e6
 dev = torch.device("cuda")
 ws = v.workspace(dev)
-for (M, K, N, g) in [(6912, 2560, 256, 4), (6912, 2560, 512, 4), (3840, 2560, 2048, 4)]:
+SHAPES = [(6912, 2560, 256, 4), (6912, 2560, 512, 4), (3840, 2560, 2048, 4)]
+if os.environ.get("PROBE_SHAPES"):  # "M,K,N,g;M,K,N,g"
+    SHAPES = [tuple(int(x) for x in t.split(",")) for t in os.environ["PROBE_SHAPES"].split(";")]
+for (M, K, N, g) in SHAPES:
     W = torch.from_numpy(synth.ternary_weights(M, K, 1, 0.4)).to(dev)
     pw0 = v.pack_weights_device(W, g)
     copies = int(min(96, max(2, -(-300_000_000 // pw0.nbytes))))
@@ -23,7 +26,7 @@ for (M, K, N, g) in [(6912, 2560, 256, 4), (6912, 2560, 512, 4), (3840, 2560, 20
     lk = M * (K // g) * N
     for name, pl in [("auto", None), ("sk32 12x1", v.LaunchPlan(12, 1, m_cta=384, n_cta=32, streamk=1)),
                      ("sk32 12x2", v.LaunchPlan(12, 1, m_cta=768, n_cta=32, streamk=1))]:
-        for envv in ("", "1"):
+        for envv in ("",) if os.environ.get("PROBE_SHAPES") else ("", "1"):
             if envv:
                 os.environ["VLUT_SK32_INT_PARTIALS"] = "1"
             else:
